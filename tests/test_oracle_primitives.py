@@ -1,0 +1,309 @@
+"""Pins of the oracle's relaxation primitives, MatrixInv and blends against what the paper
+and mathematics fix (not against the oracle itself).  CPU only."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def rand_form(rng, n, scale=1.0, width=0.5):
+    """Random sound-looking form: lower and upper affine maps with lo <= hi at every vertex
+    is not required by the primitives; we build hi = lo + nonneg slack + slope noise."""
+    lA = rng.normal(0, scale, n)
+    lb = rng.normal(0, scale)
+    uA = lA + rng.normal(0, width * scale, n) * (rng.uniform() < 0.7)
+    ub = lb + abs(rng.normal(0, width * scale)) + np.abs(uA - lA).sum()
+    return np.concatenate([lA, [lb], uA, [ub]])
+
+
+def ev(f, n, xi):
+    return f[:n] @ xi + f[n], f[n + 1:2 * n + 1] @ xi + f[2 * n + 1]
+
+
+# ------------------------------------------------------------------ concretisation
+def test_conc_hand(oracle):
+    # lower 2 xi + 1, upper -3 xi + 4 on xi in [-1,1]: min lower = -1, max upper = 7
+    f = oracle.form([2.0], 1.0, [-3.0], 4.0)
+    assert oracle.form_conc(f, 1) == (-1.0, 7.0)
+    g = oracle.form([1.0, -2.0], 0.5, [0.5, 0.5], 1.0)
+    assert oracle.form_conc(g, 2) == (0.5 - 3.0, 1.0 + 1.0)
+
+
+# ------------------------------------------------------------------ R1 McCormick (G1)
+@pytest.mark.parametrize("n", [1, 3, 6])
+def test_mul_sandwich(oracle, n):
+    """Prop. 1 / Def. 1: for any values y_f in [f_lo(xi), f_hi(xi)] and
+    y_g in [g_lo(xi), g_hi(xi)], mul's planes sandwich y_f * y_g."""
+    rng = np.random.default_rng(10 + n)
+    viol = 0
+    for _ in range(300):
+        f = rand_form(rng, n)
+        g = rand_form(rng, n, scale=rng.uniform(0.1, 3))
+        m = oracle.form_mul(f, g, n)
+        for _ in range(30):
+            xi = rng.uniform(-1, 1, n)
+            fl, fh = ev(f, n, xi)
+            gl, gh = ev(g, n, xi)
+            if fl > fh or gl > gh:
+                continue
+            yf = rng.uniform(fl, fh)
+            yg = rng.uniform(gl, gh)
+            ml, mh = ev(m, n, xi)
+            tol = 1e-9 * (1 + abs(yf * yg))
+            viol += (ml > yf * yg + tol) or (mh < yf * yg - tol)
+    assert viol == 0
+
+
+def test_mul_exact_with_constant(oracle):
+    rng = np.random.default_rng(1)
+    n = 3
+    g = rand_form(rng, n)
+    for c in (2.5, -1.5, 0.0):
+        f = oracle.form(np.zeros(n), c, np.zeros(n), c)
+        m = oracle.form_mul(f, g, n)
+        for xi in rng.uniform(-1, 1, (50, n)):
+            gl, gh = ev(g, n, xi)
+            ml, mh = ev(m, n, xi)
+            want = sorted([c * gl, c * gh])
+            assert abs(ml - want[0]) < 1e-12 and abs(mh - want[1]) < 1e-12
+
+
+def test_mul_mccormick_corners(oracle):
+    """The lower plane comes from (x - x_lo)(y - y_lo) >= 0, so it is exact where x = x_lo
+    or y = y_lo; the upper plane from (x - x_lo)(y - y_hi) <= 0 is exact where x = x_lo or
+    y = y_hi.  Independent vars x = xi0 in [-1,1], y = 1 + 2 xi1 in [-1,3]."""
+    n = 2
+    x = oracle.form([1, 0], 0.0, [1, 0], 0.0)
+    y = oracle.form([0, 2], 1.0, [0, 2], 1.0)
+    m = oracle.form_mul(x, y, n)
+    for a in (-1.0, 1.0):
+        for b in (-1.0, 1.0):
+            xi = np.array([a, b])
+            ml, mh = ev(m, n, xi)
+            true = a * (1 + 2 * b)
+            assert ml <= true + 1e-15 and mh >= true - 1e-15
+            if a == -1 or b == -1:
+                assert abs(ml - true) < 1e-15
+            if a == -1 or b == 1:
+                assert abs(mh - true) < 1e-15
+    # and is not exact at the opposite corner (x_hi, y_lo) for the upper plane
+    assert ev(m, n, np.array([1.0, -1.0]))[1] > -1 + 1.0
+
+
+# ------------------------------------------------------------------ R2 square (G2)
+@pytest.mark.parametrize("n", [1, 4])
+def test_sq_sandwich_and_tangent(oracle, n):
+    rng = np.random.default_rng(20 + n)
+    for _ in range(300):
+        f = rand_form(rng, n)
+        s = oracle.form_sq(f, n)
+        xl, xh = oracle.form_conc(f, n)
+        for _ in range(30):
+            xi = rng.uniform(-1, 1, n)
+            fl, fh = ev(f, n, xi)
+            y = rng.uniform(fl, fh)
+            sl, sh = ev(s, n, xi)
+            tol = 1e-9 * (1 + y * y)
+            assert sl <= y * y + tol and sh >= y * y - tol
+    # single variable identity form: x in [-1, 2] -> p = 0 tangent (lower = 0),
+    # chord upper = (x_lo + x_hi) x - x_lo x_hi = x + 2
+    f = oracle.form([1.5], 0.5, [1.5], 0.5)
+    s = oracle.form_sq(f, 1)
+    assert np.allclose(s, [0.0, 0.0, 1.5, 2.5])
+    # x in [1, 3] (no sign change): tangent at x_lo = 1: 2x - 1
+    f = oracle.form([1.0], 2.0, [1.0], 2.0)
+    s = oracle.form_sq(f, 1)
+    assert np.allclose(s[:2], [2.0, 3.0])  # 2(xi+2) - 1
+    # constant form is exact
+    c = oracle.form([0.0], -1.7, [0.0], -1.7)
+    assert np.allclose(oracle.form_sq(c, 1), [0, 1.7 ** 2, 0, 1.7 ** 2])
+
+
+# ------------------------------------------------------------------ Table 2
+def test_table2_exp_and_ind(oracle):
+    g = _gold("table2.json")
+    ls, li, hs, hi = oracle.exp_relax(0.0, 1.0)
+    e = g["exp_0_1"]
+    assert math.isclose(ls, e["lo_slope"]) and math.isclose(li, e["lo_icpt"])
+    assert math.isclose(hs, e["hi_slope"]) and math.isclose(hi, e["hi_icpt"])
+    # degenerate interval: tangent == chord == e^c
+    ls, li, hs, hi = oracle.exp_relax(0.3, 0.3)
+    assert math.isclose(ls * 0.3 + li, math.exp(0.3)) and math.isclose(hs * 0.3 + hi, math.exp(0.3))
+    # sandwich on [-3, 2]
+    ls, li, hs, hi = oracle.exp_relax(-3.0, 2.0)
+    xs = np.linspace(-3, 2, 1001)
+    assert np.all(ls * xs + li <= np.exp(xs) + 1e-12) and np.all(hs * xs + hi >= np.exp(xs) - 1e-12)
+    for case in g["ind"]:
+        assert oracle.ind_relax(*case["x"]) == case["out"]
+
+
+# ------------------------------------------------------------------ MatrixInv (Alg. 4)
+def oracle_form_const(n, v):
+    z = np.zeros(n)
+    return np.concatenate([z, [v], z, [v]])
+
+
+def _entry(n, c, r, k):
+    A = np.zeros(n)
+    if r != 0:
+        A[k] = r
+    return np.concatenate([A, [c], A, [c]])
+
+
+def test_example1(oracle):
+    """Example 1 under reading G16: the enclosure contains every inverse in the
+    set, its Frobenius width lies between the empirical width (paper 0.66) and the SPEC
+    acceptance window (<= 0.80; paper's CROWN number 0.70)."""
+    g = _gold("example1.json")
+    lo = np.array(g["X_lo"])
+    hi = np.array(g["X_hi"])
+    c00, r00 = (lo[0, 0] + hi[0, 0]) / 2, (hi[0, 0] - lo[0, 0]) / 2
+    c11, r11 = (lo[1, 1] + hi[1, 1]) / 2, (hi[1, 1] - lo[1, 1]) / 2
+    r01 = hi[0, 1]  # symmetric reading: [-0.02, 0.02]
+    n = 3
+    X = np.stack([_entry(n, c00, r00, 0), _entry(n, 0.0, r01, 2), _entry(n, 0.0, r01, 2),
+                  _entry(n, c11, r11, 1)])
+    st, conic, eps, rho = oracle.matrix_inv(X, n, g["k"])
+    assert st == 0 and 0 < rho < 1
+    L = np.array([oracle.form_conc(conic[e], n)[0] for e in range(4)]).reshape(2, 2)
+    U = np.array([oracle.form_conc(conic[e], n)[1] for e in range(4)]).reshape(2, 2)
+    width = np.linalg.norm(U - L)
+    # empirical width over the set, recomputed here by sampling true inverses
+    rng = np.random.default_rng(0)
+    xs = rng.uniform(-1, 1, (200000, 3))
+    xs[:8] = [[a, b, c] for a in (-1, 1) for b in (-1, 1) for c in (-1, 1)]
+    M = np.empty((len(xs), 2, 2))
+    M[:, 0, 0] = c00 + r00 * xs[:, 0]
+    M[:, 1, 1] = c11 + r11 * xs[:, 1]
+    M[:, 0, 1] = M[:, 1, 0] = r01 * xs[:, 2]
+    inv = np.linalg.inv(M)
+    emp = np.linalg.norm(inv.max(axis=0) - inv.min(axis=0))
+    assert abs(emp - g["width_empirical_paper"]) < 0.01
+    assert np.all(inv >= L - 1e-12) and np.all(inv <= U + 1e-12)  # Lemma 1 containment
+    assert emp <= width <= 0.80
+    assert abs(width - g["width_matrixinv_paper"]) < 0.1  # SPEC.md:531 window
+    assert width < g["width_adjugate_paper"]  # MatrixInv beats the adjugate baseline
+    # Cross-check against the independent survey-time prototype of the same rules
+    # (0.7588 with these L and U).
+    assert abs(width - 0.7588) < 5e-4
+    assert np.allclose(L, [[1.0443, -0.0562], [-0.0585, 0.7315]], atol=6e-5)
+    assert np.allclose(U, [[1.6725, 0.0705], [0.0758, 1.1152]], atol=6e-5)
+
+
+@pytest.mark.parametrize("c,r", [(2.0, 0.5), (1.0, 0.3), (4.0, 0.4)])
+def test_matrixinv_diag_closed_form(oracle, c, r):
+    """X = diag(c + r xi, 1), k = 2, derived by hand from Alg. 4 with R1/R2:
+    X0 = diag(1/c, 1); IXX0 = diag(-rho xi, 0) with rho = r/c; P^2_00 = sq(-rho xi) in
+    [0, rho^2] (tangent at 0, chord); Xp_00 = (1 - rho xi + [0, rho^2]) / c;
+    Eps = sqrt(1/c^2 + 1) rho^3 / (1 - rho)  =>  Conic_00 in
+    [(1 - rho)/c - Eps, (1 + rho + rho^2)/c + Eps] and Conic_11 = [1 - Eps, 1 + Eps]."""
+    n = 1
+    rho = r / c
+    X = np.stack([_entry(n, c, r, 0), oracle_form_const(n, 0.0), oracle_form_const(n, 0.0),
+                  oracle_form_const(n, 1.0)])
+    st, conic, eps, rho_o = oracle.matrix_inv(X, n, 2)
+    assert st == 0
+    assert math.isclose(rho_o, rho, rel_tol=1e-14)
+    E = math.sqrt(1 / c ** 2 + 1) * rho ** 3 / (1 - rho)
+    assert math.isclose(eps, E, rel_tol=1e-12)
+    l00, h00 = oracle.form_conc(conic[0], n)
+    assert math.isclose(l00, (1 - rho) / c - E, rel_tol=1e-12)
+    assert math.isclose(h00, (1 + rho + rho * rho) / c + E, rel_tol=1e-12)
+    l11, h11 = oracle.form_conc(conic[3], n)
+    assert math.isclose(l11, 1 - E, rel_tol=1e-12) and math.isclose(h11, 1 + E, rel_tol=1e-12)
+    # containment of the true inverse 1/(c + r xi)
+    xs = np.linspace(-1, 1, 2001)
+    lo = conic[0][0] * xs + conic[0][1] - 0  # lower form incl. -Eps already
+    hi = conic[0][2] * xs + conic[0][3]
+    true = 1 / (c + r * xs)
+    assert np.all(lo <= true + 1e-14) and np.all(hi >= true - 1e-14)
+
+
+def test_matrixinv_point_and_fail(oracle):
+    n = 1
+    # point input: rho = 0, eps = 0, exact inverse
+    A = np.array([[2.0, 0.3], [0.3, 1.0]])
+    X = np.stack([oracle_form_const(n, v) for v in A.reshape(-1)])
+    st, conic, eps, rho = oracle.matrix_inv(X, n, 8)
+    assert st == 0 and eps == 0 and rho < 1e-15
+    inv = np.linalg.inv(A).reshape(-1)
+    for e in range(4):
+        lo, hi = oracle.form_conc(conic[e], n)
+        assert abs(lo - inv[e]) < 1e-14 and abs(hi - inv[e]) < 1e-14
+    # centre determinant <= 0 -> FAIL(1); contraction violated -> FAIL(2) (Alg. 4 l.2)
+    X = np.stack([oracle_form_const(n, v) for v in (1.0, 2.0, 2.0, 1.0)])
+    assert oracle.matrix_inv(X, n, 8)[0] == 1
+    X = np.stack([_entry(n, 1.0, 1.2, 0), oracle_form_const(n, 0), oracle_form_const(n, 0),
+                  oracle_form_const(n, 1.0)])
+    assert oracle.matrix_inv(X, n, 8)[0] == 2
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 8])
+def test_lemma1_containment(oracle, k):
+    """Lemma 1: the enclosure contains X^{-1} for every X in the set, for
+    random SPD interval inputs with rho up to ~0.9 and small k (where Eps matters)."""
+    rng = np.random.default_rng(100 + k)
+    n = 3
+    checked = 0
+    for _ in range(200):
+        a = rng.uniform(0.5, 3)
+        d = rng.uniform(0.5, 3)
+        b = rng.uniform(-0.4, 0.4) * math.sqrt(a * d)
+        ra, rd, rb = rng.uniform(0, 0.35) * a, rng.uniform(0, 0.35) * d, rng.uniform(0, 0.2) * math.sqrt(a * d)
+        X = np.stack([_entry(n, a, ra, 0), _entry(n, b, rb, 2), _entry(n, b, rb, 2), _entry(n, d, rd, 1)])
+        st, conic, eps, rho = oracle.matrix_inv(X, n, k)
+        if st != 0:
+            continue
+        xs = rng.uniform(-1, 1, (2000, 3))
+        xs[:8] = [[p, q, s] for p in (-1, 1) for q in (-1, 1) for s in (-1, 1)]
+        M = np.empty((len(xs), 2, 2))
+        M[:, 0, 0] = a + ra * xs[:, 0]
+        M[:, 1, 1] = d + rd * xs[:, 1]
+        M[:, 0, 1] = M[:, 1, 0] = b + rb * xs[:, 2]
+        ok = np.linalg.det(M) > 0
+        inv = np.linalg.inv(M[ok]).reshape(-1, 4)
+        for e in range(4):
+            lo = xs[ok] @ conic[e][:n] + conic[e][n]
+            hi = xs[ok] @ conic[e][n + 1:2 * n + 1] + conic[e][2 * n + 1]
+            assert np.all(lo <= inv[:, e] + 1e-10) and np.all(hi >= inv[:, e] - 1e-10)
+        checked += 1
+    assert checked > 100
+
+
+# ------------------------------------------------------------------ blends (Alg. 2 / 3)
+def test_blend_hand_traces(oracle):
+    g = _gold("blend_traces.json")
+    for case in g["cases"]:
+        a, c, d = case["a"], case["c"], case["d"]
+        assert np.allclose(oracle.blend_sort(a, c, d), case["sort"], atol=1e-15)
+        assert np.allclose(oracle.blend_ind(a, c, d, tiebreak=False), case["ind_strict"], atol=1e-15)
+        # G6: the index tie-break makes BlendInd equal stable BlendSort even with ties
+        assert np.allclose(oracle.blend_ind(a, c, d, tiebreak=True), case["sort"], atol=1e-15)
+
+
+def test_lemma2_random(oracle):
+    """Lemma 2: BlendSort == BlendInd for 1000 random inputs, distinct depths;
+    permutation invariance; sum T a <= 1."""
+    rng = np.random.default_rng(7)
+    worst = 0.0
+    for _ in range(1000):
+        N = int(rng.integers(1, 51))
+        a = rng.uniform(0, 1, N)
+        c = rng.uniform(0, 1, (N, 3))
+        d = rng.uniform(0.1, 10, N)
+        ps = oracle.blend_sort(a, c, d)
+        pi = oracle.blend_ind(a, c, d, tiebreak=False)
+        worst = max(worst, np.abs(ps - pi).max())
+        perm = rng.permutation(N)
+        assert np.allclose(oracle.blend_ind(a[perm], c[perm], d[perm]), pi, atol=1e-12)
+        assert np.all(ps <= 1 + 1e-12)
+    assert worst <= 1e-12
