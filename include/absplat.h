@@ -1,0 +1,180 @@
+/* absplat.h -- C ABI of the B200 abstract-rendering library (libabsplat.so).
+ *
+ * Computes, for a Gaussian-splat scene and a box of camera poses / scene parameters, lower
+ * and upper bound images lo <= hi that contain every concrete render GaussianSplat(Sc, C, u)
+ * (Alg. 1) for every scene Sc and camera C in the box (abstract rendering
+ * problem; Theorem 1).  The method is AbstractSplat
+ * (PAPER.md:539-558): Alg. 1 lifted to affine forms, MatrixInv (Alg. 4) at
+ * line 8 and BlendInd (Alg. 3) at line 11, evaluated per image tile and
+ * Gaussian batch, with the readings listed in DESIGN.md §2.
+ *
+ * Conventions (all functions):
+ *   - return an as_status; on error nothing is written to caller outputs and
+ *     as_last_error(ctx) describes the failure;
+ *   - no C++ types or exceptions cross the ABI; all pointers are plain host or device
+ *     pointers as documented per argument; inputs are copied (the library owns its copies),
+ *     outputs are caller-owned;
+ *   - work is enqueued on the context's CUDA stream (as_create); one context per host thread.
+ */
+#ifndef ABSPLAT_H
+#define ABSPLAT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ABSPLAT_VERSION 1
+#define AS_MAX_VARS 9 /* 3 translation + 3 Euler + up to 3 group-shift variables */
+
+typedef struct as_ctx as_ctx; /* opaque; owns all device state */
+
+typedef enum {
+  AS_OK = 0,
+  AS_E_ARG = 1,     /* invalid argument (sizes, ranges, NULL pointers, bad flags) */
+  AS_E_SCENE = 2,   /* scene data invalid (non-finite, chol diagonal <= 0, o or c outside [0,1]) */
+  AS_E_NUMERIC = 3, /* reserved: numerical failure that has no sound fallback */
+  AS_E_CUDA = 4,    /* a CUDA runtime call failed */
+  AS_E_OOM = 5,     /* device allocation failed */
+  AS_E_STATE = 6    /* call order violated (e.g. render before as_load_scene) */
+} as_status;
+
+/* Camera.  Extrinsics as XYZ Euler angles of the camera->world
+ * rotation, R_c2w = Rz(euler[2]) Ry(euler[1]) Rx(euler[0]) (Table 3 caption PAPER.md:624,
+ * reading G9), camera centre t in world; the camera looks along +z_cam; the world->camera
+ * rotation of Alg. 1 line 2 is R = R_c2w^T.  Pixel (x, y) has centre (x + 0.5, y + 0.5). */
+typedef struct {
+  double fx, fy, cx, cy;
+  int32_t W, H;
+  double euler[3];
+  double t[3];
+} as_camera;
+
+/* Pose box B_{eps_t, eps_R}(C0): translation offset in
+ * [t_off - eps_t, t_off + eps_t] per axis (world axes, or the nominal camera axes when
+ * t_frame == 1), Euler offset in [R_off - eps_R, R_off + eps_R].  A zero half-width means the
+ * axis is not perturbed.  parts[k] >= 1 splits axis k into that many equal sub-intervals
+ * (input-set partitioning); parts > 1 on an unperturbed axis is AS_E_ARG.
+ * Axis order: tx, ty, tz, e0, e1, e2. */
+typedef struct {
+  double eps_t[3];
+  double eps_R[3];
+  double t_off[3];
+  double R_off[3];
+  int32_t t_frame;
+  int32_t parts[6];
+} as_pose_box;
+
+/* Scene-parameter box.  All pointers are HOST pointers; data is copied.
+ *   n_groups 0..3 shared mean-shift groups: Gaussian i with group_of[i] = g >= 0 has its mean
+ *   moved by s * dir[g] with s in [shift_lo[g], shift_hi[g]] (one shared variable per group);
+ *   col_lo/col_hi [N][3] (or NULL): colour intervals; op_lo/op_hi [N] (or NULL): opacity
+ *   intervals.  Intervals must satisfy 0 <= lo <= hi <= 1. */
+typedef struct {
+  int32_t n_groups;
+  const int32_t* group_of; /* [N] or NULL if n_groups == 0 */
+  const double* dir;       /* [n_groups][3] */
+  const double* shift_lo;  /* [n_groups] */
+  const double* shift_hi;  /* [n_groups] */
+  int32_t parts[3];        /* partitions per group variable */
+  const float* col_lo;
+  const float* col_hi;
+  const float* op_lo;
+  const float* op_hi;
+} as_scene_box;
+
+/* Counters and per-phase device times of the last render (times in ms, CUDA events). */
+typedef struct {
+  int64_t pairs;           /* sum over (sub-box, tile) of |L_T| (tile-level Gaussian lists) */
+  int64_t active_pairs;    /* (pixel, Gaussian) pairs not culled at the pixel */
+  int64_t uncertain_pairs; /* unordered depth pairs with Ind = '?' */
+  int64_t fails;           /* MatrixInv FAIL Gaussians (summed over sub-boxes) */
+  int64_t straddles;       /* Gaussians whose depth straddles d_min */
+  int64_t dropped;         /* Gaussians entirely behind d_min (or with o_hi <= tau) */
+  int64_t order_violations;/* pairs contradicting the (kappa, index) order (must be 0) */
+  int64_t launches;        /* kernel launches issued (own kernels + CUB calls) */
+  int32_t kmax;            /* max |L_T| */
+  int32_t n_sub;           /* number of sub-boxes */
+  int32_t n_vars;          /* number of box variables n */
+  int32_t n_tiles;         /* tiles rendered by this context */
+  double ms_pose, ms_setup, ms_bin, ms_pairs, ms_tile, ms_total;
+  double tile_kernel_ms;   /* sum of k_tile durations */
+  size_t device_bytes;     /* bytes currently held by the context */
+} as_stats;
+
+/* Flags */
+#define AS_PTR_DEVICE 1 /* pointer arguments are device pointers */
+#define AS_ASYNC 2      /* return without synchronising the stream (device outputs only) */
+
+/* Create a context on CUDA device `device`, enqueueing on `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream). */
+as_status as_create(as_ctx** out, int32_t device, void* cuda_stream);
+as_status as_destroy(as_ctx* ctx);
+const char* as_last_error(const as_ctx* ctx); /* owned by ctx; valid until the next call */
+int32_t as_version(void);
+
+/* Load the scene (Gaussians <uw, Mw, o, c>): mean [N][3], chol [N][6]
+ * (lower-triangular Cholesky factor Mw of Cov = Mw Mw^T, packed m00 m10 m11 m20 m21 m22),
+ * opacity [N] in [0,1], color [N][3] in [0,1]; float32.  Host pointers unless AS_PTR_DEVICE.
+ * Validated: finite, chol diagonal > 0, o and c in [0,1] (AS_E_SCENE otherwise).
+ * Clears any scene box. */
+as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* chol,
+                        const float* opacity, const float* color, int32_t flags);
+as_status as_set_camera(as_ctx* ctx, const as_camera* cam);
+as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box);
+/* Optional scene box (NULL clears).  Must be called after as_load_scene (uses N). */
+as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sbox);
+
+/* Abstract render of the whole image.  tile = TS in {8, 16, 32}; batch = BS, the number of
+ * Gaussians staged in shared memory per step (1..256).  TS and BS are performance knobs
+ * only (reading O1): the bounds do not depend on them.  lo/hi: caller-owned float32
+ * [H][W][3], host pointers unless AS_PTR_DEVICE.  Returns once lo/hi are written unless
+ * AS_ASYNC (device outputs only).  stats may be NULL. */
+as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, float* hi,
+                           int32_t flags, as_stats* stats);
+
+/* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----
+ * Every rank holds the full scene and runs the per-Gaussian setup; image tiles are
+ * assigned to ranks by a deterministic longest-processing-time rule over per-tile Gaussian
+ * counts (identical on every rank), so each rank renders only its own tiles and the bound
+ * images are assembled with one gather.
+ *
+ * as_render_shard: renders the tiles owned by `rank` of `world` into the compact tile-major
+ * buffers lo_tm/hi_tm [max_tiles][tile*tile][3] (device pointers unless flags lack
+ * AS_PTR_DEVICE) and writes their tile ids (ascending) to owned[] (host, int32[max_tiles])
+ * and their number to *n_owned.  max_tiles (identical on every rank) caps the tiles per rank
+ * and must be >= ceil(n_tiles / world), n_tiles = ceil(W/tile)*ceil(H/tile). */
+as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank, int32_t world,
+                          float* lo_tm, float* hi_tm, int32_t max_tiles, int32_t* owned,
+                          int32_t* n_owned, int32_t flags, as_stats* stats);
+/* Assemble gathered tile-major buffers of `world` ranks ([world][max_tiles][tile*tile][3]
+ * floats, with owned ids [world][max_tiles] and counts n_owned[world], host int32 arrays)
+ * into row-major images lo/hi [H][W][3].  Pointer space per AS_PTR_DEVICE (tm and images
+ * alike); with host pointers ctx may be NULL (pure host index arithmetic).  Every tile must be
+ * owned exactly once (AS_E_ARG otherwise). */
+as_status as_untile(as_ctx* ctx, int32_t W, int32_t H, int32_t tile, int32_t world,
+                    int32_t max_tiles, const int32_t* owned, const int32_t* n_owned,
+                    const float* lo_tm, const float* hi_tm, float* lo, float* hi, int32_t flags);
+/* The deterministic owner map used by as_render_shard for the current scene / camera /
+ * box (host int32 [n_tiles]); costs optional (host int64 [n_tiles], per-tile pair counts
+ * summed over sub-boxes).  Runs the setup and counting passes. */
+as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_tiles,
+                         int32_t* owner, int64_t* costs);
+/* Pure host function: longest-processing-time assignment of n_tiles tiles with the given
+ * costs to `world` ranks, at most `cap` tiles per rank (cap >= ceil(n_tiles / world)).
+ * Tiles in descending cost (ties: lower id first) go to the least-loaded rank with room
+ * (ties: lower rank).  owner: int32 [n_tiles]. */
+as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, int32_t cap,
+                        int32_t* owner);
+
+/* Concrete render (Alg. 1 + BlendSort, reading G6/G8) at one point of the box: xi[n] in
+ * [-1,1]^n are the box variables of the FULL box in order (perturbed axes tx,ty,tz,e0,e1,e2,
+ * then group shifts), with the scene's nominal colours and opacities.  img: [H][W][3]
+ * float32, host unless AS_PTR_DEVICE.  Used by soundness tests on large scenes. */
+as_status as_render_concrete(as_ctx* ctx, const double* xi, float* img, int32_t flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1231 @@
+// absplat.cu -- C ABI (include/absplat.h) and host orchestration of the B200 abstract-
+// rendering path: context, device buffers, per-sub-box pipeline (pose -> setup -> depth
+// sort -> bin -> tile sort -> pair classification -> tile kernel), tile sharding (LPT owner
+// map, compact tile-major outputs, untile), and the concrete renderer used by tests.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace absplat;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct Err {
+  as_status st;
+};
+
+}  // namespace
+
+struct as_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // scene
+  int64_t N = -1;
+  DevBuf mean, chol, opacity, color;
+  // scene box
+  int n_groups = 0;
+  double dir[3][3] = {};
+  double shift_lo[3] = {}, shift_hi[3] = {};
+  int gparts[3] = {1, 1, 1};
+  DevBuf group_of, col_lo, col_hi, op_lo, op_hi;
+  bool has_group = false, has_col = false, has_op = false;
+  // camera / box
+  as_camera cam{};
+  as_pose_box box{};
+  bool have_cam = false, have_box = false;
+  // work buffers
+  DevBuf pose, hot, pair, kkey, kkey2, kval, order, counts, offsets, cub_tmp;
+  DevBuf keys, keys2, vals, vals2, tbegin, tend, tcost, tkey, tkey2, tids, tlist, tslot, owner;
+  DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
+  DevBuf img_lo, img_hi, counters, conc_g, untile_map;
+  size_t bytes = 0;
+  int64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+  bool events = false;
+};
+
+namespace {
+
+void set_err(as_ctx* c, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  c->err = buf;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      set_err(ctx, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+              __LINE__);                                                             \
+      throw Err{e_ == cudaErrorMemoryAllocation ? AS_E_OOM : AS_E_CUDA};             \
+    }                                                                                \
+  } while (0)
+
+#define LAUNCHED(ctx, n)                                                                    \
+  do {                                                                                      \
+    (ctx)->launches += (n);                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess) {                                                                \
+      set_err(ctx, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+              __LINE__);                                                                    \
+      throw Err{AS_E_CUDA};                                                                 \
+    }                                                                                       \
+  } while (0)
+
+void ensure(as_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return;
+  if (b.p) {
+    CK(cudaFree(b.p));
+    ctx->bytes -= b.cap;
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t want = bytes + bytes / 4;
+  CK(cudaMalloc(&b.p, want));
+  b.cap = want;
+  ctx->bytes += want;
+}
+void release(as_ctx* ctx, DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  ctx->bytes -= b.cap;
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+template <typename T>
+T* P(DevBuf& b) {
+  return reinterpret_cast<T*>(b.p);
+}
+
+size_t hot_size(int nv) {
+  switch (nv) {
+#define CASE(K) \
+  case K:       \
+    return sizeof(HotRec<K>);
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
+#undef CASE
+  }
+  return 0;
+}
+size_t pair_size(int nv) { return sizeof(double) * (2 * (nv + 1) + 2); }
+
+bool finite_f(float v) { return std::isfinite(v); }
+
+// ---------------------------------------------------------------- box (a0)
+struct BoxInfo {
+  BoxParams bp;
+  int n_sub;
+  int n_vars;
+  // full-box variables (for as_render_concrete)
+  int axis[NVMAX];
+  double c[NVMAX], r[NVMAX];
+};
+
+as_status make_box(as_ctx* ctx, BoxInfo& bi) {
+  BoxParams& bp = bi.bp;
+  std::memset(&bp, 0, sizeof bp);
+  const as_pose_box& b = ctx->box;
+  for (int a = 0; a < 3; ++a) {
+    if (!(b.eps_t[a] >= 0) || !(b.eps_R[a] >= 0) || !std::isfinite(b.eps_t[a]) ||
+        !std::isfinite(b.eps_R[a]) || !std::isfinite(b.t_off[a]) || !std::isfinite(b.R_off[a])) {
+      set_err(ctx, "pose box: half-widths must be finite and >= 0");
+      return AS_E_ARG;
+    }
+    bp.lo[a] = b.t_off[a] - b.eps_t[a];
+    bp.hi[a] = b.t_off[a] + b.eps_t[a];
+    bp.lo[3 + a] = b.R_off[a] - b.eps_R[a];
+    bp.hi[3 + a] = b.R_off[a] + b.eps_R[a];
+    bp.parts[a] = b.parts[a];
+    bp.parts[3 + a] = b.parts[3 + a];
+  }
+  for (int g = 0; g < 3; ++g) {
+    if (g < ctx->n_groups) {
+      bp.lo[6 + g] = ctx->shift_lo[g];
+      bp.hi[6 + g] = ctx->shift_hi[g];
+      bp.parts[6 + g] = ctx->gparts[g];
+      for (int k = 0; k < 3; ++k) bp.dir[g][k] = ctx->dir[g][k];
+    } else {
+      bp.lo[6 + g] = bp.hi[6 + g] = 0.0;
+      bp.parts[6 + g] = 1;
+    }
+  }
+  long long nsub = 1;
+  int nv = 0;
+  for (int a = 0; a < 9; ++a) {
+    if (bp.parts[a] < 1) {
+      set_err(ctx, "parts must be >= 1");
+      return AS_E_ARG;
+    }
+    const bool var = bp.hi[a] > bp.lo[a];
+    if (!var && bp.parts[a] != 1) {
+      set_err(ctx, "parts > 1 on an unperturbed axis %d", a);
+      return AS_E_ARG;
+    }
+    if (var) {
+      bi.axis[nv] = a;
+      bi.c[nv] = 0.5 * (bp.lo[a] + bp.hi[a]);
+      bi.r[nv] = 0.5 * (bp.hi[a] - bp.lo[a]);
+      ++nv;
+    }
+    nsub *= bp.parts[a];
+  }
+  if (nsub > 1000000) {
+    set_err(ctx, "too many sub-boxes (%lld)", nsub);
+    return AS_E_ARG;
+  }
+  bp.n_sub = (int)nsub;
+  bp.t_frame = b.t_frame;
+  for (int k = 0; k < 3; ++k) {
+    bp.euler0[k] = ctx->cam.euler[k];
+    bp.t0[k] = ctx->cam.t[k];
+  }
+  bi.n_sub = (int)nsub;
+  bi.n_vars = nv;
+  return AS_OK;
+}
+
+struct Geometry {
+  int ts, ntx, nty, ntiles;
+};
+
+// ---------------------------------------------------------------- per sub-box pipeline
+struct SubResult {
+  int64_t pairs = 0;
+  int kmax = 0;
+};
+
+void run_setup(as_ctx* ctx, const BoxInfo& bi, int s) {
+  SetupArgs a{};
+  a.mean = P<float>(ctx->mean);
+  a.chol = P<float>(ctx->chol);
+  a.opacity = P<float>(ctx->opacity);
+  a.color = P<float>(ctx->color);
+  a.group_of = ctx->has_group ? P<int32_t>(ctx->group_of) : nullptr;
+  a.col_lo = ctx->has_col ? P<float>(ctx->col_lo) : nullptr;
+  a.col_hi = ctx->has_col ? P<float>(ctx->col_hi) : nullptr;
+  a.op_lo = ctx->has_op ? P<float>(ctx->op_lo) : nullptr;
+  a.op_hi = ctx->has_op ? P<float>(ctx->op_hi) : nullptr;
+  a.N = ctx->N;
+  a.fx = ctx->cam.fx;
+  a.fy = ctx->cam.fy;
+  a.cx = ctx->cam.cx;
+  a.cy = ctx->cam.cy;
+  for (int g = 0; g < 3; ++g)
+    for (int k = 0; k < 3; ++k) a.dir[g][k] = ctx->dir[g][k];
+  a.pose = P<PoseDev>(ctx->pose) + s;
+  a.hot = ctx->hot.p;
+  a.pair = ctx->pair.p;
+  a.kkey = P<unsigned long long>(ctx->kkey);
+  a.kval = P<int32_t>(ctx->kval);
+  a.wsmax = P<unsigned long long>(ctx->counters) + 4;
+  a.counters = P<unsigned long long>(ctx->counters);
+  launch_setup(bi.n_vars, a, ctx->stream);
+  LAUNCHED(ctx, 1);
+}
+
+void cub_sort_keys64(as_ctx* ctx, unsigned long long* kin, unsigned long long* kout,
+                     int32_t* vin, int32_t* vout, int64_t n, int end_bit) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                  ctx->stream);
+  ensure(ctx, ctx->cub_tmp, tmp);
+  CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, kin, kout, vin, vout, (int)n, 0,
+                                     end_bit, ctx->stream));
+  LAUNCHED(ctx, 1);
+}
+void cub_sort_keys32(as_ctx* ctx, uint32_t* kin, uint32_t* kout, int32_t* vin, int32_t* vout,
+                     int64_t n, int end_bit, bool descending) {
+  size_t tmp = 0;
+  if (descending)
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, kin, kout, vin, vout, (int)n, 0,
+                                              end_bit, ctx->stream);
+  else
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                    ctx->stream);
+  ensure(ctx, ctx->cub_tmp, tmp);
+  if (descending)
+    CK(cub::DeviceRadixSort::SortPairsDescending(ctx->cub_tmp.p, tmp, kin, kout, vin, vout,
+                                                 (int)n, 0, end_bit, ctx->stream));
+  else
+    CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, kin, kout, vin, vout, (int)n, 0,
+                                       end_bit, ctx->stream));
+  LAUNCHED(ctx, 1);
+}
+template <typename TI, typename TO>
+void cub_exclusive_sum(as_ctx* ctx, TI* in, TO* out, int64_t n) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, ctx->stream);
+  ensure(ctx, ctx->cub_tmp, tmp);
+  CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, in, out, (int)n, ctx->stream));
+  LAUNCHED(ctx, 1);
+}
+template <typename T>
+void cub_inclusive_sum(as_ctx* ctx, T* in, T* out, int64_t n) {
+  size_t tmp = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, (int)n, ctx->stream);
+  ensure(ctx, ctx->cub_tmp, tmp);
+  CK(cub::DeviceScan::InclusiveSum(ctx->cub_tmp.p, tmp, in, out, (int)n, ctx->stream));
+  LAUNCHED(ctx, 1);
+}
+
+int bits_for(int64_t v) {
+  int b = 1;
+  while ((1ll << b) <= v) ++b;
+  return b;
+}
+
+__global__ void k_seq(int32_t* v, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+__global__ void k_tile_keys(const int32_t* list, int n, const int64_t* tb, const int64_t* te,
+                            uint32_t* key) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int t = list[i];
+    const int64_t k = te[t] - tb[t];
+    key[i] = (uint32_t)(k > 0x7fffffff ? 0x7fffffff : k);
+  }
+}
+__global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned long long* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int64_t k = te[i] - tb[i];
+    if (k > 0) atomicMax(out, (unsigned long long)k);
+  }
+}
+__global__ void k_slot_map(const int32_t* list, int n, int32_t* slot_of_tile) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) slot_of_tile[list[i]] = i;
+}
+
+// counters layout (unsigned long long[16])
+enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6, C_UNC = 8,
+       C_VIOL = 9, C_NCOUNTERS = 16 };
+
+int64_t read_i64(as_ctx* ctx, const int64_t* dptr) {
+  int64_t v = 0;
+  CK(cudaMemcpyAsync(&v, dptr, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return v;
+}
+
+struct PhaseTimes {
+  double setup = 0, bin = 0, pairs = 0, tile = 0;
+};
+
+// Render one sub-box (rows a2-a10) into row-major (tslot == nullptr) or compact tile-major
+// outputs.  tlist: device list of n_list tiles to render; owner: device owner map or null.
+void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const Geometry& G,
+                   int bs, const int32_t* owner, int rank, const int32_t* tlist, int n_list,
+                   const int32_t* tslot, float* lo, float* hi, bool first, int64_t& pairs_out,
+                   PhaseTimes* pt) {
+  cudaStream_t st = ctx->stream;
+  const int64_t N = ctx->N;
+  const int nv = bi.n_vars;
+  unsigned long long* ctr = P<unsigned long long>(ctx->counters);
+  if (pt) CK(cudaEventRecord(ctx->ev[1], st));
+  if (do_setup) {
+    CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
+    run_setup(ctx, bi, s);
+  }
+  if (pt) CK(cudaEventRecord(ctx->ev[2], st));
+  // ---- a6: depth order (stable radix sort by kappa: ties keep ascending index, G6)
+  cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
+                  P<int32_t>(ctx->kval), P<int32_t>(ctx->order), N, 64);
+  // ---- a6: count overlapped tiles per Gaussian, scan, emit in depth order
+  BinArgs ba{};
+  ba.order = P<int32_t>(ctx->order);
+  ba.N = N;
+  ba.hot = ctx->hot.p;
+  ba.nv = nv;
+  ba.ts = G.ts;
+  ba.ntx = G.ntx;
+  ba.nty = G.nty;
+  ba.W = ctx->cam.W;
+  ba.H = ctx->cam.H;
+  ba.owner = owner;
+  ba.rank = rank;
+  ba.counts = P<int64_t>(ctx->counts);
+  ba.offsets = P<int64_t>(ctx->offsets);
+  ba.tile_cost = nullptr;
+  CK(cudaMemsetAsync(ba.counts + N, 0, sizeof(int64_t), st));
+  launch_count(ba, st);
+  LAUNCHED(ctx, 1);
+  cub_exclusive_sum(ctx, ba.counts, P<int64_t>(ctx->offsets), N + 1);
+  const int64_t M = read_i64(ctx, P<int64_t>(ctx->offsets) + N);
+  pairs_out = M;
+  ensure(ctx, ctx->keys, sizeof(uint32_t) * (M + 1));
+  ensure(ctx, ctx->keys2, sizeof(uint32_t) * (M + 1));
+  ensure(ctx, ctx->vals, sizeof(int32_t) * (M + 1));
+  ensure(ctx, ctx->vals2, sizeof(int32_t) * (M + 1));
+  ba.keys = P<uint32_t>(ctx->keys);
+  ba.vals = P<int32_t>(ctx->vals);
+  launch_emit(ba, st);
+  LAUNCHED(ctx, 1);
+  // stable sort by tile id: within a tile the depth order of emission is kept
+  if (M > 0)
+    cub_sort_keys32(ctx, P<uint32_t>(ctx->keys), P<uint32_t>(ctx->keys2), P<int32_t>(ctx->vals),
+                    P<int32_t>(ctx->vals2), M, bits_for(G.ntiles), false);
+  const uint32_t* skeys = P<uint32_t>(ctx->keys2);
+  const int32_t* svals = P<int32_t>(ctx->vals2);
+  launch_ranges(skeys, M, G.ntiles, P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), st);
+  LAUNCHED(ctx, 1);
+  k_tile_max<<<(G.ntiles + 255) / 256, 256, 0, st>>>(P<int64_t>(ctx->tbegin),
+                                                     P<int64_t>(ctx->tend), G.ntiles, ctr + C_KMAX);
+  LAUNCHED(ctx, 1);
+  if (pt) CK(cudaEventRecord(ctx->ev[3], st));
+  // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
+  TileArgs ta{};
+  ta.pflag = nullptr;
+  if (nv > 0 && M > 0) {
+    ensure(ctx, ctx->nF, sizeof(int32_t) * M);
+    ensure(ctx, ctx->nG, sizeof(int32_t) * M);
+    ensure(ctx, ctx->ntot, sizeof(int64_t) * (M + 1));
+    ensure(ctx, ctx->eoff, sizeof(int64_t) * (M + 1));
+    PairArgs pa{};
+    pa.keys = skeys;
+    pa.vals = svals;
+    pa.tbegin = P<int64_t>(ctx->tbegin);
+    pa.tend = P<int64_t>(ctx->tend);
+    pa.M = M;
+    pa.pair = ctx->pair.p;
+    pa.wsmax = ctr + C_WSMAX;
+    pa.nv = nv;
+    pa.nF = P<int32_t>(ctx->nF);
+    pa.nG = P<int32_t>(ctx->nG);
+    pa.ntot = P<int64_t>(ctx->ntot);
+    pa.counters = ctr + C_UNC;
+    CK(cudaMemsetAsync(pa.ntot + M, 0, sizeof(int64_t), st));
+    launch_pairs_count(pa, st);
+    LAUNCHED(ctx, 1);
+    cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
+    const int64_t nexc = read_i64(ctx, P<int64_t>(ctx->eoff) + M);
+    if (nexc > 0) {
+      pa.off = P<int64_t>(ctx->eoff);
+      ensure(ctx, ctx->exc, sizeof(int32_t) * nexc);
+      ensure(ctx, ctx->hpos, sizeof(int32_t) * M);
+      ensure(ctx, ctx->diff, sizeof(int32_t) * (M + 1));
+      ensure(ctx, ctx->cover, sizeof(int32_t) * (M + 1));
+      ensure(ctx, ctx->pflag, sizeof(int32_t) * M);
+      ensure(ctx, ctx->is_store, sizeof(int32_t) * (M + 1));
+      ensure(ctx, ctx->slot, sizeof(int32_t) * (M + 1));
+      pa.exc = P<int32_t>(ctx->exc);
+      pa.hpos = P<int32_t>(ctx->hpos);
+      launch_pairs_fill(pa, st);
+      LAUNCHED(ctx, 1);
+      CK(cudaMemsetAsync(ctx->diff.p, 0, sizeof(int32_t) * (M + 1), st));
+      launch_mark(pa, P<int32_t>(ctx->diff), st);
+      LAUNCHED(ctx, 1);
+      cub_inclusive_sum(ctx, P<int32_t>(ctx->diff), P<int32_t>(ctx->cover), M + 1);
+      CK(cudaMemsetAsync(P<int32_t>(ctx->is_store) + M, 0, sizeof(int32_t), st));
+      launch_flags(pa, P<int32_t>(ctx->cover), P<int32_t>(ctx->pflag), P<int32_t>(ctx->is_store),
+                   st);
+      LAUNCHED(ctx, 1);
+      cub_exclusive_sum(ctx, P<int32_t>(ctx->is_store), P<int32_t>(ctx->slot), M + 1);
+      int32_t nslots = 0;
+      CK(cudaMemcpyAsync(&nslots, P<int32_t>(ctx->slot) + M, sizeof nslots,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ensure(ctx, ctx->scratch, sizeof(float4) * (size_t)std::max(nslots, 1) * G.ts * G.ts);
+      ta.pflag = P<int32_t>(ctx->pflag);
+      ta.slot = P<int32_t>(ctx->slot);
+      ta.eoff = P<int64_t>(ctx->eoff);
+      ta.nF = P<int32_t>(ctx->nF);
+      ta.nG = P<int32_t>(ctx->nG);
+      ta.exc = P<int32_t>(ctx->exc);
+      ta.hpos = P<int32_t>(ctx->hpos);
+      ta.scratch = P<float4>(ctx->scratch);
+    }
+  }
+  if (pt) CK(cudaEventRecord(ctx->ev[4], st));
+  // ---- tile order: descending Gaussian count (longest tiles first)
+  k_tile_keys<<<(n_list + 255) / 256, 256, 0, st>>>(tlist, n_list, P<int64_t>(ctx->tbegin),
+                                                    P<int64_t>(ctx->tend), P<uint32_t>(ctx->tkey));
+  LAUNCHED(ctx, 1);
+  cub_sort_keys32(ctx, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tkey2),
+                  const_cast<int32_t*>(tlist), P<int32_t>(ctx->tids), n_list, 32, true);
+  // ---- a8-a10: the tile kernel
+  ta.hot = ctx->hot.p;
+  ta.vals = svals;
+  ta.tbegin = P<int64_t>(ctx->tbegin);
+  ta.tend = P<int64_t>(ctx->tend);
+  ta.tile_list = P<int32_t>(ctx->tids);
+  ta.tile_slot = tslot;
+  ta.n_list = n_list;
+  ta.ts = G.ts;
+  ta.ntx = G.ntx;
+  ta.W = ctx->cam.W;
+  ta.H = ctx->cam.H;
+  ta.bs = bs;
+  ta.first = first ? 1 : 0;
+  ta.ntau = (float)((double)N * TAU);
+  ta.lo = lo;
+  ta.hi = hi;
+  ta.active = ctr + C_ACTIVE;
+  launch_tile(nv, ta, st);
+  LAUNCHED(ctx, 1);
+  if (pt) {
+    CK(cudaEventRecord(ctx->ev[5], st));
+    CK(cudaEventSynchronize(ctx->ev[5]));
+    float a = 0, b = 0, c = 0, d = 0;
+    CK(cudaEventElapsedTime(&a, ctx->ev[1], ctx->ev[2]));
+    CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
+    CK(cudaEventElapsedTime(&c, ctx->ev[3], ctx->ev[4]));
+    CK(cudaEventElapsedTime(&d, ctx->ev[4], ctx->ev[5]));
+    pt->setup += a;
+    pt->bin += b;
+    pt->pairs += c;
+    pt->tile += d;
+  }
+}
+
+as_status check_ready(as_ctx* ctx) {
+  if (!ctx) return AS_E_ARG;
+  if (ctx->N < 0) {
+    set_err(ctx, "no scene loaded (as_load_scene)");
+    return AS_E_STATE;
+  }
+  if (!ctx->have_cam) {
+    set_err(ctx, "no camera (as_set_camera)");
+    return AS_E_STATE;
+  }
+  if (!ctx->have_box) {
+    set_err(ctx, "no pose box (as_set_pose_box)");
+    return AS_E_STATE;
+  }
+  return AS_OK;
+}
+
+as_status check_tile_args(as_ctx* ctx, int tile, int batch, int nv) {
+  if (tile != 8 && tile != 16 && tile != 32) {
+    set_err(ctx, "tile must be 8, 16 or 32 (got %d)", tile);
+    return AS_E_ARG;
+  }
+  if (batch < 1 || batch > 256) {
+    set_err(ctx, "batch must be in [1, 256] (got %d)", batch);
+    return AS_E_ARG;
+  }
+  if (tile_smem_bytes(nv, tile, batch) > 200 * 1024) {
+    set_err(ctx, "batch %d too large for shared memory at n=%d, tile=%d", batch, nv, tile);
+    return AS_E_ARG;
+  }
+  return AS_OK;
+}
+
+void prepare_common(as_ctx* ctx, const BoxInfo& bi, const Geometry& G) {
+  const int64_t N = ctx->N;
+  const int nv = bi.n_vars;
+  ensure(ctx, ctx->hot, hot_size(nv) * (size_t)std::max<int64_t>(N, 1));
+  ensure(ctx, ctx->pair, pair_size(nv) * (size_t)std::max<int64_t>(N, 1));
+  ensure(ctx, ctx->kkey, sizeof(unsigned long long) * (N + 1));
+  ensure(ctx, ctx->kkey2, sizeof(unsigned long long) * (N + 1));
+  ensure(ctx, ctx->kval, sizeof(int32_t) * (N + 1));
+  ensure(ctx, ctx->order, sizeof(int32_t) * (N + 1));
+  ensure(ctx, ctx->counts, sizeof(int64_t) * (N + 1));
+  ensure(ctx, ctx->offsets, sizeof(int64_t) * (N + 1));
+  ensure(ctx, ctx->counters, sizeof(unsigned long long) * C_NCOUNTERS);
+  ensure(ctx, ctx->pose, sizeof(PoseDev) * bi.n_sub);
+  ensure(ctx, ctx->tbegin, sizeof(int64_t) * G.ntiles);
+  ensure(ctx, ctx->tend, sizeof(int64_t) * G.ntiles);
+  ensure(ctx, ctx->tcost, sizeof(unsigned long long) * G.ntiles);
+  ensure(ctx, ctx->tkey, sizeof(uint32_t) * G.ntiles);
+  ensure(ctx, ctx->tkey2, sizeof(uint32_t) * G.ntiles);
+  ensure(ctx, ctx->tids, sizeof(int32_t) * G.ntiles);
+  ensure(ctx, ctx->tlist, sizeof(int32_t) * G.ntiles);
+  ensure(ctx, ctx->tslot, sizeof(int32_t) * G.ntiles);
+  ensure(ctx, ctx->owner, sizeof(int32_t) * G.ntiles);
+  CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, ctx->stream));
+  launch_pose(bi.bp, P<PoseDev>(ctx->pose), ctx->stream);
+  LAUNCHED(ctx, 1);
+}
+
+Geometry geometry(const as_ctx* ctx, int tile) {
+  Geometry G;
+  G.ts = tile;
+  G.ntx = (ctx->cam.W + tile - 1) / tile;
+  G.nty = (ctx->cam.H + tile - 1) / tile;
+  G.ntiles = G.ntx * G.nty;
+  return G;
+}
+
+void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_rendered,
+                int64_t pairs, const PhaseTimes& pt, double total_ms, as_stats* out) {
+  unsigned long long h[C_NCOUNTERS];
+  CK(cudaMemcpyAsync(h, ctx->counters.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::memset(out, 0, sizeof *out);
+  out->pairs = pairs;
+  out->active_pairs = (int64_t)h[C_ACTIVE];
+  out->uncertain_pairs = (int64_t)h[C_UNC];
+  out->fails = (int64_t)h[C_FAIL];
+  out->straddles = (int64_t)h[C_STRAD];
+  out->dropped = (int64_t)h[C_DROP];
+  out->order_violations = (int64_t)h[C_VIOL];
+  out->launches = ctx->launches;
+  out->kmax = (int32_t)h[C_KMAX];
+  out->n_sub = bi.n_sub;
+  out->n_vars = bi.n_vars;
+  out->n_tiles = n_tiles_rendered;
+  out->ms_setup = pt.setup;
+  out->ms_bin = pt.bin;
+  out->ms_pairs = pt.pairs;
+  out->ms_tile = pt.tile;
+  out->tile_kernel_ms = pt.tile;
+  out->ms_total = total_ms;
+  out->device_bytes = ctx->bytes;
+  (void)G;
+}
+
+void lpt(int n, const int64_t* costs, int world, int cap, int32_t* owner) {
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return costs[a] > costs[b]; });
+  std::vector<int64_t> load(world, 0);
+  std::vector<int> cnt(world, 0);
+  for (int t : idx) {
+    int best = -1;
+    for (int r = 0; r < world; ++r) {
+      if (cnt[r] >= cap) continue;
+      if (best < 0 || load[r] < load[best]) best = r;
+    }
+    owner[t] = best;
+    load[best] += costs[t] + 1;
+    ++cnt[best];
+  }
+}
+
+// per-tile cost pass over all sub-boxes (setup + count), host costs out
+void tile_costs(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, std::vector<int64_t>& costs) {
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemsetAsync(ctx->tcost.p, 0, sizeof(unsigned long long) * G.ntiles, st));
+  unsigned long long* ctr = P<unsigned long long>(ctx->counters);
+  for (int s = 0; s < bi.n_sub; ++s) {
+    CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
+    run_setup(ctx, bi, s);
+    BinArgs ba{};
+    ba.order = P<int32_t>(ctx->kval);  // identity order suffices for counting
+    ba.N = ctx->N;
+    ba.hot = ctx->hot.p;
+    ba.nv = bi.n_vars;
+    ba.ts = G.ts;
+    ba.ntx = G.ntx;
+    ba.nty = G.nty;
+    ba.W = ctx->cam.W;
+    ba.H = ctx->cam.H;
+    ba.owner = nullptr;
+    ba.counts = P<int64_t>(ctx->counts);
+    ba.tile_cost = P<unsigned long long>(ctx->tcost);
+    launch_count(ba, st);
+    LAUNCHED(ctx, 1);
+  }
+  std::vector<unsigned long long> h(G.ntiles);
+  CK(cudaMemcpyAsync(h.data(), ctx->tcost.p, sizeof(unsigned long long) * G.ntiles,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  costs.assign(h.begin(), h.end());
+  // counters of the cost pass must not leak into the render's stats
+  CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, st));
+}
+
+void rot_c2w_host(const double e[3], double R[9]) {
+  const double c0 = std::cos(e[0]), s0 = std::sin(e[0]), c1 = std::cos(e[1]), s1 = std::sin(e[1]);
+  const double c2 = std::cos(e[2]), s2 = std::sin(e[2]);
+  const double X[9] = {1, 0, 0, 0, c0, -s0, 0, s0, c0};
+  const double Y[9] = {c1, 0, s1, 0, 1, 0, -s1, 0, c1};
+  const double Z[9] = {c2, -s2, 0, s2, c2, 0, 0, 0, 1};
+  double T[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) T[3 * i + j] = Z[3 * i] * Y[j] + Z[3 * i + 1] * Y[3 + j] + Z[3 * i + 2] * Y[6 + j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) R[3 * i + j] = T[3 * i] * X[j] + T[3 * i + 1] * X[3 + j] + T[3 * i + 2] * X[6 + j];
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+int32_t as_version(void) { return ABSPLAT_VERSION; }
+
+const char* as_last_error(const as_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+as_status as_create(as_ctx** out, int32_t device, void* cuda_stream) {
+  if (!out) return AS_E_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return AS_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return AS_E_CUDA;
+  as_ctx* c = new as_ctx();
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  for (int k = 0; k < 8; ++k)
+    if (cudaEventCreate(&c->ev[k]) != cudaSuccess) {
+      delete c;
+      return AS_E_CUDA;
+    }
+  *out = c;
+  return AS_OK;
+}
+
+as_status as_destroy(as_ctx* ctx) {
+  if (!ctx) return AS_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->group_of,
+                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->pose, &ctx->hot,
+                    &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
+                    &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
+                    &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
+                    &ctx->tids, &ctx->tlist, &ctx->tslot, &ctx->owner, &ctx->nF, &ctx->nG,
+                    &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->diff, &ctx->cover,
+                    &ctx->pflag, &ctx->is_store, &ctx->slot, &ctx->scratch, &ctx->img_lo,
+                    &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map};
+  for (DevBuf* b : bufs) release(ctx, *b);
+  for (int k = 0; k < 8; ++k)
+    if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+  delete ctx;
+  return AS_OK;
+}
+
+as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* chol,
+                        const float* opacity, const float* color, int32_t flags) {
+  if (!ctx) return AS_E_ARG;
+  if (N < 0 || (N > 0 && (!mean || !chol || !opacity || !color))) {
+    set_err(ctx, "as_load_scene: bad arguments");
+    return AS_E_ARG;
+  }
+  if (N > (int64_t)INT32_MAX / 16) {
+    set_err(ctx, "as_load_scene: N too large");
+    return AS_E_ARG;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    const bool dev = flags & AS_PTR_DEVICE;
+    std::vector<float> hm, hc, ho, hcol;
+    const float *m = mean, *c = chol, *o = opacity, *col = color;
+    if (dev) {  // validate from a host copy
+      hm.resize(3 * N);
+      hc.resize(6 * N);
+      ho.resize(N);
+      hcol.resize(3 * N);
+      CK(cudaMemcpyAsync(hm.data(), mean, 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(hc.data(), chol, 24 * N, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(ho.data(), opacity, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(hcol.data(), color, 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      m = hm.data();
+      c = hc.data();
+      o = ho.data();
+      col = hcol.data();
+    }
+    for (int64_t i = 0; i < N; ++i) {
+      for (int k = 0; k < 3; ++k)
+        if (!finite_f(m[3 * i + k]) || !finite_f(col[3 * i + k]) || !(col[3 * i + k] >= 0.f) ||
+            !(col[3 * i + k] <= 1.f)) {
+          set_err(ctx, "Gaussian %lld: mean/colour not finite or colour outside [0,1]", (long long)i);
+          return AS_E_SCENE;
+        }
+      for (int k = 0; k < 6; ++k)
+        if (!finite_f(c[6 * i + k])) {
+          set_err(ctx, "Gaussian %lld: chol not finite", (long long)i);
+          return AS_E_SCENE;
+        }
+      if (!(c[6 * i] > 0.f) || !(c[6 * i + 2] > 0.f) || !(c[6 * i + 5] > 0.f)) {
+        set_err(ctx, "Gaussian %lld: chol diagonal must be > 0", (long long)i);
+        return AS_E_SCENE;
+      }
+      if (!(o[i] >= 0.f) || !(o[i] <= 1.f)) {
+        set_err(ctx, "Gaussian %lld: opacity outside [0,1]", (long long)i);
+        return AS_E_SCENE;
+      }
+    }
+    ensure(ctx, ctx->mean, 12 * std::max<int64_t>(N, 1));
+    ensure(ctx, ctx->chol, 24 * std::max<int64_t>(N, 1));
+    ensure(ctx, ctx->opacity, 4 * std::max<int64_t>(N, 1));
+    ensure(ctx, ctx->color, 12 * std::max<int64_t>(N, 1));
+    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (N > 0) {
+      CK(cudaMemcpyAsync(ctx->mean.p, mean, 12 * N, kind, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->chol.p, chol, 24 * N, kind, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->opacity.p, opacity, 4 * N, kind, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->color.p, color, 12 * N, kind, ctx->stream));
+    }
+    ctx->N = N;
+    ctx->n_groups = 0;
+    ctx->has_group = ctx->has_col = ctx->has_op = false;
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_set_camera(as_ctx* ctx, const as_camera* cam) {
+  if (!ctx) return AS_E_ARG;
+  if (!cam || cam->W <= 0 || cam->H <= 0 || cam->W > 65536 || cam->H > 65536 ||
+      !(cam->fx > 0) || !(cam->fy > 0) || !std::isfinite(cam->cx) || !std::isfinite(cam->cy)) {
+    set_err(ctx, "as_set_camera: invalid camera");
+    return AS_E_ARG;
+  }
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(cam->euler[k]) || !std::isfinite(cam->t[k])) {
+      set_err(ctx, "as_set_camera: non-finite pose");
+      return AS_E_ARG;
+    }
+  ctx->cam = *cam;
+  ctx->have_cam = true;
+  return AS_OK;
+}
+
+as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box) {
+  if (!ctx) return AS_E_ARG;
+  if (!box) {
+    set_err(ctx, "as_set_pose_box: NULL");
+    return AS_E_ARG;
+  }
+  as_pose_box saved = ctx->box;
+  const bool had = ctx->have_box;
+  ctx->box = *box;
+  BoxInfo bi;
+  as_status st = make_box(ctx, bi);
+  if (st != AS_OK) {
+    ctx->box = saved;
+    ctx->have_box = had;
+    return st;
+  }
+  if (box->t_frame != 0 && box->t_frame != 1) {
+    ctx->box = saved;
+    set_err(ctx, "t_frame must be 0 or 1");
+    return AS_E_ARG;
+  }
+  ctx->have_box = true;
+  return AS_OK;
+}
+
+as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
+  if (!ctx) return AS_E_ARG;
+  if (ctx->N < 0) {
+    set_err(ctx, "as_set_scene_box before as_load_scene");
+    return AS_E_STATE;
+  }
+  if (!sb) {
+    ctx->n_groups = 0;
+    ctx->has_group = ctx->has_col = ctx->has_op = false;
+    return AS_OK;
+  }
+  const int64_t N = ctx->N;
+  if (sb->n_groups < 0 || sb->n_groups > 3 || (sb->n_groups > 0 && (!sb->group_of || !sb->dir ||
+                                                                     !sb->shift_lo || !sb->shift_hi))) {
+    set_err(ctx, "as_set_scene_box: bad group arguments");
+    return AS_E_ARG;
+  }
+  if ((sb->col_lo == nullptr) != (sb->col_hi == nullptr) ||
+      (sb->op_lo == nullptr) != (sb->op_hi == nullptr)) {
+    set_err(ctx, "as_set_scene_box: lo/hi must both be given");
+    return AS_E_ARG;
+  }
+  for (int g = 0; g < sb->n_groups; ++g) {
+    if (!(sb->shift_hi[g] >= sb->shift_lo[g]) || !std::isfinite(sb->shift_lo[g]) ||
+        !std::isfinite(sb->shift_hi[g]) || sb->parts[g] < 1) {
+      set_err(ctx, "as_set_scene_box: bad shift range of group %d", g);
+      return AS_E_ARG;
+    }
+  }
+  for (int64_t i = 0; i < N; ++i) {
+    if (sb->n_groups > 0 && (sb->group_of[i] < -1 || sb->group_of[i] >= sb->n_groups)) {
+      set_err(ctx, "group_of[%lld] out of range", (long long)i);
+      return AS_E_ARG;
+    }
+    if (sb->col_lo)
+      for (int k = 0; k < 3; ++k) {
+        const float l = sb->col_lo[3 * i + k], h = sb->col_hi[3 * i + k];
+        if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) {
+          set_err(ctx, "colour interval of Gaussian %lld invalid", (long long)i);
+          return AS_E_SCENE;
+        }
+      }
+    if (sb->op_lo) {
+      const float l = sb->op_lo[i], h = sb->op_hi[i];
+      if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) {
+        set_err(ctx, "opacity interval of Gaussian %lld invalid", (long long)i);
+        return AS_E_SCENE;
+      }
+    }
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    ctx->n_groups = sb->n_groups;
+    for (int g = 0; g < 3; ++g) {
+      ctx->gparts[g] = g < sb->n_groups ? sb->parts[g] : 1;
+      ctx->shift_lo[g] = g < sb->n_groups ? sb->shift_lo[g] : 0.0;
+      ctx->shift_hi[g] = g < sb->n_groups ? sb->shift_hi[g] : 0.0;
+      for (int k = 0; k < 3; ++k) ctx->dir[g][k] = g < sb->n_groups ? sb->dir[3 * g + k] : 0.0;
+    }
+    ctx->has_group = sb->n_groups > 0;
+    if (ctx->has_group) {
+      ensure(ctx, ctx->group_of, 4 * std::max<int64_t>(N, 1));
+      CK(cudaMemcpyAsync(ctx->group_of.p, sb->group_of, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->has_col = sb->col_lo != nullptr;
+    if (ctx->has_col) {
+      ensure(ctx, ctx->col_lo, 12 * std::max<int64_t>(N, 1));
+      ensure(ctx, ctx->col_hi, 12 * std::max<int64_t>(N, 1));
+      CK(cudaMemcpyAsync(ctx->col_lo.p, sb->col_lo, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->col_hi.p, sb->col_hi, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->has_op = sb->op_lo != nullptr;
+    if (ctx->has_op) {
+      ensure(ctx, ctx->op_lo, 4 * std::max<int64_t>(N, 1));
+      ensure(ctx, ctx->op_hi, 4 * std::max<int64_t>(N, 1));
+      CK(cudaMemcpyAsync(ctx->op_lo.p, sb->op_lo, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->op_hi.p, sb->op_hi, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));  // host sources may be freed after return
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, float* hi,
+                           int32_t flags, as_stats* stats) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  if (!lo || !hi) {
+    set_err(ctx, "as_render_bounds: NULL output");
+    return AS_E_ARG;
+  }
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if ((st = check_tile_args(ctx, tile, batch, bi.n_vars)) != AS_OK) return st;
+  if ((flags & AS_ASYNC) && !(flags & AS_PTR_DEVICE)) {
+    set_err(ctx, "AS_ASYNC requires device outputs");
+    return AS_E_ARG;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const Geometry G = geometry(ctx, tile);
+    ctx->launches = 0;
+    if (stats) CK(cudaEventRecord(ctx->ev[0], s));
+    prepare_common(ctx, bi, G);
+    const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
+    float *dlo = lo, *dhi = hi;
+    if (!(flags & AS_PTR_DEVICE)) {
+      ensure(ctx, ctx->img_lo, sizeof(float) * img);
+      ensure(ctx, ctx->img_hi, sizeof(float) * img);
+      dlo = P<float>(ctx->img_lo);
+      dhi = P<float>(ctx->img_hi);
+    }
+    k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), G.ntiles);
+    LAUNCHED(ctx, 1);
+    PhaseTimes pt;
+    int64_t pairs = 0;
+    for (int sb = 0; sb < bi.n_sub; ++sb) {
+      int64_t M = 0;
+      render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
+                    nullptr, dlo, dhi, sb == 0, M, stats ? &pt : nullptr);
+      pairs += M;
+    }
+    if (!(flags & AS_PTR_DEVICE)) {
+      CK(cudaMemcpyAsync(lo, dlo, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hi, dhi, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
+    }
+    if (stats) {
+      CK(cudaEventRecord(ctx->ev[6], s));
+      CK(cudaEventSynchronize(ctx->ev[6]));
+      float tot = 0;
+      CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+      fill_stats(ctx, bi, G, G.ntiles, pairs, pt, tot, stats);
+    }
+    if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, int32_t cap,
+                        int32_t* owner) {
+  if (n_tiles < 0 || world < 1 || !owner || (n_tiles > 0 && !costs)) return AS_E_ARG;
+  if ((int64_t)cap * world < n_tiles) return AS_E_ARG;
+  lpt(n_tiles, costs, world, cap, owner);
+  return AS_OK;
+}
+
+as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_tiles,
+                         int32_t* owner, int64_t* costs) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if ((st = check_tile_args(ctx, tile, 1, bi.n_vars)) != AS_OK) return st;
+  if (world < 1 || !owner) {
+    set_err(ctx, "as_tile_owners: bad arguments");
+    return AS_E_ARG;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    const Geometry G = geometry(ctx, tile);
+    if ((int64_t)max_tiles * world < G.ntiles) {
+      set_err(ctx, "max_tiles * world < n_tiles");
+      return AS_E_ARG;
+    }
+    prepare_common(ctx, bi, G);
+    std::vector<int64_t> c;
+    tile_costs(ctx, bi, G, c);
+    lpt(G.ntiles, c.data(), world, max_tiles, owner);
+    if (costs) std::copy(c.begin(), c.end(), costs);
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank, int32_t world,
+                          float* lo_tm, float* hi_tm, int32_t max_tiles, int32_t* owned,
+                          int32_t* n_owned, int32_t flags, as_stats* stats) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if ((st = check_tile_args(ctx, tile, batch, bi.n_vars)) != AS_OK) return st;
+  if (world < 1 || rank < 0 || rank >= world || !lo_tm || !hi_tm || !owned || !n_owned) {
+    set_err(ctx, "as_render_shard: bad arguments");
+    return AS_E_ARG;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const Geometry G = geometry(ctx, tile);
+    if ((int64_t)max_tiles * world < G.ntiles) {
+      set_err(ctx, "max_tiles * world < n_tiles");
+      return AS_E_ARG;
+    }
+    ctx->launches = 0;
+    if (stats) CK(cudaEventRecord(ctx->ev[0], s));
+    prepare_common(ctx, bi, G);
+    // ---- owner map (identical on every rank): LPT over per-tile pair counts
+    std::vector<int32_t> own(G.ntiles, 0);
+    if (world > 1) {
+      std::vector<int64_t> c;
+      tile_costs(ctx, bi, G, c);
+      lpt(G.ntiles, c.data(), world, max_tiles, own.data());
+    }
+    std::vector<int32_t> mine;
+    for (int t = 0; t < G.ntiles; ++t)
+      if (own[t] == rank) mine.push_back(t);
+    const int nm = (int)mine.size();
+    CK(cudaMemcpyAsync(ctx->owner.p, own.data(), sizeof(int32_t) * G.ntiles,
+                       cudaMemcpyHostToDevice, s));
+    if (nm > 0)
+      CK(cudaMemcpyAsync(ctx->tlist.p, mine.data(), sizeof(int32_t) * nm, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->tslot.p, 0xff, sizeof(int32_t) * G.ntiles, s));
+    if (nm > 0) {
+      k_slot_map<<<(nm + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), nm, P<int32_t>(ctx->tslot));
+      LAUNCHED(ctx, 1);
+    }
+    const size_t tm = (size_t)std::max(nm, 1) * tile * tile * 3;
+    float *dlo = lo_tm, *dhi = hi_tm;
+    if (!(flags & AS_PTR_DEVICE)) {
+      ensure(ctx, ctx->img_lo, sizeof(float) * tm);
+      ensure(ctx, ctx->img_hi, sizeof(float) * tm);
+      dlo = P<float>(ctx->img_lo);
+      dhi = P<float>(ctx->img_hi);
+    }
+    PhaseTimes pt;
+    int64_t pairs = 0;
+    if (nm > 0) {
+      for (int sb = 0; sb < bi.n_sub; ++sb) {
+        int64_t M = 0;
+        const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0
+        render_subbox(ctx, bi, sb, need_setup, G, batch, P<int32_t>(ctx->owner), rank,
+                      P<int32_t>(ctx->tlist), nm, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0, M,
+                      stats ? &pt : nullptr);
+        pairs += M;
+      }
+    }
+    if (!(flags & AS_PTR_DEVICE) && nm > 0) {
+      CK(cudaMemcpyAsync(lo_tm, dlo, sizeof(float) * nm * tile * tile * 3, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hi_tm, dhi, sizeof(float) * nm * tile * tile * 3, cudaMemcpyDeviceToHost, s));
+    }
+    for (int k = 0; k < nm; ++k) owned[k] = mine[k];
+    *n_owned = nm;
+    if (stats) {
+      CK(cudaEventRecord(ctx->ev[6], s));
+      CK(cudaEventSynchronize(ctx->ev[6]));
+      float tot = 0;
+      CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+      fill_stats(ctx, bi, G, nm, pairs, pt, tot, stats);
+    }
+    if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_untile(as_ctx* ctx, int32_t W, int32_t H, int32_t tile, int32_t world,
+                    int32_t max_tiles, const int32_t* owned, const int32_t* n_owned,
+                    const float* lo_tm, const float* hi_tm, float* lo, float* hi, int32_t flags) {
+  const bool dev = flags & AS_PTR_DEVICE;
+  if (dev && !ctx) return AS_E_ARG;
+  if ((tile != 8 && tile != 16 && tile != 32) || W <= 0 || H <= 0 || world < 1 ||
+      max_tiles < 1 || !owned || !n_owned || !lo_tm || !hi_tm || !lo || !hi) {
+    if (ctx) set_err(ctx, "as_untile: bad arguments");
+    return AS_E_ARG;
+  }
+  Geometry G;
+  G.ts = tile;
+  G.ntx = (W + tile - 1) / tile;
+  G.nty = (H + tile - 1) / tile;
+  G.ntiles = G.ntx * G.nty;
+  std::vector<int32_t> slot_of(G.ntiles, -1);
+  for (int r = 0; r < world; ++r) {
+    if (n_owned[r] < 0 || n_owned[r] > max_tiles) {
+      if (ctx) set_err(ctx, "as_untile: n_owned[%d] out of range", r);
+      return AS_E_ARG;
+    }
+    for (int k = 0; k < n_owned[r]; ++k) {
+      const int t = owned[(size_t)r * max_tiles + k];
+      if (t < 0 || t >= G.ntiles || slot_of[t] != -1) {
+        if (ctx) set_err(ctx, "as_untile: tile %d invalid or owned twice", t);
+        return AS_E_ARG;
+      }
+      slot_of[t] = r * max_tiles + k;
+    }
+  }
+  for (int t = 0; t < G.ntiles; ++t)
+    if (slot_of[t] < 0) {
+      if (ctx) set_err(ctx, "as_untile: tile %d not owned by any rank", t);
+      return AS_E_ARG;
+    }
+  const int ts = tile;
+  if (!dev) {  // host assembly (plain index arithmetic)
+    for (int py = 0; py < H; ++py)
+      for (int px = 0; px < W; ++px) {
+        const int t = (py / ts) * G.ntx + px / ts;
+        const size_t src = ((size_t)slot_of[t] * ts * ts + (size_t)(py % ts) * ts + (px % ts)) * 3;
+        const size_t dst = ((size_t)py * W + px) * 3;
+        for (int c = 0; c < 3; ++c) {
+          lo[dst + c] = lo_tm[src + c];
+          hi[dst + c] = hi_tm[src + c];
+        }
+      }
+    return AS_OK;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
+    CK(cudaMemcpyAsync(ctx->untile_map.p, slot_of.data(), sizeof(int32_t) * G.ntiles,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    launch_untile(lo_tm, hi_tm, P<int32_t>(ctx->untile_map), ts, G.ntx, G.nty, W, H, lo, hi,
+                  ctx->stream);
+    LAUNCHED(ctx, 1);
+    if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(ctx->stream));
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+as_status as_render_concrete(as_ctx* ctx, const double* xi, float* img, int32_t flags) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if (!img || (bi.n_vars > 0 && !xi)) {
+    set_err(ctx, "as_render_concrete: bad arguments");
+    return AS_E_ARG;
+  }
+  double param[9];
+  for (int a = 0; a < 9; ++a) param[a] = bi.bp.lo[a];
+  for (int i = 0; i < bi.n_vars; ++i) {
+    if (!(xi[i] >= -1.0 && xi[i] <= 1.0)) {
+      set_err(ctx, "xi[%d] outside [-1,1]", i);
+      return AS_E_ARG;
+    }
+    param[bi.axis[i]] = bi.c[i] + bi.r[i] * xi[i];
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    ConcreteArgs a{};
+    double e[3], Rc[9], Mf[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    for (int k = 0; k < 3; ++k) e[k] = ctx->cam.euler[k] + param[3 + k];
+    rot_c2w_host(e, Rc);
+    if (ctx->box.t_frame == 1) rot_c2w_host(ctx->cam.euler, Mf);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) a.R[3 * r + c] = Rc[3 * c + r];
+    for (int k = 0; k < 3; ++k)
+      a.t[k] = ctx->cam.t[k] + Mf[3 * k] * param[0] + Mf[3 * k + 1] * param[1] + Mf[3 * k + 2] * param[2];
+    for (int g = 0; g < 3; ++g)
+      for (int k = 0; k < 3; ++k) a.shift[g][k] = (g < ctx->n_groups) ? param[6 + g] * ctx->dir[g][k] : 0.0;
+    const int64_t N = ctx->N;
+    ensure(ctx, ctx->conc_g, sizeof(double) * 8 * std::max<int64_t>(N, 1));
+    ensure(ctx, ctx->kkey, sizeof(unsigned long long) * (N + 1));
+    ensure(ctx, ctx->kkey2, sizeof(unsigned long long) * (N + 1));
+    ensure(ctx, ctx->kval, sizeof(int32_t) * (N + 1));
+    ensure(ctx, ctx->order, sizeof(int32_t) * (N + 1));
+    a.mean = P<float>(ctx->mean);
+    a.chol = P<float>(ctx->chol);
+    a.opacity = P<float>(ctx->opacity);
+    a.color = P<float>(ctx->color);
+    a.group_of = ctx->has_group ? P<int32_t>(ctx->group_of) : nullptr;
+    a.N = N;
+    a.fx = ctx->cam.fx;
+    a.fy = ctx->cam.fy;
+    a.cx = ctx->cam.cx;
+    a.cy = ctx->cam.cy;
+    a.W = ctx->cam.W;
+    a.H = ctx->cam.H;
+    a.gdata = P<double>(ctx->conc_g);
+    a.key = P<unsigned long long>(ctx->kkey);
+    a.val = P<int32_t>(ctx->kval);
+    launch_concrete_setup(a, s);
+    LAUNCHED(ctx, 1);
+    if (N > 0)
+      cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
+                      P<int32_t>(ctx->kval), P<int32_t>(ctx->order), N, 64);
+    a.order = P<int32_t>(ctx->order);
+    const size_t n = (size_t)a.W * a.H * 3;
+    float* dimg = img;
+    if (!(flags & AS_PTR_DEVICE)) {
+      ensure(ctx, ctx->img_lo, sizeof(float) * n);
+      dimg = P<float>(ctx->img_lo);
+    }
+    a.img = dimg;
+    launch_concrete_render(a, s);
+    LAUNCHED(ctx, 1);
+    if (!(flags & AS_PTR_DEVICE))
+      CK(cudaMemcpyAsync(img, dimg, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
+}  // extern "C"
+
+

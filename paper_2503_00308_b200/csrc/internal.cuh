@@ -1,0 +1,326 @@
+// internal.cuh -- device-side data layout and affine-form arithmetic of libabsplat.
+//
+// B200 (sm_100a) implementation of the AbstractSplat hot path (arXiv 2503.00308).  This
+// header is private to the CUDA sources in this directory; it shares nothing with oracle/.
+//
+// Affine forms (D7): y(xi) in [lo(xi), hi(xi)] over xi in [-1,1]^NV, stored as
+// coefficient arrays c[0..NV-1] (slopes) and c[NV] (constant).  Per-Gaussian setup runs in
+// fp64 (all discontinuous decisions are taken on fp64 data, H1); the per-pixel hot
+// loop runs in fp32 on tile-centred forms (H2).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/absplat.h"
+
+namespace absplat {
+
+constexpr int NVMAX = AS_MAX_VARS;
+constexpr double TAU = 1e-12;   // per-pixel cull threshold on a (G12)
+constexpr double DMIN = 0.01;   // near plane (G8)
+constexpr int KTAYLOR = 8;      // MatrixInv order
+constexpr double WCAP = 1e12;   // |W| guard -> FAIL (reading O3)
+
+enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4 };
+enum : int { P_EXC = 1, P_STORE = 2 };  // per list-position flags (exceptions, a9)
+
+// ------------------------------------------------------------------------- pose / box
+// One sub-box: the perturbed axes in canonical order with their centre and radius.
+struct SubBoxDev {
+  int n;
+  int axis[NVMAX];
+  double c[NVMAX], r[NVMAX];
+  double fixed[9];  // parameter value of every axis at xi = 0
+};
+
+struct BoxParams {  // kernel-argument copy of the box (a0)
+  double lo[9], hi[9];
+  int parts[9];
+  int n_sub;
+  int t_frame;
+  double euler0[3], t0[3];
+  double dir[3][3];
+};
+
+// Pose forms of one sub-box (a1): R (world->camera, row-major 3x3), t, group shifts,
+// all as forms over NVMAX+1 coefficients (only the first n slopes are meaningful), plus
+// the common depth slope g used to bound the pair-classification window.
+struct PoseDev {
+  double Rl[9][NVMAX + 1], Ru[9][NVMAX + 1];
+  double t[3][NVMAX + 1];  // exact affine
+  double g[3][NVMAX + 1];  // exact affine
+  double gslope[NVMAX];
+  int n;
+};
+
+// ------------------------------------------------------------------------- records
+// Hot record of one Gaussian for one sub-box, read by the tile kernel's staging step.
+// Layout (AoS, 16-byte aligned, NV-dependent size):
+//   double d2[2][NV+1]        D2 = d^2 lower / upper coefficients
+//   double du[2][2][NV+1]     DU_a = d*up_a  [a][lo/hi][coef]
+//   double mu[4]              mu-rect x_lo, y_lo, x_hi, y_hi (footprint, step 11)
+//   double r2                 s_cut * lambda_bar
+//   double pad
+//   float  w[6][2][NV+1]      W_ac = (Conic Mp)_ac  [a*3+c][lo/hi][coef]
+//   float  wc[6][2]           concretised W (lo, hi)
+//   float  o[2], clo[3], chi[3]
+//   int    flags, pad
+template <int NV>
+struct alignas(16) HotRec {
+  static constexpr int C = NV + 1;
+  double d2[2][C];
+  double du[2][2][C];
+  double mu[4];
+  double r2;
+  double pad0;
+  float w[6][2][C];
+  float wc[6][2];
+  float o[2];
+  float clo[3], chi[3];
+  int flags;
+};
+
+// Pair record (decisions): depth form and the window half-width w + S (a7).
+template <int NV>
+struct PairRec {
+  double dl[NV + 1], du[NV + 1];
+  double kappa;
+  double ws;
+};
+
+// ------------------------------------------------------------------------- fp64 forms
+template <int NV>
+struct DF {
+  double l[NV + 1], u[NV + 1];
+};
+
+template <int NV>
+__device__ __forceinline__ DF<NV> df_const(double v) {
+  DF<NV> f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) f.l[k] = f.u[k] = 0.0;
+  f.l[NV] = f.u[NV] = v;
+  return f;
+}
+template <int NV>
+__device__ __forceinline__ double df_min(const DF<NV>& f) {
+  double v = f.l[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v -= fabs(f.l[k]);
+  return v;
+}
+template <int NV>
+__device__ __forceinline__ double df_max(const DF<NV>& f) {
+  double v = f.u[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v += fabs(f.u[k]);
+  return v;
+}
+template <int NV>
+__device__ __forceinline__ void df_addto(DF<NV>& a, const DF<NV>& b) {
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    a.l[k] += b.l[k];
+    a.u[k] += b.u[k];
+  }
+}
+// c * f, exact (sides swap for c < 0)
+template <int NV>
+__device__ __forceinline__ DF<NV> df_scale(const DF<NV>& f, double c) {
+  DF<NV> r;
+  if (c >= 0) {
+#pragma unroll
+    for (int k = 0; k <= NV; ++k) {
+      r.l[k] = c * f.l[k];
+      r.u[k] = c * f.u[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k <= NV; ++k) {
+      r.l[k] = c * f.u[k];
+      r.u[k] = c * f.l[k];
+    }
+  }
+  return r;
+}
+// acc += c * f
+template <int NV>
+__device__ __forceinline__ void df_axpy(DF<NV>& acc, const DF<NV>& f, double c) {
+  if (c >= 0) {
+#pragma unroll
+    for (int k = 0; k <= NV; ++k) {
+      acc.l[k] += c * f.l[k];
+      acc.u[k] += c * f.u[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k <= NV; ++k) {
+      acc.l[k] += c * f.u[k];
+      acc.u[k] += c * f.l[k];
+    }
+  }
+}
+// acc += x*y under fixed McCormick planes (G1):
+//   lower: y_lo*x + x_lo*y - x_lo*y_lo,  upper: y_hi*x + x_lo*y - x_lo*y_hi
+template <int NV>
+__device__ __forceinline__ void df_mul_acc(DF<NV>& acc, const DF<NV>& x, const DF<NV>& y) {
+  const double xl = df_min(x), yl = df_min(y), yh = df_max(y);
+  const bool a = yl >= 0, b = xl >= 0, c = yh >= 0;
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    acc.l[k] += yl * (a ? x.l[k] : x.u[k]) + xl * (b ? y.l[k] : y.u[k]);
+    acc.u[k] += yh * (c ? x.u[k] : x.l[k]) + xl * (b ? y.u[k] : y.l[k]);
+  }
+  acc.l[NV] -= xl * yl;
+  acc.u[NV] -= xl * yh;
+}
+// acc += x*x: tangent at p = clamp(0, x_lo, x_hi) (lower), chord (upper) (G2)
+template <int NV>
+__device__ __forceinline__ void df_sq_acc(DF<NV>& acc, const DF<NV>& x) {
+  const double xl = df_min(x), xh = df_max(x);
+  const double p = fmin(fmax(0.0, xl), xh);
+  const double tp = 2.0 * p, sh = xl + xh;
+  const bool a = tp >= 0, b = sh >= 0;
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    acc.l[k] += tp * (a ? x.l[k] : x.u[k]);
+    acc.u[k] += sh * (b ? x.u[k] : x.l[k]);
+  }
+  acc.l[NV] -= p * p;
+  acc.u[NV] -= xl * xh;
+}
+
+// monotone uint64 image of a double (for radix sorting by kappa)
+__device__ __forceinline__ unsigned long long key_of_double(double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// ------------------------------------------------------------------------- launch plumbing
+struct LaunchCounter {
+  int64_t* counter;
+};
+
+// host-side launchers implemented in the .cu files (all enqueue on `st`)
+struct SetupArgs {
+  const float* mean;
+  const float* chol;
+  const float* opacity;
+  const float* color;
+  const int32_t* group_of;
+  const float* col_lo;
+  const float* col_hi;
+  const float* op_lo;
+  const float* op_hi;
+  int64_t N;
+  double fx, fy, cx, cy;
+  double dir[3][3];           // group shift directions
+  const PoseDev* pose;        // device pointer (one sub-box)
+  void* hot;                  // HotRec<NV>[N]
+  void* pair;                 // PairRec<NV>[N]
+  unsigned long long* kkey;   // [N] sort keys (kappa)
+  int32_t* kval;              // [N] Gaussian index
+  unsigned long long* wsmax;  // max over kept Gaussians of w+S (as ordered bits)
+  unsigned long long* counters;  // [4]: fails, straddles, dropped, spare
+};
+
+void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st);
+void launch_setup(int nv, const SetupArgs& a, cudaStream_t st);
+
+struct BinArgs {
+  const int32_t* order;  // [N] Gaussians in (kappa, index) order
+  int64_t N;
+  const void* hot;
+  int nv;
+  int ts, ntx, nty, W, H;
+  const int32_t* owner;  // [ntiles] or nullptr
+  int rank;
+  int64_t* counts;       // [N+1]
+  const int64_t* offsets;  // [N+1]
+  uint32_t* keys;        // [M] tile id
+  int32_t* vals;         // [M] Gaussian index
+  unsigned long long* tile_cost;  // [ntiles] or nullptr
+};
+void launch_count(const BinArgs& a, cudaStream_t st);
+void launch_emit(const BinArgs& a, cudaStream_t st);
+void launch_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin, int64_t* end,
+                   cudaStream_t st);
+
+struct PairArgs {
+  const uint32_t* keys;   // [M] sorted tile ids
+  const int32_t* vals;    // [M] Gaussian ids
+  const int64_t* tbegin;  // [ntiles]
+  const int64_t* tend;
+  int64_t M;
+  const void* pair;       // PairRec<NV>[N]
+  const unsigned long long* wsmax;
+  int nv;
+  int32_t* nF;            // [M]
+  int32_t* nG;            // [M]
+  int64_t* ntot;          // [M+1] nF + nG (scanned into off)
+  const int64_t* off;     // [M+1] exclusive scan of nF+nG
+  int32_t* exc;           // [total] tile-local positions: E_F ascending then E_G ascending
+  int32_t* hpos;          // [M] first position of E_F (tile-local) or own position
+  unsigned long long* counters;  // [0] uncertain pairs, [1] order violations
+};
+void launch_pairs_count(const PairArgs& a, cudaStream_t st);
+void launch_pairs_fill(const PairArgs& a, cudaStream_t st);
+void launch_mark(const PairArgs& a, int32_t* diff, cudaStream_t st);
+void launch_flags(const PairArgs& a, const int32_t* cover, int32_t* pflag, int32_t* is_store,
+                  cudaStream_t st);
+
+struct TileArgs {
+  const void* hot;            // HotRec<NV>[N]
+  const int32_t* vals;        // [M] Gaussian ids in (tile, kappa, index) order
+  const int64_t* tbegin;
+  const int64_t* tend;
+  const int32_t* tile_list;   // tiles to render (cost-descending), [n_list]
+  const int32_t* tile_slot;   // output slot of each tile id (tile-major) or nullptr
+  int n_list;
+  int ts, ntx, W, H;
+  int bs;
+  int first;                  // first sub-box: store instead of union
+  float ntau;                 // N * tau slack
+  // exceptions
+  const int32_t* pflag;       // [M] or nullptr
+  const int32_t* slot;        // [M] scratch slot of stored positions
+  const int64_t* eoff;        // [M+1]
+  const int32_t* nF;
+  const int32_t* nG;
+  const int32_t* exc;
+  const int32_t* hpos;
+  float4* scratch;            // [slots][ts*ts]
+  // outputs
+  float* lo;                  // row-major [H][W][3] (tile_slot == nullptr) or tile-major
+  float* hi;
+  unsigned long long* active; // active pair counter
+};
+void launch_tile(int nv, const TileArgs& a, cudaStream_t st);
+int tile_threads(int ts);
+size_t tile_smem_bytes(int nv, int ts, int bs);
+
+// concrete renderer (tests)
+struct ConcreteArgs {
+  const float* mean;
+  const float* chol;
+  const float* opacity;
+  const float* color;
+  const int32_t* group_of;
+  int64_t N;
+  double R[9], t[3], shift[3][3];  // world->camera R, camera centre, shift vector per group
+  double fx, fy, cx, cy;
+  int W, H;
+  double* gdata;                   // [N][8] scratch: mu, conic-like, depth, opacity
+  unsigned long long* key;         // [N]
+  int32_t* val;                    // [N]
+  const int32_t* order;            // [N] after sort
+  float* img;
+};
+void launch_concrete_setup(const ConcreteArgs& a, cudaStream_t st);
+void launch_concrete_render(const ConcreteArgs& a, cudaStream_t st);
+
+void launch_untile(const float* lo_tm, const float* hi_tm, const int32_t* slot_of_tile,
+                   int ts, int ntx, int nty, int W, int H, float* lo, float* hi,
+                   cudaStream_t st);
+
+}  // namespace absplat

@@ -1,0 +1,286 @@
+// k_bin.cu -- rows a6-a7: tile culling + binning of (tile, Gaussian) pairs in depth order,
+// per-tile ranges, and the depth-order abstraction (three-valued Ind with index tie-break,
+// Alg. 3 line 1 P:382 with Table 2's Ind relaxation P:222-229, reading G6) restricted to a
+// provably sufficient window of the (kappa, index)-sorted list.
+#include "internal.cuh"
+
+namespace absplat {
+
+// exact fp64 cull test of a rectangle of pixel centres (no FMA contraction: the decision
+// must be reproducible bit for bit, H1 / reading O1)
+__device__ __forceinline__ bool rect_culled(const double mu[4], double r2, double x0, double x1,
+                                            double y0, double y1) {
+  const double dx = fmax(0.0, fmax(__dsub_rn(mu[0], x1), __dsub_rn(x0, mu[2])));
+  const double dy = fmax(0.0, fmax(__dsub_rn(mu[1], y1), __dsub_rn(y0, mu[3])));
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
+}
+
+template <int NV>
+__device__ __forceinline__ void footprint(const HotRec<NV>* H, double mu[4], double& r2,
+                                          int& flags) {
+  flags = H->flags;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mu[k] = H->mu[k];
+  r2 = H->r2;
+}
+
+// candidate tile range (superset) of a footprint
+__device__ __forceinline__ void tile_range(const double mu[4], double r2, int ts, int W, int H,
+                                           int& tx0, int& tx1, int& ty0, int& ty1) {
+  const double R = sqrt(r2) * (1.0 + 1e-9) + 1e-6;
+  const double xl = mu[0] - R, xh = mu[2] + R, yl = mu[1] - R, yh = mu[3] + R;
+  // pixel centres px + 0.5 in [xl, xh]
+  double pxl = floor(xl - 0.5) - 1.0, pxh = ceil(xh - 0.5) + 1.0;
+  double pyl = floor(yl - 0.5) - 1.0, pyh = ceil(yh - 0.5) + 1.0;
+  pxl = fmax(pxl, 0.0);
+  pyl = fmax(pyl, 0.0);
+  pxh = fmin(pxh, (double)(W - 1));
+  pyh = fmin(pyh, (double)(H - 1));
+  if (!(pxl <= pxh) || !(pyl <= pyh)) {
+    tx0 = 1;
+    tx1 = 0;
+    ty0 = 1;
+    ty1 = 0;
+    return;
+  }
+  tx0 = (int)pxl / ts;
+  tx1 = (int)pxh / ts;
+  ty0 = (int)pyl / ts;
+  ty1 = (int)pyh / ts;
+}
+
+template <int NV, bool EMIT>
+__global__ void k_bin(BinArgs A) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= A.N) return;
+  const int32_t g = A.order[r];
+  const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
+  double mu[4], r2;
+  int flags;
+  footprint<NV>(H, mu, r2, flags);
+  int cnt = 0;
+  int64_t out = EMIT ? A.offsets[r] : 0;
+  if (!(flags & F_DROP)) {
+    int tx0, tx1, ty0, ty1;
+    tile_range(mu, r2, A.ts, A.W, A.H, tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ++ty) {
+      const double y0 = ty * A.ts + 0.5, y1 = fmin((double)((ty + 1) * A.ts), (double)A.H) - 0.5;
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const double x0 = tx * A.ts + 0.5, x1 = fmin((double)((tx + 1) * A.ts), (double)A.W) - 0.5;
+        if (rect_culled(mu, r2, x0, x1, y0, y1)) continue;
+        const int tile = ty * A.ntx + tx;
+        if (A.owner && A.owner[tile] != A.rank) {
+          if (!EMIT && A.tile_cost) atomicAdd(&A.tile_cost[tile], 1ull);
+          continue;
+        }
+        if (EMIT) {
+          A.keys[out] = (uint32_t)tile;
+          A.vals[out] = g;
+          ++out;
+        } else if (A.tile_cost) {
+          atomicAdd(&A.tile_cost[tile], 1ull);
+        }
+        ++cnt;
+      }
+    }
+  }
+  if (!EMIT) A.counts[r] = cnt;
+}
+
+#define NV_SWITCH(nv, ...)                                   \
+  switch (nv) {                                              \
+    case 0: { constexpr int NVc = 0; __VA_ARGS__; } break;   \
+    case 1: { constexpr int NVc = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int NVc = 2; __VA_ARGS__; } break;   \
+    case 3: { constexpr int NVc = 3; __VA_ARGS__; } break;   \
+    case 4: { constexpr int NVc = 4; __VA_ARGS__; } break;   \
+    case 5: { constexpr int NVc = 5; __VA_ARGS__; } break;   \
+    case 6: { constexpr int NVc = 6; __VA_ARGS__; } break;   \
+    case 7: { constexpr int NVc = 7; __VA_ARGS__; } break;   \
+    case 8: { constexpr int NVc = 8; __VA_ARGS__; } break;   \
+    case 9: { constexpr int NVc = 9; __VA_ARGS__; } break;   \
+    default: break;                                          \
+  }
+
+void launch_count(const BinArgs& a, cudaStream_t st) {
+  if (a.N <= 0) return;
+  const unsigned blocks = (unsigned)((a.N + 127) / 128);
+  NV_SWITCH(a.nv, (k_bin<NVc, false><<<blocks, 128, 0, st>>>(a)));
+}
+void launch_emit(const BinArgs& a, cudaStream_t st) {
+  if (a.N <= 0) return;
+  const unsigned blocks = (unsigned)((a.N + 127) / 128);
+  NV_SWITCH(a.nv, (k_bin<NVc, true><<<blocks, 128, 0, st>>>(a)));
+}
+
+__global__ void k_ranges(const uint32_t* keys, int64_t M, int64_t* begin, int64_t* end) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M) return;
+  const uint32_t t = keys[p];
+  if (p == 0 || keys[p - 1] != t) begin[t] = p;
+  if (p == M - 1 || keys[p + 1] != t) end[t] = p + 1;
+}
+void launch_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin, int64_t* end,
+                   cudaStream_t st) {
+  cudaMemsetAsync(begin, 0, sizeof(int64_t) * ntiles, st);
+  cudaMemsetAsync(end, 0, sizeof(int64_t) * ntiles, st);
+  if (M <= 0) return;
+  k_ranges<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(keys, M, begin, end);
+}
+
+// ------------------------------------------------------------------------- pairs (a7)
+// Ind(d_i - d_j) over the box with the index tie-break (G6): 1 = j certainly in front of i,
+// 0 = certainly not, -1 = '?'.  Same expression order as the definition (no FMA).
+template <int NV>
+__device__ __forceinline__ int ind_class(const PairRec<NV>& Pi, int32_t i, const PairRec<NV>& Pj,
+                                         int32_t j) {
+  double dl = __dsub_rn(Pi.dl[NV], Pj.du[NV]);
+  double du = __dsub_rn(Pi.du[NV], Pj.dl[NV]);
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    s1 = __dadd_rn(s1, fabs(__dsub_rn(Pi.dl[k], Pj.du[k])));
+    s2 = __dadd_rn(s2, fabs(__dsub_rn(Pi.du[k], Pj.dl[k])));
+  }
+  dl = __dsub_rn(dl, s1);
+  du = __dadd_rn(du, s2);
+  if (i > j) {
+    if (dl >= 0.0) return 1;
+    if (du < 0.0) return 0;
+  } else {
+    if (dl > 0.0) return 1;
+    if (du <= 0.0) return 0;
+  }
+  return -1;
+}
+
+template <int NV>
+__device__ __forceinline__ PairRec<NV> load_pair(const void* base, int32_t g) {
+  return reinterpret_cast<const PairRec<NV>*>(base)[g];
+}
+
+// Window bound: a '?' pair (j before i) needs kappa_i - kappa_j <= ws_i + ws_j <= ws_i + M.
+__device__ __forceinline__ bool beyond(double dk, double wsi, double M, double ki, double kj) {
+  const double bound = (wsi + M) * (1.0 + 1e-9) + 1e-12 * (fabs(ki) + fabs(kj)) + 1e-300;
+  return dk > bound;
+}
+
+template <int NV, int PASS>  // PASS 0: count, 1: fill
+__global__ void k_pairs(PairArgs A) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.M) return;
+  const uint32_t t = A.keys[p];
+  const int64_t b = A.tbegin[t], e = A.tend[t];
+  const int32_t gi = A.vals[p];
+  const PairRec<NV> Pi = load_pair<NV>(A.pair, gi);
+  const double M = __longlong_as_double((long long)*A.wsmax);
+  int nF = 0, nG = 0, viol = 0;
+  int64_t off = 0;
+  int nFt = 0;
+  if (PASS == 1) {
+    off = A.off[p];
+    nFt = A.nF[p];
+  }
+  int hmin = (int)(p - b);
+  // backward: earlier positions (expected Ind in {1, ?})
+  for (int64_t q = p - 1; q >= b; --q) {
+    const int32_t gj = A.vals[q];
+    const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
+    if (beyond(Pi.kappa - Pj.kappa, Pi.ws, M, Pi.kappa, Pj.kappa)) break;
+    const int c = ind_class<NV>(Pi, gi, Pj, gj);
+    if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
+      if (c == 0) ++viol;
+      if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
+      hmin = (int)(q - b);
+      ++nF;
+    }
+  }
+  // forward: later positions (expected Ind in {0, ?})
+  for (int64_t q = p + 1; q < e; ++q) {
+    const int32_t gj = A.vals[q];
+    const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
+    if (beyond(Pj.kappa - Pi.kappa, Pi.ws, M, Pi.kappa, Pj.kappa)) break;
+    const int c = ind_class<NV>(Pi, gi, Pj, gj);
+    if (c == -1 || c == 1) {
+      if (c == 1) ++viol;
+      if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);
+      ++nG;
+    }
+  }
+  if (PASS == 0) {
+    A.nF[p] = nF;
+    A.nG[p] = nG;
+    A.ntot[p] = nF + nG;
+    if (nG) atomicAdd(&A.counters[0], (unsigned long long)nG);
+    if (viol) atomicAdd(&A.counters[1], (unsigned long long)viol);
+  } else {
+    A.hpos[p] = hmin;
+  }
+}
+
+void launch_pairs_count(const PairArgs& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  const unsigned blocks = (unsigned)((a.M + 127) / 128);
+  NV_SWITCH(a.nv, (k_pairs<NVc, 0><<<blocks, 128, 0, st>>>(a)));
+}
+void launch_pairs_fill(const PairArgs& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  const unsigned blocks = (unsigned)((a.M + 127) / 128);
+  NV_SWITCH(a.nv, (k_pairs<NVc, 1><<<blocks, 128, 0, st>>>(a)));
+}
+
+// exceptional position p needs scratch entries on [tile_begin + h_p, p] (its T_hi window,
+// which contains E_F(p)) and at every element of E_G(p) (those are exceptional themselves
+// and mark their own windows, which contain their position).
+__global__ void k_mark(PairArgs A, int32_t* diff) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.M) return;
+  if (A.nF[p] + A.nG[p] == 0) return;
+  const int64_t b = A.tbegin[A.keys[p]];
+  atomicAdd(&diff[b + A.hpos[p]], 1);
+  atomicAdd(&diff[p + 1], -1);
+}
+void launch_mark(const PairArgs& a, int32_t* diff, cudaStream_t st) {
+  if (a.M <= 0) return;
+  k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, diff);
+}
+
+__global__ void k_flags(PairArgs A, const int32_t* cover, int32_t* pflag, int32_t* is_store) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.M) return;
+  const bool exc = (A.nF[p] + A.nG[p]) > 0;
+  const bool store = cover[p] > 0;
+  pflag[p] = (exc ? P_EXC : 0) | (store ? P_STORE : 0);
+  is_store[p] = store ? 1 : 0;
+}
+void launch_flags(const PairArgs& a, const int32_t* cover, int32_t* pflag, int32_t* is_store,
+                  cudaStream_t st) {
+  if (a.M <= 0) return;
+  k_flags<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cover, pflag, is_store);
+}
+
+// ------------------------------------------------------------------------- untile (a11)
+__global__ void k_untile(const float* lo_tm, const float* hi_tm, const int32_t* slot_of_tile,
+                         int ts, int ntx, int W, int H, float* lo, float* hi) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)W * H) return;
+  const int px = (int)(idx % W), py = (int)(idx / W);
+  const int tile = (py / ts) * ntx + px / ts;
+  const int64_t s = slot_of_tile[tile];
+  const int64_t src = (s * ts * ts + (int64_t)(py % ts) * ts + (px % ts)) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[3 * idx + c] = lo_tm[src + c];
+    hi[3 * idx + c] = hi_tm[src + c];
+  }
+}
+void launch_untile(const float* lo_tm, const float* hi_tm, const int32_t* slot_of_tile, int ts,
+                   int ntx, int nty, int W, int H, float* lo, float* hi, cudaStream_t st) {
+  (void)nty;
+  const int64_t n = (int64_t)W * H;
+  if (n <= 0) return;
+  k_untile<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lo_tm, hi_tm, slot_of_tile, ts, ntx, W, H,
+                                                        lo, hi);
+}
+
+}  // namespace absplat

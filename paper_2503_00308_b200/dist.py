@@ -1,0 +1,66 @@
+"""Tile sharding over GPUs (north_star (3)): one process per GPU, the scene
+replicated on every rank, image tiles assigned by the library's deterministic LPT owner
+map, each rank rendering only its tiles into a compact tile-major buffer, then ONE
+all-gather of the bound tiles (NCCL over NVLink / NVSwitch) and an untile on the root.
+
+Gaussians are never split across ranks: blending order is not commutative.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .api import Context, as_untile
+
+
+class ShardedRenderer:
+    """Render the abstract image of the context's scene/camera/box across `world` ranks."""
+
+    def __init__(self, ctx: Context, rank: int, world: int, group=None, tile: int = 16,
+                 batch: int = 64, slack: float = 0.25, device=None):
+        import torch
+        self.ctx, self.rank, self.world, self.group = ctx, rank, world, group
+        self.tile, self.batch = tile, batch
+        nt = ctx.n_tiles(tile)
+        base = -(-nt // world)
+        self.cap = base + max(1, int(base * slack))
+        dev = device if device is not None else f"cuda:{ctx.device}"
+        shape = (self.cap, tile * tile, 3)
+        self.lo_tm = torch.empty(shape, dtype=torch.float32, device=dev)
+        self.hi_tm = torch.empty(shape, dtype=torch.float32, device=dev)
+        # gathered buffers are flat along dim 0 (world * cap) as both NCCL and gloo accept
+        self.g_lo = torch.empty((world * self.cap,) + shape[1:], dtype=torch.float32, device=dev)
+        self.g_hi = torch.empty((world * self.cap,) + shape[1:], dtype=torch.float32, device=dev)
+        self.meta = torch.empty((self.cap + 1,), dtype=torch.int32, device=dev)
+        self.g_meta = torch.empty((world * (self.cap + 1),), dtype=torch.int32, device=dev)
+
+    def step(self, stats: bool = False):
+        """One sharded render.  Returns (lo, hi) on rank 0 (None elsewhere) and stats."""
+        import torch
+        import torch.distributed as dist
+        lo_tm, hi_tm, owned, n_owned, st = self.ctx.as_render_shard(
+            self.tile, self.batch, self.rank, self.world, self.cap, self.lo_tm, self.hi_tm,
+            stats=stats)
+        meta = np.concatenate([[n_owned], owned]).astype(np.int32)
+        self.meta.copy_(torch.from_numpy(meta), non_blocking=False)
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.g_lo, self.lo_tm, group=self.group)
+            dist.all_gather_into_tensor(self.g_hi, self.hi_tm, group=self.group)
+            dist.all_gather_into_tensor(self.g_meta, self.meta, group=self.group)
+        else:
+            self.g_lo.copy_(self.lo_tm)
+            self.g_hi.copy_(self.hi_tm)
+            self.g_meta.copy_(self.meta)
+        if self.rank != 0:
+            return None, None, st
+        gm = self.g_meta.cpu().numpy().reshape(self.world, self.cap + 1)
+        g_lo, g_hi = self.g_lo, self.g_hi
+        if not g_lo.is_cuda:  # host assembly path (CPU / gloo)
+            g_lo, g_hi = g_lo.numpy(), g_hi.numpy()
+        lo, hi = self.ctx.as_untile(self.tile, self.world, self.cap, gm[:, 1:], gm[:, 0],
+                                    g_lo, g_hi)
+        return lo, hi, st
+
+
+def assemble_host(W: int, H: int, tile: int, world: int, cap: int, owned, n_owned, lo_tm, hi_tm):
+    """Host-side assembly (as_untile with host pointers; no GPU needed)."""
+    return as_untile(W, H, tile, world, cap, owned, n_owned, lo_tm, hi_tm)

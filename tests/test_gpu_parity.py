@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element,
+at reduced sizes (several tiles, ragged tails) and at BASELINE.json's full sizes on sampled
+pixels; plus soundness of the GPU bounds against concrete renders, TS/BS invariance, and
+tile-sharded rendering == single-GPU rendering.  Tolerance: 1e-4 absolute per channel
+(north_star)."""
+import copy
+import math
+
+import numpy as np
+import pytest
+
+from tests import helpers as H
+from workloads import make_config
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def gpu_render(ctx, w, tile=None, batch=None):
+    ctx.load_workload(w)
+    lo, hi, st = ctx.as_render_bounds(tile=tile or w.tile, batch=batch or w.batch)
+    return lo.cpu().numpy().astype(np.float64), hi.cpu().numpy().astype(np.float64), st
+
+
+SMALL = {"C1": dict(), "C2": dict(N=4000, res=72), "C3": dict(N=5000, res=56),
+         "C4": dict(N=6000, res=72), "C5": dict(N=4000, res=72)}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_parity_reduced(ctx, oracle, name):
+    w = make_config(name, **SMALL[name])
+    lo, hi, st = gpu_render(ctx, w)
+    olo, ohi, ost = oracle.render_bounds(w)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= TOL, (name, err)
+    assert st["order_violations"] == 0
+    assert st["pairs"] == ost["pairs"]
+    assert st["uncertain_pairs"] == ost["uncertain_pairs"]
+    assert st["active_pairs"] == ost["active_pairs"]
+    assert st["fails"] == ost["fails"] and st["dropped"] == ost["dropped"]
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
+    w = make_config(name, **SMALL[name])
+    base_lo, base_hi, _ = gpu_render(ctx, w, 16, 64)
+    for tile, batch in ((8, 1), (8, 256), (16, 7), (32, 32), (32, 128)):
+        lo, hi, _ = gpu_render(ctx, w, tile, batch)
+        assert np.abs(lo - base_lo).max() <= 1e-5 and np.abs(hi - base_hi).max() <= 1e-5
+
+
+def test_parity_full_c2(ctx, oracle):
+    """Full-size C2 (100k Gaussians, 200x200) against the oracle's full image."""
+    w = make_config("C2")
+    lo, hi, st = gpu_render(ctx, w)
+    olo, ohi, ost = oracle.render_bounds(w)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= TOL, err
+    assert st["pairs"] == ost["pairs"]
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_parity_full_sampled(ctx, oracle, name):
+    """BASELINE.json full sizes in the bench's launch configuration; the oracle computes
+    sampled pixels one by one with the tile-free direct definition."""
+    w = make_config(name)
+    lo, hi, st = gpu_render(ctx, w)
+    rng = np.random.default_rng(7)
+    Wd, Hd = w.camera["W"], w.camera["H"]
+    # random pixels + the brightest-gap pixels (where errors would show)
+    gap = (hi - lo).sum(-1)
+    top = np.argsort(gap.reshape(-1))[-16:]
+    px = np.concatenate([rng.integers(0, Wd, 24), top % Wd])
+    py = np.concatenate([rng.integers(0, Hd, 24), top // Wd])
+    olo, ohi = oracle.pixel_bounds(w, px, py)
+    err = max(np.abs(lo[py, px] - olo).max(), np.abs(hi[py, px] - ohi).max())
+    assert err <= TOL, (name, err)
+    assert st["order_violations"] == 0
+    assert np.all(lo <= hi) and lo.min() >= 0 and hi.max() <= 1
+
+
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+def test_gpu_bounds_contain_concrete_renders(ctx, oracle, name):
+    """Theorem 1 on the GPU output: concrete renders at sampled box points (GPU concrete
+    renderer, itself checked against the fp64 oracle renderer) lie inside [lo, hi]."""
+    w = make_config(name, **SMALL[name])
+    lo, hi, st = gpu_render(ctx, w)
+    ax = H.box_axes(w)
+    var = [k for k in range(9) if ax[k][1] > ax[k][0]]
+    rng = np.random.default_rng(3)
+    worst = 0.0
+    for trial in range(24):
+        xi = rng.uniform(-1, 1, len(var)) if trial else np.ones(len(var))
+        img = ctx.as_render_concrete(xi).cpu().numpy().astype(np.float64)
+        if trial < 2:  # the GPU concrete renderer against the fp64 oracle renderer
+            p = np.array([(lo_ + hi_) / 2 for lo_, hi_ in ax])
+            for k, x in zip(var, xi):
+                p[k] = (ax[k][0] + ax[k][1]) / 2 + x * (ax[k][1] - ax[k][0]) / 2
+            e, t, shifts = H.pose_of(w, p)
+            ref = oracle.render_concrete(w, euler=e, t=t, shifts=shifts)
+            assert np.abs(img - ref).max() <= 1e-5
+        worst = max(worst, (lo - img).max(), (img - hi).max())
+    assert worst <= 2e-5, worst
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_equals_single(ctx, world):
+    """Tiles rendered rank by rank (sequentially on one GPU) and assembled with as_untile are
+    bitwise identical to the single-GPU image (north_star tile sharding)."""
+    import torch
+    w = make_config("C4", N=8000, res=96)
+    ctx.load_workload(w)
+    lo, hi, _ = ctx.as_render_bounds(tile=16, batch=64)
+    nt = ctx.n_tiles(16)
+    cap = -(-nt // world) + 2
+    tl, th, owned, nown = [], [], [], []
+    for r in range(world):
+        a, b, o, n, _ = ctx.as_render_shard(16, 64, r, world, cap)
+        tl.append(a)
+        th.append(b)
+        owned.append(o)
+        nown.append(n)
+    assert sum(nown) == nt
+    glo = torch.stack(tl)
+    ghi = torch.stack(th)
+    ulo, uhi = ctx.as_untile(16, world, cap, np.stack(owned), np.array(nown, np.int32), glo, ghi)
+    assert torch.equal(ulo, lo) and torch.equal(uhi, hi)
+    owner, costs = ctx.as_tile_owners(16, world, cap)
+    for r in range(world):
+        assert sorted(np.nonzero(owner == r)[0].tolist()) == sorted(owned[r][:nown[r]].tolist())
+
+
+def test_host_pointer_path(ctx):
+    """as_render_bounds with HOST output buffers (the e2e path) equals the device path."""
+    w = make_config("C2", N=3000, res=40)
+    ctx.load_workload(w)
+    lo_d, hi_d, _ = ctx.as_render_bounds(16, 64)
+    lo = np.zeros((40, 40, 3), np.float32)
+    hi = np.zeros((40, 40, 3), np.float32)
+    ctx.as_render_bounds(16, 64, lo=lo, hi=hi)
+    assert np.array_equal(lo, lo_d.cpu().numpy()) and np.array_equal(hi, hi_d.cpu().numpy())
+
+
+def test_edge_cases(ctx, oracle):
+    from workloads.synth import Workload
+    w = make_config("C1")
+    empty = Workload("empty", w.mean[:0], w.chol[:0], w.opacity[:0], w.color[:0], w.camera,
+                     w.pose_box, None)
+    lo, hi, st = gpu_render(ctx, empty)
+    assert np.all(lo == 0) and np.all(hi == 0)
+    behind = copy.deepcopy(w)
+    behind.mean = behind.mean.copy()
+    behind.mean[:, 2] *= -1
+    lo, hi, st = gpu_render(ctx, behind)
+    assert st["dropped"] == 16 and hi.max() <= 1e-10
+    # ragged image (not a multiple of the tile) and a spiky scene with FAIL Gaussians
+    w = make_config("C1", N=24, res=21)
+    ch = w.chol.copy()
+    ch[:, 2] *= 1e-3
+    ch[:, 4] *= 1e-3
+    ch[:, 5] *= 1e-3
+    w.chol = ch
+    w.pose_box["eps_R"] = [0.0, 0.0, math.radians(3.0)]
+    lo, hi, st = gpu_render(ctx, w)
+    olo, ohi, ost = oracle.render_bounds(w)
+    assert st["fails"] == ost["fails"] > 0
+    assert max(np.abs(lo - olo).max(), np.abs(hi - ohi).max()) <= TOL
