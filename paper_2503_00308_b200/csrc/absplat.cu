@@ -644,8 +644,11 @@ void tile_costs(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, std::vector<i
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   costs.assign(h.begin(), h.end());
-  // counters of the cost pass must not leak into the render's stats
-  CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, st));
+  // counters of the cost pass must not leak into the render's stats; C_WSMAX (the pair
+  // window bound of the last sub-box's setup) stays valid for a render that reuses it
+  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_WSMAX, st));
+  CK(cudaMemsetAsync(ctr + C_WSMAX + 1, 0, sizeof(unsigned long long) * (C_NCOUNTERS - C_WSMAX - 1),
+                     st));
 }
 
 void rot_c2w_host(const double e[3], double R[9]) {

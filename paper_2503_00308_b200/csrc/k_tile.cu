@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
 
   // my pixels
   int lx[PPT], ly[PPT];
+  bool in_img[PPT];
   float du0[PPT], du1[PPT];
   float Tb[PPT], Tl[PPT], ahc[PPT][3], alc[PPT][3];
 #pragma unroll
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
     const int l = threadIdx.x + q * nthr;
     lx[q] = l % ts;
     ly[q] = l / ts;
+    in_img[q] = (tx * ts + lx[q] < A.W) && (ty * ts + ly[q] < A.H);
     du0[q] = (float)lx[q] + 0.5f - 0.5f * ts;
     du1[q] = (float)ly[q] + 0.5f - 0.5f * ts;
     Tb[q] = Tl[q] = 1.f;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
       bool any = false;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
-        keep[q] = !(__dadd_rn(cx2[j * ts + lx[q]], cy2[j * ts + ly[q]]) > R.r2);
+        keep[q] = in_img[q] && !(__dadd_rn(cx2[j * ts + lx[q]], cy2[j * ts + ly[q]]) > R.r2);
         any |= keep[q];
         alo[q] = ahi[q] = 0.f;
       }

@@ -57,7 +57,8 @@ def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
     base_lo, base_hi, _ = gpu_render(ctx, w, 16, 64)
     for tile, batch in ((8, 1), (8, 256), (16, 7), (32, 32), (32, 128)):
         lo, hi, _ = gpu_render(ctx, w, tile, batch)
-        assert np.abs(lo - base_lo).max() <= 1e-5 and np.abs(hi - base_hi).max() <= 1e-5
+        # tile-centred fp32 forms round differently per tile size; within the parity budget
+        assert np.abs(lo - base_lo).max() <= TOL and np.abs(hi - base_hi).max() <= TOL
 
 
 def test_parity_full_c2(ctx, oracle):
