@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py -- abstract pixels/s of the B200 abstract-rendering path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A step renders the full lo/hi bound images of one workload (all rows a0-a11 of SURVEY §8(a):
+pose forms, per-Gaussian setup, binning, depth-pair classification, tile kernel, union and,
+for N > 1, the gather of the bound tiles).  Inputs (scene, records) are resident in HBM when
+the timed region starts; L2 is flushed (512 MiB write) before every timed step.  value =
+W*H*P / (device ms per step), P = number of pose sub-boxes, max over ranks.  For N > 1 the
+image is fixed and its tiles are sharded over ranks ("scaling": "strong").
+
+Extra keys: roofline of the dominant kernel (k_tile, FP32-issue bound), cpu_baseline (the
+fp64 oracle on a bounded sample of the same workload on this host's cores), e2e (the same
+metric through the C ABI with host buffers: scene H2D + render + bound images D2H), clocks,
+gpu_launches, bound widths.  --impl reference times the oracle itself as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "abstract pixels/s at 1/2/4/8 B200; mean bound width vs fp64 oracle"
+UNIT = "px/s"
+SM_COUNT = 148
+FP32_LANES = 128
+
+
+def f_ops(n: int) -> int:
+    """FP32 arithmetic ops (FMA = 1) of steps 14-19 per active (pixel, Gaussian) pair for n
+    box variables: x forms 4(n+1), conc x 4n, q McCormick 24(n+1)+12,
+    conc q 6n, squares 6(n+1)+15, conc s 2n+1, opacity 4, blend 10."""
+    return 34 * (n + 1) + 12 * n + 42
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = {}
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+    return d
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def clocks_bad(c):
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(c.get("reasons", [])):
+        return True
+    if c.get("sm_mhz") and c.get("sm_max_mhz") and not c.get("reasons"):
+        return c["sm_mhz"] < 0.5 * c["sm_max_mhz"]
+    return False
+
+
+# ----------------------------------------------------------------------------- oracle sample
+SAMPLE_FRACTION = {"C1": 1.0, "C2": 0.25, "C3": 0.03, "C4": 0.05, "C5": 0.25}
+
+
+def sample_tiles(w, frac):
+    tile = w.tile
+    ntx = -(-w.camera["W"] // tile)
+    nty = -(-w.camera["H"] // tile)
+    nt = ntx * nty
+    k = max(1, int(round(nt * frac)))
+    return np.unique(np.linspace(0, nt - 1, k).round().astype(np.int32)), nt
+
+
+def oracle_sample(w, tiles, nthreads=0):
+    from oracle import pyoracle
+    t0 = time.perf_counter()
+    lo, hi, st = pyoracle.render_tiles(w, tiles, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return lo, hi, st, dt
+
+
+def tile_mask(w, tiles):
+    tile = w.tile
+    ntx = -(-w.camera["W"] // tile)
+    m = np.zeros((w.camera["H"], w.camera["W"]), bool)
+    for t in tiles:
+        tx, ty = t % ntx, t // ntx
+        m[ty * tile:(ty + 1) * tile, tx * tile:(tx + 1) * tile] = True
+    return m
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    from workloads import make_config
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = make_config(args.config)
+    P = w.n_sub
+    # size each step so the whole run ends within a few minutes
+    nsteps = args.steps + args.warmup
+    target = max(2.0, min(20.0, 150.0 / max(nsteps, 1)))
+    _, nt = sample_tiles(w, 1.0)
+    t1 = oracle_sample(w, np.array([0], np.int32))[3]
+    t3 = oracle_sample(w, np.array([0, nt // 2, nt - 1], np.int32))[3]
+    per_tile = max((t3 - t1) / 2.0, 1e-3)
+    fixed = max(t1 - per_tile, 0.0)
+    k = int(max(1, min(nt, (target - fixed) / per_tile)))
+    tiles, _ = sample_tiles(w, k / nt)
+    for _ in range(args.warmup):
+        oracle_sample(w, tiles)
+    times = []
+    for _ in range(args.steps):
+        times.append(oracle_sample(w, tiles)[3])
+    px = int(tile_mask(w, tiles).sum()) * P
+    ms = 1000.0 * float(np.mean(times))
+    value = px / (ms / 1000.0)
+    cores = os.cpu_count()
+    sample = (f"{len(tiles)} of {nt} tiles ({px // P} px x {P} sub-boxes) of {args.config}, "
+              f"evenly spaced; each step = full per-Gaussian setup + those tiles")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {w.description}", "N_gaussians": w.N,
+                       "res": f"{w.camera['W']}x{w.camera['H']}", "sub_boxes": P,
+                       "tile": w.tile},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def count_launches(step):
+    """Kernel launches of one step, from the CUDA activity trace (torch.profiler / CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        n = 0
+        names = {}
+        for e in prof.events():
+            dt = getattr(e, "device_type", None)
+            if dt is not None and "CUDA" in str(dt) and not e.name.startswith(("Memcpy", "Memset")):
+                n += 1
+                names[e.name] = names.get(e.name, 0) + 1
+        return n, names
+    except Exception as ex:  # pragma: no cover
+        return None, {"error": str(ex)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_00308_b200 import Context
+    from paper_2503_00308_b200.dist import ShardedRenderer
+    from workloads import make_config
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = local
+    w = make_config(args.config)
+    tile = args.tile or w.tile
+    batch = args.batch or w.batch
+    P = w.n_sub
+    H, W = w.camera["H"], w.camera["W"]
+    ctx = Context(dev)
+    ctx.load_workload(w)
+    lo = torch.empty((H, W, 3), dtype=torch.float32, device=f"cuda:{dev}")
+    hi = torch.empty_like(lo)
+    sr = ShardedRenderer(ctx, rank, world, tile=tile, batch=batch) if world > 1 else None
+
+    def step(stats=True):
+        if sr is None:
+            return ctx.as_render_bounds(tile, batch, lo, hi, stats=stats)[2]
+        return sr.step(stats=stats)[2]
+
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def timed():
+        total, tile_ms, st_last = 0.0, 0.0, None
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(args.steps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0.record()
+            st = step()
+            e1.record()
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1)
+            tile_ms += st["tile_kernel_ms"]
+            st_last = st
+        return total, tile_ms, st_last
+
+    with ClockSampler(dev) as cs:
+        total, tile_ms, st = timed()
+    clocks = cs.summary()
+    if clocks_bad(clocks):  # re-measure once
+        with ClockSampler(dev) as cs:
+            total, tile_ms, st = timed()
+        clocks = cs.summary()
+        clocks["remeasured"] = True
+    ms = total / args.steps
+    tile_ms_step = tile_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms, tile_ms_step], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, tile_ms_step = float(t[0]), float(t[1])
+    value = W * H * P / (ms / 1000.0)
+
+    # ---- roofline of k_tile (FP32 issue bound), this rank's share
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_ops = SM_COUNT * FP32_LANES * sm_max * 1e6
+    n = st["n_vars"]
+    ops_step = f_ops(n) * st["active_pairs"]
+    achieved = ops_step / (st["tile_kernel_ms"] / 1000.0) if st["tile_kernel_ms"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("k_tile_dram_bytes_per_launch")
+    roofline = {"bound": "alu", "kernel": "k_tile", "achieved": achieved / 1e12,
+                "peak": peak_ops / 1e12, "unit": "Tops/s (FP32 instr, FMA=1)",
+                "frac": achieved / peak_ops, "traffic": traffic,
+                "ops_per_active_pair": f_ops(n), "active_pairs_per_step": st["active_pairs"],
+                "tile_kernel_ms_per_step": st["tile_kernel_ms"], "launches_per_step": P,
+                "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES} FP32 lanes x {sm_max:.0f} MHz "
+                              "(MEASURED_PEAKS.json sm_max_mhz)",
+                "frac_at_measured_clock": (achieved / (SM_COUNT * FP32_LANES * clocks["sm_mhz"] * 1e6)
+                                           if clocks.get("sm_mhz") else None),
+                "share_of_step": st["tile_kernel_ms"] / ms if ms > 0 else None}
+
+    # ---- launches
+    n_launch, names = count_launches(step)
+    gpu_launches = n_launch * args.steps if n_launch is not None else st["launches"] * args.steps
+
+    # ---- e2e: through the C ABI with host buffers (pinned scene in, bound images out)
+    e2e = None
+    if not args.no_e2e:
+        import torch as T
+        mean = T.from_numpy(w.mean).pin_memory()
+        chol = T.from_numpy(w.chol).pin_memory()
+        opac = T.from_numpy(w.opacity).pin_memory()
+        col = T.from_numpy(w.color).pin_memory()
+        hlo = T.empty((H, W, 3), dtype=T.float32).pin_memory()
+        hhi = T.empty_like(hlo).pin_memory()
+
+        def e2e_step():
+            ctx.as_load_scene(mean, chol, opac, col)
+            ctx.as_set_scene_box(w.scene_box)
+            if sr is None:
+                ctx.as_render_bounds(tile, batch, hlo, hhi, stats=False)
+            else:
+                olo, ohi, _ = sr.step(stats=False)
+                if rank == 0:
+                    hlo.copy_(olo)
+                    hhi.copy_(ohi)
+        e2e_step()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        e_ms = 1000.0 * float(np.mean(times))
+        if world > 1:
+            t = torch.tensor([e_ms], device=f"cuda:{dev}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": W * H * P / (e_ms / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(w.N * 52 * world + (0 if w.scene_box is None else
+                                                            w.N * 28)),
+               "d2h_bytes_per_step": int(2 * H * W * 3 * 4), "ms_per_step": e_ms,
+               "timing": "host wall clock around synchronous C-ABI calls"}
+        ctx.load_workload(w)  # restore the device-resident state
+
+    # ---- bound widths (metric part 2) and CPU baseline (rank 0, N=1)
+    out = None
+    if rank == 0:
+        lo_np = lo.cpu().numpy().astype(np.float64) if sr is None else None
+        if sr is not None:
+            a, b, _ = sr.step(stats=False)
+            lo_np, hi_np = a.cpu().numpy().astype(np.float64), b.cpu().numpy().astype(np.float64)
+        else:
+            hi_np = hi.cpu().numpy().astype(np.float64)
+        gap = np.linalg.norm(hi_np - lo_np, axis=-1)
+        widths = {"mpg": float(gap.mean()), "xpg": float(gap.max()),
+                  "mean_channel_width": float((hi_np - lo_np).mean())}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            tiles, nt = sample_tiles(w, SAMPLE_FRACTION.get(args.config, 0.05))
+            olo, ohi, ost, dt = oracle_sample(w, tiles)
+            m = tile_mask(w, tiles)
+            px = int(m.sum()) * P
+            cpu = {"value": px / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"{len(tiles)} of {nt} tiles of {args.config} ({int(m.sum())} px x "
+                             f"{P} sub-boxes), evenly spaced, incl. the full per-Gaussian setup",
+                   "seconds": dt}
+            d = np.maximum(np.abs(lo_np[m] - olo[m]), np.abs(hi_np[m] - ohi[m]))
+            og = np.linalg.norm(ohi[m] - olo[m], axis=-1)
+            widths.update({"oracle_sample_mpg": float(og.mean()),
+                           "gpu_sample_mpg": float(gap[m].mean()),
+                           "max_abs_diff_vs_oracle_sample": float(d.max())})
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32", "data": "synthetic",
+               "config": {"workload": f"{args.config}: {w.description}", "N_gaussians": w.N,
+                          "res": f"{W}x{H}", "n_vars": n, "sub_boxes": P, "tile": tile,
+                          "batch": batch, "setup_dtype": "f64",
+                          "l2": "flushed before every timed step (512 MiB write)",
+                          "parallelism": f"image tiles over {world} GPU(s), LPT owner map, "
+                                         "one all-gather"},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": gpu_launches, "launch_kernels": names, "clocks": clocks,
+               "bound_width": widths,
+               "stats": {k: st[k] for k in ("pairs", "active_pairs", "uncertain_pairs", "fails",
+                                            "straddles", "dropped", "kmax", "ms_setup", "ms_bin",
+                                            "ms_pairs", "ms_tile", "device_bytes", "n_items",
+                                            "grid", "ring_len", "max_window")}}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warmup raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

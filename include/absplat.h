@@ -101,6 +101,10 @@ typedef struct {
   double ms_pose, ms_setup, ms_bin, ms_pairs, ms_tile, ms_total;
   double tile_kernel_ms;   /* sum of k_tile durations */
   size_t device_bytes;     /* bytes currently held by the context */
+  int32_t n_items;         /* (tile, chunk) work items of the last sub-box */
+  int32_t grid;            /* persistent CTAs of the tile kernel (last sub-box) */
+  int32_t ring_len;        /* exception ring length R (last sub-box; 1 = no exceptions) */
+  int32_t max_window;      /* longest exception window, positions (max over sub-boxes) */
 } as_stats;
 
 /* Flags */

@@ -45,7 +45,8 @@ class AsStats(C.Structure):
                 ("n_tiles", C.c_int32), ("ms_pose", C.c_double), ("ms_setup", C.c_double),
                 ("ms_bin", C.c_double), ("ms_pairs", C.c_double), ("ms_tile", C.c_double),
                 ("ms_total", C.c_double), ("tile_kernel_ms", C.c_double),
-                ("device_bytes", C.c_size_t)]
+                ("device_bytes", C.c_size_t), ("n_items", C.c_int32), ("grid", C.c_int32),
+                ("ring_len", C.c_int32), ("max_window", C.c_int32)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

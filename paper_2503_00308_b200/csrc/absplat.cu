@@ -52,9 +52,13 @@ struct as_ctx {
   DevBuf pose, hot, pair, kkey, kkey2, kval, order, counts, offsets, cub_tmp;
   DevBuf keys, keys2, vals, vals2, tbegin, tend, tcost, tkey, tkey2, tids, tlist, tslot, owner;
   DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
+  DevBuf tileh, tilemax, wsP, kapP;
+  DevBuf item_off, items, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
+  DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
   size_t bytes = 0;
   int64_t launches = 0;
+  int last_items = 0, last_grid = 0, last_R = 1, max_window = 0;
   cudaEvent_t ev[8] = {};
   bool events = false;
 };
@@ -321,7 +325,7 @@ __global__ void k_slot_map(const int32_t* list, int n, int32_t* slot_of_tile) {
 
 // counters layout (unsigned long long[16])
 enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6, C_UNC = 8,
-       C_VIOL = 9, C_NCOUNTERS = 16 };
+       C_VIOL = 9, C_WMAX = 10, C_NCOUNTERS = 16 };
 
 int64_t read_i64(as_ctx* ctx, const int64_t* dptr) {
   int64_t v = 0;
@@ -397,12 +401,17 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   if (pt) CK(cudaEventRecord(ctx->ev[3], st));
   // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
   TileArgs ta{};
-  ta.pflag = nullptr;
+  bool has_exc = false;
+  int R = 1;
   if (nv > 0 && M > 0) {
     ensure(ctx, ctx->nF, sizeof(int32_t) * M);
     ensure(ctx, ctx->nG, sizeof(int32_t) * M);
     ensure(ctx, ctx->ntot, sizeof(int64_t) * (M + 1));
     ensure(ctx, ctx->eoff, sizeof(int64_t) * (M + 1));
+    ensure(ctx, ctx->wsP, sizeof(double) * M);
+    ensure(ctx, ctx->kapP, sizeof(double) * M);
+    ensure(ctx, ctx->tileh, sizeof(double) * (NVMAX + 1) * G.ntiles);
+    ensure(ctx, ctx->tilemax, sizeof(unsigned long long) * G.ntiles);
     PairArgs pa{};
     pa.keys = skeys;
     pa.vals = svals;
@@ -410,13 +419,26 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     pa.tend = P<int64_t>(ctx->tend);
     pa.M = M;
     pa.pair = ctx->pair.p;
-    pa.wsmax = ctr + C_WSMAX;
     pa.nv = nv;
+    pa.pose = P<PoseDev>(ctx->pose) + s;
+    pa.fx = ctx->cam.fx;
+    pa.fy = ctx->cam.fy;
+    pa.cx = ctx->cam.cx;
+    pa.cy = ctx->cam.cy;
+    pa.ts = G.ts;
+    pa.ntx = G.ntx;
+    pa.ntiles = G.ntiles;
+    pa.tileh = P<double>(ctx->tileh);
+    pa.tilemax = P<unsigned long long>(ctx->tilemax);
+    pa.wsP = P<double>(ctx->wsP);
+    pa.kapP = P<double>(ctx->kapP);
     pa.nF = P<int32_t>(ctx->nF);
     pa.nG = P<int32_t>(ctx->nG);
     pa.ntot = P<int64_t>(ctx->ntot);
     pa.counters = ctr + C_UNC;
     CK(cudaMemsetAsync(pa.ntot + M, 0, sizeof(int64_t), st));
+    launch_pairs_prep(pa, st);
+    LAUNCHED(ctx, 2);
     launch_pairs_count(pa, st);
     LAUNCHED(ctx, 1);
     cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
@@ -425,54 +447,103 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       pa.off = P<int64_t>(ctx->eoff);
       ensure(ctx, ctx->exc, sizeof(int32_t) * nexc);
       ensure(ctx, ctx->hpos, sizeof(int32_t) * M);
-      ensure(ctx, ctx->diff, sizeof(int32_t) * (M + 1));
-      ensure(ctx, ctx->cover, sizeof(int32_t) * (M + 1));
-      ensure(ctx, ctx->pflag, sizeof(int32_t) * M);
-      ensure(ctx, ctx->is_store, sizeof(int32_t) * (M + 1));
-      ensure(ctx, ctx->slot, sizeof(int32_t) * (M + 1));
+      ensure(ctx, ctx->diff, sizeof(int32_t) * 2 * (M + 1));
+      ensure(ctx, ctx->cover, sizeof(int32_t) * 2 * (M + 1));
+      ensure(ctx, ctx->pflag, sizeof(int4) * M);
       pa.exc = P<int32_t>(ctx->exc);
       pa.hpos = P<int32_t>(ctx->hpos);
       launch_pairs_fill(pa, st);
       LAUNCHED(ctx, 1);
-      CK(cudaMemsetAsync(ctx->diff.p, 0, sizeof(int32_t) * (M + 1), st));
-      launch_mark(pa, P<int32_t>(ctx->diff), st);
+      int32_t* dstore = P<int32_t>(ctx->diff);
+      int32_t* dcut = dstore + (M + 1);
+      int32_t* cstore = P<int32_t>(ctx->cover);
+      int32_t* ccut = cstore + (M + 1);
+      CK(cudaMemsetAsync(dstore, 0, sizeof(int32_t) * 2 * (M + 1), st));
+      launch_mark(pa, dstore, dcut, st);
       LAUNCHED(ctx, 1);
-      cub_inclusive_sum(ctx, P<int32_t>(ctx->diff), P<int32_t>(ctx->cover), M + 1);
-      CK(cudaMemsetAsync(P<int32_t>(ctx->is_store) + M, 0, sizeof(int32_t), st));
-      launch_flags(pa, P<int32_t>(ctx->cover), P<int32_t>(ctx->pflag), P<int32_t>(ctx->is_store),
-                   st);
+      cub_inclusive_sum(ctx, dstore, cstore, M + 1);
+      cub_inclusive_sum(ctx, dcut, ccut, M + 1);
+      unsigned int* wmax = reinterpret_cast<unsigned int*>(ctr + C_WMAX);
+      CK(cudaMemsetAsync(wmax, 0, sizeof(unsigned long long), st));
+      ensure(ctx, ctx->finkey, sizeof(uint32_t) * M);
+      ensure(ctx, ctx->finkey2, sizeof(uint32_t) * M);
+      ensure(ctx, ctx->finval, sizeof(int32_t) * M);
+      ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
+      ensure(ctx, ctx->fin_b, sizeof(int32_t) * M);
+      ensure(ctx, ctx->fin_e, sizeof(int32_t) * M);
+      launch_meta(pa, cstore, ccut, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
+                  P<int32_t>(ctx->finval), st);
       LAUNCHED(ctx, 1);
-      cub_exclusive_sum(ctx, P<int32_t>(ctx->is_store), P<int32_t>(ctx->slot), M + 1);
-      int32_t nslots = 0;
-      CK(cudaMemcpyAsync(&nslots, P<int32_t>(ctx->slot) + M, sizeof nslots,
-                         cudaMemcpyDeviceToHost, st));
+      cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
+                      P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
+      launch_fin_ranges(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->fin_b),
+                        P<int32_t>(ctx->fin_e), st);
+      LAUNCHED(ctx, 1);
+      ta.fin_b = P<int32_t>(ctx->fin_b);
+      ta.fin_e = P<int32_t>(ctx->fin_e);
+      ta.fin_val = P<int32_t>(ctx->finval2);
+      unsigned int hw = 0;
+      CK(cudaMemcpyAsync(&hw, wmax, sizeof hw, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      ensure(ctx, ctx->scratch, sizeof(float4) * (size_t)std::max(nslots, 1) * G.ts * G.ts);
-      ta.pflag = P<int32_t>(ctx->pflag);
-      ta.slot = P<int32_t>(ctx->slot);
-      ta.eoff = P<int64_t>(ctx->eoff);
-      ta.nF = P<int32_t>(ctx->nF);
+      while (R <= (int)hw) R <<= 1;
+      ctx->max_window = std::max(ctx->max_window, (int)hw);
+      has_exc = true;
+      ta.pm = P<int4>(ctx->pflag);
       ta.nG = P<int32_t>(ctx->nG);
+      ta.eoff = P<int64_t>(ctx->eoff);
       ta.exc = P<int32_t>(ctx->exc);
-      ta.hpos = P<int32_t>(ctx->hpos);
-      ta.scratch = P<float4>(ctx->scratch);
     }
   }
   if (pt) CK(cudaEventRecord(ctx->ev[4], st));
-  // ---- tile order: descending Gaussian count (longest tiles first)
-  k_tile_keys<<<(n_list + 255) / 256, 256, 0, st>>>(tlist, n_list, P<int64_t>(ctx->tbegin),
-                                                    P<int64_t>(ctx->tend), P<uint32_t>(ctx->tkey));
+  // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
+  int grid = tile_grid(nv, G.ts, bs);
+  const size_t npix = (size_t)G.ts * G.ts;
+  if (has_exc) {  // ring memory: grid x R x npix float4 (cap the total at ~8 GB)
+    const size_t per = (size_t)R * npix * sizeof(float4);
+    const size_t budget = (size_t)8 << 30;
+    if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
+    ensure(ctx, ctx->scratch, (size_t)grid * per);
+  }
+  const int target = (int)std::max<int64_t>(2 * bs, M / ((int64_t)grid * 6) + 1);
+  int64_t* caps = P<int64_t>(ctx->ntot);  // reuse: int64 [ntiles+1]
+  ensure(ctx, ctx->ntot, sizeof(int64_t) * (std::max<int64_t>(M, G.ntiles) + 1));
+  caps = P<int64_t>(ctx->ntot);
+  ensure(ctx, ctx->item_off, sizeof(int64_t) * (G.ntiles + 1));
+  launch_item_caps(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), G.ntiles, target, caps, st);
   LAUNCHED(ctx, 1);
-  cub_sort_keys32(ctx, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tkey2),
-                  const_cast<int32_t*>(tlist), P<int32_t>(ctx->tids), n_list, 32, true);
-  // ---- a8-a10: the tile kernel
+  CK(cudaMemsetAsync(caps + G.ntiles, 0, sizeof(int64_t), st));
+  cub_exclusive_sum(ctx, caps, P<int64_t>(ctx->item_off), G.ntiles + 1);
+  const int64_t n_items = read_i64(ctx, P<int64_t>(ctx->item_off) + G.ntiles);
+  ensure(ctx, ctx->items, sizeof(int4) * n_items);
+  ensure(ctx, ctx->item_key, sizeof(uint32_t) * n_items);
+  ensure(ctx, ctx->item_key2, sizeof(uint32_t) * n_items);
+  ensure(ctx, ctx->item_idx, sizeof(int32_t) * n_items);
+  ensure(ctx, ctx->item_order, sizeof(int32_t) * n_items);
+  ensure(ctx, ctx->item_cnt, sizeof(int32_t) * G.ntiles);
+  ensure(ctx, ctx->partial, sizeof(float) * 8 * npix * n_items);
+  launch_chunks(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), has_exc ? P<int4>(ctx->pflag) : nullptr,
+                P<int64_t>(ctx->item_off), G.ntiles, target, owner, rank, P<int4>(ctx->items),
+                P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
+  LAUNCHED(ctx, 1);
+  k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
+  LAUNCHED(ctx, 1);
+  cub_sort_keys32(ctx, P<uint32_t>(ctx->item_key), P<uint32_t>(ctx->item_key2),
+                  P<int32_t>(ctx->item_idx), P<int32_t>(ctx->item_order), n_items, 32, true);
+  ensure(ctx, ctx->work_counter, sizeof(int));
+  CK(cudaMemsetAsync(ctx->work_counter.p, 0, sizeof(int), st));
+  // ---- a8-a10: the tile kernel (+ merge of split tiles)
   ta.hot = ctx->hot.p;
   ta.vals = svals;
   ta.tbegin = P<int64_t>(ctx->tbegin);
   ta.tend = P<int64_t>(ctx->tend);
-  ta.tile_list = P<int32_t>(ctx->tids);
+  ta.items = P<int4>(ctx->items);
+  ta.order = P<int32_t>(ctx->item_order);
+  ta.n_items = (int)n_items;
+  ta.counter = P<int>(ctx->work_counter);
+  ta.item_off = P<int64_t>(ctx->item_off);
+  ta.item_cnt = P<int32_t>(ctx->item_cnt);
   ta.tile_slot = tslot;
-  ta.n_list = n_list;
+  ta.ntiles = G.ntiles;
   ta.ts = G.ts;
   ta.ntx = G.ntx;
   ta.W = ctx->cam.W;
@@ -480,21 +551,33 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.bs = bs;
   ta.first = first ? 1 : 0;
   ta.ntau = (float)((double)N * TAU);
+  ta.ring = has_exc ? P<float4>(ctx->scratch) : nullptr;
+  ta.R = R;
+  ta.partial = P<float>(ctx->partial);
   ta.lo = lo;
   ta.hi = hi;
   ta.active = ctr + C_ACTIVE;
-  launch_tile(nv, ta, st);
+  ctx->last_items = (int)n_items;
+  ctx->last_grid = grid;
+  ctx->last_R = R;
+  if (pt) CK(cudaEventRecord(ctx->ev[7], st));
+  launch_tile(nv, ta, grid, st);
   LAUNCHED(ctx, 1);
+  if (pt) CK(cudaEventRecord(ctx->ev[5], st));
+  launch_merge(ta, st);
+  LAUNCHED(ctx, 1);
+  (void)tlist;
+  (void)n_list;
   if (pt) {
-    CK(cudaEventRecord(ctx->ev[5], st));
     CK(cudaEventSynchronize(ctx->ev[5]));
-    float a = 0, b = 0, c = 0, d = 0;
+    float a = 0, b = 0, c = 0, d = 0, e = 0;
     CK(cudaEventElapsedTime(&a, ctx->ev[1], ctx->ev[2]));
     CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
     CK(cudaEventElapsedTime(&c, ctx->ev[3], ctx->ev[4]));
-    CK(cudaEventElapsedTime(&d, ctx->ev[4], ctx->ev[5]));
+    CK(cudaEventElapsedTime(&e, ctx->ev[4], ctx->ev[7]));
+    CK(cudaEventElapsedTime(&d, ctx->ev[7], ctx->ev[5]));
     pt->setup += a;
-    pt->bin += b;
+    pt->bin += b + e;
     pt->pairs += c;
     pt->tile += d;
   }
@@ -594,6 +677,10 @@ void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_r
   out->tile_kernel_ms = pt.tile;
   out->ms_total = total_ms;
   out->device_bytes = ctx->bytes;
+  out->n_items = ctx->last_items;
+  out->grid = ctx->last_grid;
+  out->ring_len = ctx->last_R;
+  out->max_window = ctx->max_window;
   (void)G;
 }
 
@@ -703,7 +790,11 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->tids, &ctx->tlist, &ctx->tslot, &ctx->owner, &ctx->nF, &ctx->nG,
                     &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->diff, &ctx->cover,
                     &ctx->pflag, &ctx->is_store, &ctx->slot, &ctx->scratch, &ctx->img_lo,
-                    &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map};
+                    &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map, &ctx->tileh,
+                    &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->item_off, &ctx->items,
+                    &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
+                    &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
+                    &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e};
   for (DevBuf* b : bufs) release(ctx, *b);
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
@@ -930,6 +1021,7 @@ as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, 
     cudaStream_t s = ctx->stream;
     const Geometry G = geometry(ctx, tile);
     ctx->launches = 0;
+    ctx->max_window = 0;
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
     const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
@@ -1026,6 +1118,7 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       return AS_E_ARG;
     }
     ctx->launches = 0;
+    ctx->max_window = 0;
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
     // ---- owner map (identical on every rank): LPT over per-tile pair counts

@@ -22,7 +22,9 @@ constexpr int KTAYLOR = 8;      // MatrixInv order
 constexpr double WCAP = 1e12;   // |W| guard -> FAIL (reading O3)
 
 enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4 };
-enum : int { P_EXC = 1, P_STORE = 2 };  // per list-position flags (exceptions, a9)
+// per list-position flags (exceptions, a9) and work-item flags
+enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8 };
+enum : int { IT_EXC = 1, IT_SINGLE = 2 };
 
 // ------------------------------------------------------------------------- pose / box
 // One sub-box: the perturbed axes in canonical order with their centre and radius.
@@ -253,8 +255,15 @@ struct PairArgs {
   const int64_t* tend;
   int64_t M;
   const void* pair;       // PairRec<NV>[N]
-  const unsigned long long* wsmax;
   int nv;
+  // slope-aware window (a7): per tile the depth slope model m(kappa) = g0 + kappa h_T
+  const PoseDev* pose;    // sub-box pose forms (R slopes, translation slope g0)
+  double fx, fy, cx, cy;
+  int ts, ntx, ntiles;
+  double* tileh;          // [ntiles][NVMAX+1]: h_T and, at [NVMAX], 1 - |h_T|_1 (0 = no pruning)
+  unsigned long long* tilemax;  // [ntiles] max over the tile's list of w + S' (ordered bits)
+  double* wsP;            // [M] w + S' of the Gaussian at each position
+  double* kapP;           // [M] kappa at each position
   int32_t* nF;            // [M]
   int32_t* nG;            // [M]
   int64_t* ntot;          // [M+1] nF + nG (scanned into off)
@@ -263,40 +272,57 @@ struct PairArgs {
   int32_t* hpos;          // [M] first position of E_F (tile-local) or own position
   unsigned long long* counters;  // [0] uncertain pairs, [1] order violations
 };
+void launch_pairs_prep(const PairArgs& a, cudaStream_t st);
 void launch_pairs_count(const PairArgs& a, cudaStream_t st);
 void launch_pairs_fill(const PairArgs& a, cudaStream_t st);
-void launch_mark(const PairArgs& a, int32_t* diff, cudaStream_t st);
-void launch_flags(const PairArgs& a, const int32_t* cover, int32_t* pflag, int32_t* is_store,
-                  cudaStream_t st);
+void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t st);
+void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st);
+void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe, cudaStream_t st);
+void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
+                      int64_t* caps, cudaStream_t st);
+void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
+                   const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
+                   int4* items, int32_t* item_cnt, uint32_t* item_key, cudaStream_t st);
 
 struct TileArgs {
   const void* hot;            // HotRec<NV>[N]
   const int32_t* vals;        // [M] Gaussian ids in (tile, kappa, index) order
   const int64_t* tbegin;
   const int64_t* tend;
-  const int32_t* tile_list;   // tiles to render (cost-descending), [n_list]
+  // work items: {tile, begin, end (tile-local positions), flags}, processed in `order`
+  const int4* items;
+  const int32_t* order;       // item indices, longest first
+  int n_items;
+  int* counter;               // dynamic work counter (zeroed before the launch)
+  const int64_t* item_off;    // [ntiles+1] first item of each tile
+  const int32_t* item_cnt;    // [ntiles] items per tile
   const int32_t* tile_slot;   // output slot of each tile id (tile-major) or nullptr
-  int n_list;
+  int ntiles;
   int ts, ntx, W, H;
   int bs;
   int first;                  // first sub-box: store instead of union
   float ntau;                 // N * tau slack
-  // exceptions
-  const int32_t* pflag;       // [M] or nullptr
-  const int32_t* slot;        // [M] scratch slot of stored positions
+  // exceptions (nullptr when the sub-box has no uncertain pair)
+  const int4* pm;             // [M] {flags, h, g, nF} (tile-local positions)
+  const int32_t* nG;          // [M]
   const int64_t* eoff;        // [M+1]
-  const int32_t* nF;
-  const int32_t* nG;
-  const int32_t* exc;
-  const int32_t* hpos;
-  float4* scratch;            // [slots][ts*ts]
+  const int32_t* exc;         // E_F ascending then E_G ascending, tile-local
+  const int32_t* fin_b;       // [M] positions whose deferred T_lo is finalised here:
+  const int32_t* fin_e;       //     fin_val[fin_b[p] .. fin_e[p]) (global positions)
+  const int32_t* fin_val;
+  float4* ring;               // [gridDim][R][ts*ts] (T_hi before, 1-a_lo, 1-a_hi, deferred)
+  int R;                      // ring length (power of two > max window)
+  float* partial;             // [items][ts*ts][8] chunk partials (multi-chunk tiles)
   // outputs
   float* lo;                  // row-major [H][W][3] (tile_slot == nullptr) or tile-major
   float* hi;
   unsigned long long* active; // active pair counter
 };
-void launch_tile(int nv, const TileArgs& a, cudaStream_t st);
+void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st);
+void launch_merge(const TileArgs& a, cudaStream_t st);
 int tile_threads(int ts);
+int tile_grid(int nv, int ts, int bs);
 size_t tile_smem_bytes(int nv, int ts, int bs);
 
 // concrete renderer (tests)

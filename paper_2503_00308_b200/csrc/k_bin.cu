@@ -159,10 +159,65 @@ __device__ __forceinline__ PairRec<NV> load_pair(const void* base, int32_t g) {
   return reinterpret_cast<const PairRec<NV>*>(base)[g];
 }
 
-// Window bound: a '?' pair (j before i) needs kappa_i - kappa_j <= ws_i + ws_j <= ws_i + M.
-__device__ __forceinline__ bool beyond(double dk, double wsi, double M, double ki, double kj) {
+// Window bound (SURVEY §8(c) step 13 pruning, slope-aware).  For any vector h and
+// m_i = g0 + kappa_i h:  |lA_i - uA_j|_1 <= S'_i + |kappa_i - kappa_j| |h|_1 + S'_j with
+// S'_i = max(|lA_i - m_i|_1, |uA_i - m_i|_1).  A '?' pair (j before i) needs
+// kappa_i - kappa_j <= w_i + w_j + |lA_i - uA_j|_1, hence
+// (kappa_i - kappa_j)(1 - |h|_1) <= ws'_i + ws'_j <= ws'_i + M_T (and symmetrically forward).
+// h_T = depth slope per unit depth of the rotation variables along the tile's centre ray
+// (d = R_2 (P - t) and P - t = d R^T ray), so Gaussians of similar depth in the tile have
+// slopes close to m(kappa) and the window shrinks to about the form widths.
+__global__ void k_tile_h(PairArgs A) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.ntiles) return;
+  const PoseDev& P = *A.pose;
+  const int tx = t % A.ntx, ty = t / A.ntx;
+  const double ray[3] = {((tx + 0.5) * A.ts - A.cx) / A.fx, ((ty + 0.5) * A.ts - A.cy) / A.fy, 1.0};
+  // world direction R^T ray with R the centre rotation (mid of the constant terms)
+  double wd[3];
+  for (int b = 0; b < 3; ++b) {
+    double v = 0.0;
+    for (int a = 0; a < 3; ++a) v += 0.5 * (P.Rl[3 * a + b][NVMAX] + P.Ru[3 * a + b][NVMAX]) * ray[a];
+    wd[b] = v;
+  }
+  double* h = A.tileh + (size_t)t * (NVMAX + 1);
+  double norm = 0.0;
+  for (int k = 0; k < NVMAX; ++k) {
+    double v = 0.0;
+    if (k < P.n)
+      for (int b = 0; b < 3; ++b) v += P.Rl[6 + b][k] * wd[b];  // row 2 of R, slope k
+    h[k] = v;
+    norm += fabs(v);
+  }
+  h[NVMAX] = (norm < 0.5) ? (1.0 - norm) : 0.0;
+  A.tilemax[t] = 0ull;
+}
+
+template <int NV>
+__global__ void k_pairs_prep(PairArgs A) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.M) return;
+  const uint32_t t = A.keys[p];
+  const PairRec<NV> Pi = load_pair<NV>(A.pair, A.vals[p]);
+  const double* h = A.tileh + (size_t)t * (NVMAX + 1);
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double m = A.pose->gslope[k] + Pi.kappa * h[k];
+    s1 += fabs(Pi.dl[k] - m);
+    s2 += fabs(Pi.du[k] - m);
+  }
+  const double ws = 0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2);
+  A.wsP[p] = ws;
+  A.kapP[p] = Pi.kappa;
+  atomicMax(&A.tilemax[t], (unsigned long long)__double_as_longlong(ws));
+}
+
+// true when every later/earlier candidate is certainly ordered (the scan can stop)
+__device__ __forceinline__ bool beyond(double dk, double factor, double wsi, double M, double ki,
+                                       double kj) {
   const double bound = (wsi + M) * (1.0 + 1e-9) + 1e-12 * (fabs(ki) + fabs(kj)) + 1e-300;
-  return dk > bound;
+  return dk * factor * (1.0 - 1e-9) > bound;
 }
 
 template <int NV, int PASS>  // PASS 0: count, 1: fill
@@ -173,7 +228,9 @@ __global__ void k_pairs(PairArgs A) {
   const int64_t b = A.tbegin[t], e = A.tend[t];
   const int32_t gi = A.vals[p];
   const PairRec<NV> Pi = load_pair<NV>(A.pair, gi);
-  const double M = __longlong_as_double((long long)*A.wsmax);
+  const double M = __longlong_as_double((long long)A.tilemax[t]);
+  const double factor = A.tileh[(size_t)t * (NVMAX + 1) + NVMAX];
+  const double wsi = A.wsP[p];
   int nF = 0, nG = 0, viol = 0;
   int64_t off = 0;
   int nFt = 0;
@@ -184,9 +241,10 @@ __global__ void k_pairs(PairArgs A) {
   int hmin = (int)(p - b);
   // backward: earlier positions (expected Ind in {1, ?})
   for (int64_t q = p - 1; q >= b; --q) {
+    const double kj = A.kapP[q];
+    if (beyond(Pi.kappa - kj, factor, wsi, M, Pi.kappa, kj)) break;
     const int32_t gj = A.vals[q];
     const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
-    if (beyond(Pi.kappa - Pj.kappa, Pi.ws, M, Pi.kappa, Pj.kappa)) break;
     const int c = ind_class<NV>(Pi, gi, Pj, gj);
     if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
       if (c == 0) ++viol;
@@ -197,9 +255,10 @@ __global__ void k_pairs(PairArgs A) {
   }
   // forward: later positions (expected Ind in {0, ?})
   for (int64_t q = p + 1; q < e; ++q) {
+    const double kj = A.kapP[q];
+    if (beyond(kj - Pi.kappa, factor, wsi, M, Pi.kappa, kj)) break;
     const int32_t gj = A.vals[q];
     const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
-    if (beyond(Pj.kappa - Pi.kappa, Pi.ws, M, Pi.kappa, Pj.kappa)) break;
     const int c = ind_class<NV>(Pi, gi, Pj, gj);
     if (c == -1 || c == 1) {
       if (c == 1) ++viol;
@@ -218,6 +277,13 @@ __global__ void k_pairs(PairArgs A) {
   }
 }
 
+void launch_pairs_prep(const PairArgs& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  k_tile_h<<<(a.ntiles + 127) / 128, 128, 0, st>>>(a);
+  const unsigned blocks = (unsigned)((a.M + 255) / 256);
+  NV_SWITCH(a.nv, (k_pairs_prep<NVc><<<blocks, 256, 0, st>>>(a)));
+}
+
 void launch_pairs_count(const PairArgs& a, cudaStream_t st) {
   if (a.M <= 0) return;
   const unsigned blocks = (unsigned)((a.M + 127) / 128);
@@ -229,34 +295,145 @@ void launch_pairs_fill(const PairArgs& a, cudaStream_t st) {
   NV_SWITCH(a.nv, (k_pairs<NVc, 1><<<blocks, 128, 0, st>>>(a)));
 }
 
-// exceptional position p needs scratch entries on [tile_begin + h_p, p] (its T_hi window,
-// which contains E_F(p)) and at every element of E_G(p) (those are exceptional themselves
-// and mark their own windows, which contain their position).
-__global__ void k_mark(PairArgs A, int32_t* diff) {
+// Exception metadata (a7 -> a9).  For a position p with uncertain partners:
+//   * its T_hi window [h_p, p] (h_p = min E_F(p), or p) must be kept in the ring: every
+//     position inside some window is flagged PM_STORE (difference array `dstore`);
+//   * a chunk boundary between b-1 and b must not separate an uncertain pair (q < b <= p):
+//     positions b in (h_p, p] are flagged PM_NOCUT (difference array `dcut`).
+__global__ void k_mark(PairArgs A, int32_t* dstore, int32_t* dcut) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
-  if (A.nF[p] + A.nG[p] == 0) return;
+  const int nF = A.nF[p], nG = A.nG[p];
+  if (nF + nG == 0) return;
   const int64_t b = A.tbegin[A.keys[p]];
-  atomicAdd(&diff[b + A.hpos[p]], 1);
-  atomicAdd(&diff[p + 1], -1);
+  const int h = A.hpos[p];
+  atomicAdd(&dstore[b + h], 1);
+  atomicAdd(&dstore[p + 1], -1);
+  if (nF > 0) {
+    atomicAdd(&dcut[b + h + 1], 1);
+    atomicAdd(&dcut[p + 1], -1);
+  }
 }
-void launch_mark(const PairArgs& a, int32_t* diff, cudaStream_t st) {
+void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t st) {
   if (a.M <= 0) return;
-  k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, diff);
+  k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, dstore, dcut);
 }
 
-__global__ void k_flags(PairArgs A, const int32_t* cover, int32_t* pflag, int32_t* is_store) {
+// per-position metadata for the tile kernel: {flags, h, g, nF}; max window -> wmax
+__global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, int4* pm,
+                       unsigned int* wmax, uint32_t* finkey, int32_t* finval) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
-  const bool exc = (A.nF[p] + A.nG[p]) > 0;
-  const bool store = cover[p] > 0;
-  pflag[p] = (exc ? P_EXC : 0) | (store ? P_STORE : 0);
-  is_store[p] = store ? 1 : 0;
+  const int nF = A.nF[p], nG = A.nG[p];
+  const int64_t b = A.tbegin[A.keys[p]];
+  const int loc = (int)(p - b);
+  const int h = (nF + nG) ? A.hpos[p] : loc;
+  const int g = nG ? A.exc[A.off[p] + nF + nG - 1] : loc;
+  int fl = (nF ? PM_EF : 0) | (nG ? PM_EG : 0) | (cstore[p] > 0 ? PM_STORE : 0) |
+           (ccut[p] > 0 ? PM_NOCUT : 0);
+  pm[p] = make_int4(fl, h, g, nF);
+  const unsigned w = (unsigned)max(loc - h, g - loc);
+  if (w) atomicMax(wmax, w);
+  // deferred lower contribution of p is finalised at its last later partner b + g
+  finkey[p] = nG ? (uint32_t)(b + g) : 0xffffffffu;
+  finval[p] = (int32_t)p;
 }
-void launch_flags(const PairArgs& a, const int32_t* cover, int32_t* pflag, int32_t* is_store,
-                  cudaStream_t st) {
+void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st) {
   if (a.M <= 0) return;
-  k_flags<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cover, pflag, is_store);
+  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval);
+}
+
+// CSR of the finalisation lists: sorted keys -> [fin_b, fin_e) per position
+__global__ void k_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const uint32_t k = key[i];
+  if (k == 0xffffffffu) return;
+  if (i == 0 || key[i - 1] != k) fb[k] = (int32_t)i;
+  if (i == M - 1 || key[i + 1] != k) fe[k] = (int32_t)(i + 1);
+}
+void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe, cudaStream_t st) {
+  cudaMemsetAsync(fb, 0, sizeof(int32_t) * M, st);
+  cudaMemsetAsync(fe, 0, sizeof(int32_t) * M, st);
+  if (M <= 0) return;
+  k_fin_ranges<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(key, M, fb, fe);
+}
+
+// ------------------------------------------------------------------------- work items
+// Split every tile's list into chunks of about `target` positions, cutting only where no
+// uncertain pair is separated (so each chunk's transmittance scan is self-contained and
+// chunks compose front to back: pc = sum_k (prod_{m<k} P_m) S_k).  One thread per tile.
+__global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
+                         const int64_t* item_off, int ntiles, int target, const int32_t* owner,
+                         int rank, int4* items, int32_t* item_cnt, uint32_t* item_key) {
+  // one warp per tile: cut points found with warp ballots over the PM_NOCUT flags
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  const int64_t b = tbegin[t];
+  const int K = (int)(tend[t] - b);
+  const int64_t o = item_off[t];
+  const int64_t cap = item_off[t + 1] - o;
+  int n = 0, start = 0;
+  const bool mine = owner == nullptr || owner[t] == rank;
+  if (mine) do {
+    int end = min(start + target, K);
+    if (pm) {
+      // first position >= end that may start a chunk
+      for (int base = end; base < K; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < K && !(pm[b + i].x & PM_NOCUT);
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (m) {
+          end = base + __ffs(m) - 1;
+          break;
+        }
+        end = K;
+      }
+    }
+    bool exc = false;
+    if (pm)
+      for (int base = start; base < end; base += 32) {
+        const int i = base + lane;
+        const bool e = i < end && pm[b + i].x != 0;
+        if (__any_sync(0xffffffffu, e)) {
+          exc = true;
+          break;
+        }
+      }
+    if (lane == 0) {
+      items[o + n] = make_int4(t, start, end, exc ? IT_EXC : 0);
+      item_key[o + n] = (uint32_t)(end - start);
+    }
+    ++n;
+    start = end;
+  } while (start < K && n < cap);
+  for (int j = n + lane; j < cap; j += 32) {  // unused slots: empty items, sorted last
+    items[o + j] = make_int4(-1, 0, 0, 0);
+    item_key[o + j] = 0;
+  }
+  if (lane == 0) {
+    item_cnt[t] = n;
+    if (n == 1) items[o].w |= IT_SINGLE;
+  }
+}
+__global__ void k_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
+                            int64_t* caps) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int64_t K = tend[t] - tbegin[t];
+  caps[t] = K > 0 ? (K + target - 1) / target : 1;
+}
+void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
+                      int64_t* caps, cudaStream_t st) {
+  k_item_caps<<<(ntiles + 255) / 256, 256, 0, st>>>(tbegin, tend, ntiles, target, caps);
+}
+void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
+                   const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
+                   int4* items, int32_t* item_cnt, uint32_t* item_key, cudaStream_t st) {
+  k_chunks<<<(ntiles + 3) / 4, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, target, owner,
+                                             rank, items, item_cnt, item_key);
 }
 
 // ------------------------------------------------------------------------- untile (a11)

@@ -11,11 +11,17 @@
 // fp64 per-row / per-column squared distances for the exact per-pixel cull (reading O1).
 // Every thread then walks the batch for its pixel(s) in order: FP32 on CUDA cores.
 //
-// Uncertain depth pairs (rotation / scene boxes): positions flagged P_STORE write
-// (a_lo, a_hi, T_hi-before, T_lo-before) per pixel to a scratch slot; positions flagged
-// P_EXC are left out of the running sums and added after the walk from their exception
-// windows (T_hi over before(i) minus E_F(i), T_lo over before(i) plus E_G(i)) without any
-// division (H3).
+// Work is a list of (tile, chunk) items, longest first, pulled by persistent CTAs from an
+// atomic counter (load balance).  A chunk ends only where no uncertain depth
+// pair is split, so chunks of one tile compose front to back in k_merge.
+//
+// Uncertain depth pairs (rotation / scene boxes; step 13) are handled in the walk itself
+// with a per-CTA ring in global memory (L2-resident): position q writes (T_hi before q,
+// 1 - a_lo, 1 - a_hi, deferred T_lo a_lo) for its pixel; T_hi of a position with earlier
+// uncertain partners is re-multiplied over its window [h, q) skipping E_F (no division,
+// H3); the lower contribution of a position with later uncertain partners is deferred and
+// finalised at g = max E_G, when all of E_G's (1 - a_hi) are known.
+#include <algorithm>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -35,7 +41,10 @@ struct alignas(16) SRec {
   float wc[6][2];
   float o[2];
   float clo[3], chi[3];
-  int flags, pflag, slot, pad;
+  int flags;                // F_* of the Gaussian
+  int pmf, ph, pg, pnF, pnG;  // position metadata (PM_*, h, g, |E_F|, |E_G|)
+  int pfb, pfe;             // finalisation list range
+  long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
   double r2;
 };
 
@@ -124,213 +133,247 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 template <int NV, int PPT>
 __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_item;
   const int ts = A.ts;
+  const int npix = ts * ts;
   const int nthr = blockDim.x;
   const int BS = A.bs;
   SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
   double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][ts]
   double* cy2 = cx2 + (size_t)BS * ts;                 // [BS][ts]
-
-  const int tile = A.tile_list[blockIdx.x];
-  const int tx = tile % A.ntx, ty = tile / A.ntx;
-  const int64_t tb = A.tbegin[tile], te = A.tend[tile];
-  const int K = (int)(te - tb);
-  const double ucx = tx * ts + 0.5 * ts, ucy = ty * ts + 0.5 * ts;  // tile centre
-
-  // my pixels
-  int lx[PPT], ly[PPT];
-  bool in_img[PPT];
-  float du0[PPT], du1[PPT];
-  float Tb[PPT], Tl[PPT], ahc[PPT][3], alc[PPT][3];
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    const int l = threadIdx.x + q * nthr;
-    lx[q] = l % ts;
-    ly[q] = l / ts;
-    in_img[q] = (tx * ts + lx[q] < A.W) && (ty * ts + ly[q] < A.H);
-    du0[q] = (float)lx[q] + 0.5f - 0.5f * ts;
-    du1[q] = (float)ly[q] + 0.5f - 0.5f * ts;
-    Tb[q] = Tl[q] = 1.f;
-    ahc[q][0] = ahc[q][1] = ahc[q][2] = 0.f;
-    alc[q][0] = alc[q][1] = alc[q][2] = 0.f;
-  }
+  const bool has_exc = A.pm != nullptr;
+  float4* ring = has_exc ? A.ring + (size_t)blockIdx.x * A.R * npix : nullptr;
+  const int rmask = A.R - 1;
   unsigned active = 0;
-  const bool has_exc = A.pflag != nullptr;
 
-  for (int b0 = 0; b0 < K; b0 += BS) {
-    const int nb = min(BS, K - b0);
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(A.counter, 1);
     __syncthreads();
-    // ---- staging: fp64 record -> tile-centred fp32 forms + cull tables
-    for (int j = threadIdx.x; j < nb; j += nthr) {
-      const int32_t g = A.vals[tb + b0 + j];
-      const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
-      SRec<NV>& S = srec[j];
+    const int iidx = s_item;
+    __syncthreads();
+    if (iidx >= A.n_items) break;
+    const int islot = A.order[iidx];
+    const int4 it = A.items[islot];
+    if (it.x < 0) continue;  // padding
+    const int tile = it.x, pbeg = it.y, pend = it.z, iflags = it.w;
+    const int tx = tile % A.ntx, ty = tile / A.ntx;
+    const int64_t tb = A.tbegin[tile];
+    const double ucx = tx * ts + 0.5 * ts, ucy = ty * ts + 0.5 * ts;  // tile centre
+    const bool iexc = has_exc && (iflags & IT_EXC);
+
+    int lx[PPT], ly[PPT];
+    bool in_img[PPT];
+    float du0[PPT], du1[PPT];
+    float Tb[PPT], Tl[PPT], ahc[PPT][3], alc[PPT][3];
 #pragma unroll
-      for (int k = 0; k <= NV; ++k) {
-        const double d2l = H->d2[0][k], d2h = H->d2[1][k];
-        // x_a lower = u_a D2_lo - DU_a,hi ; upper = u_a D2_hi - DU_a,lo  (u_a > 0)
-        S.xb[0][0][k] = (float)(ucx * d2l - H->du[0][1][k]);
-        S.xb[0][1][k] = (float)(ucx * d2h - H->du[0][0][k]);
-        S.xb[1][0][k] = (float)(ucy * d2l - H->du[1][1][k]);
-        S.xb[1][1][k] = (float)(ucy * d2h - H->du[1][0][k]);
-        S.d2[0][k] = (float)d2l;
-        S.d2[1][k] = (float)d2h;
-      }
-#pragma unroll
-      for (int e = 0; e < 6; ++e) {
+    for (int q = 0; q < PPT; ++q) {
+      const int l = threadIdx.x + q * nthr;
+      lx[q] = l % ts;
+      ly[q] = l / ts;
+      in_img[q] = (tx * ts + lx[q] < A.W) && (ty * ts + ly[q] < A.H);
+      du0[q] = (float)lx[q] + 0.5f - 0.5f * ts;
+      du1[q] = (float)ly[q] + 0.5f - 0.5f * ts;
+      Tb[q] = Tl[q] = 1.f;
+      ahc[q][0] = ahc[q][1] = ahc[q][2] = 0.f;
+      alc[q][0] = alc[q][1] = alc[q][2] = 0.f;
+    }
+
+    for (int b0 = pbeg; b0 < pend; b0 += BS) {
+      const int nb = min(BS, pend - b0);
+      __syncthreads();
+      // ---- staging: fp64 record -> tile-centred fp32 forms + cull tables + metadata
+      for (int j = threadIdx.x; j < nb; j += nthr) {
+        const int64_t gp = tb + b0 + j;
+        const int32_t g = A.vals[gp];
+        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
+        SRec<NV>& S = srec[j];
 #pragma unroll
         for (int k = 0; k <= NV; ++k) {
-          S.w[e][0][k] = H->w[e][0][k];
-          S.w[e][1][k] = H->w[e][1][k];
+          const double d2l = H->d2[0][k], d2h = H->d2[1][k];
+          // x_a lower = u_a D2_lo - DU_a,hi ; upper = u_a D2_hi - DU_a,lo  (u_a > 0)
+          S.xb[0][0][k] = (float)(ucx * d2l - H->du[0][1][k]);
+          S.xb[0][1][k] = (float)(ucx * d2h - H->du[0][0][k]);
+          S.xb[1][0][k] = (float)(ucy * d2l - H->du[1][1][k]);
+          S.xb[1][1][k] = (float)(ucy * d2h - H->du[1][0][k]);
+          S.d2[0][k] = (float)d2l;
+          S.d2[1][k] = (float)d2h;
         }
-        S.wc[e][0] = H->wc[e][0];
-        S.wc[e][1] = H->wc[e][1];
-      }
-      S.o[0] = H->o[0];
-      S.o[1] = H->o[1];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        S.clo[c] = H->clo[c];
-        S.chi[c] = H->chi[c];
-      }
-      S.flags = H->flags;
-      S.pflag = has_exc ? A.pflag[tb + b0 + j] : 0;
-      S.slot = has_exc ? A.slot[tb + b0 + j] : 0;
-      S.r2 = H->r2;
-      const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
-      for (int l = 0; l < ts; ++l) {
-        const double x = tx * ts + l + 0.5, y = ty * ts + l + 0.5;
-        const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
-        const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-        cx2[j * ts + l] = __dmul_rn(dx, dx);
-        cy2[j * ts + l] = __dmul_rn(dy, dy);
-      }
-    }
-    __syncthreads();
-    // ---- walk the batch in (kappa, index) order
-    for (int j = 0; j < nb; ++j) {
-      const SRec<NV>& R = srec[j];
-      const int flags = R.flags, pflag = R.pflag;
-      float alo[PPT], ahi[PPT];
-      bool keep[PPT];
-      bool any = false;
+        for (int e = 0; e < 6; ++e) {
 #pragma unroll
-      for (int q = 0; q < PPT; ++q) {
-        keep[q] = in_img[q] && !(__dadd_rn(cx2[j * ts + lx[q]], cy2[j * ts + ly[q]]) > R.r2);
-        any |= keep[q];
-        alo[q] = ahi[q] = 0.f;
-      }
-      if (__any_sync(FULLM, any)) {
-        if (flags & F_FAIL) {
-#pragma unroll
-          for (int q = 0; q < PPT; ++q) {
-            alo[q] = 0.f;
-            ahi[q] = keep[q] ? R.o[1] : 0.f;
+          for (int k = 0; k <= NV; ++k) {
+            S.w[e][0][k] = H->w[e][0][k];
+            S.w[e][1][k] = H->w[e][1][k];
           }
+          S.wc[e][0] = H->wc[e][0];
+          S.wc[e][1] = H->wc[e][1];
+        }
+        S.o[0] = H->o[0];
+        S.o[1] = H->o[1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          S.clo[c] = H->clo[c];
+          S.chi[c] = H->chi[c];
+        }
+        S.flags = H->flags;
+        if (iexc) {
+          const int4 m = A.pm[gp];
+          S.pmf = m.x;
+          S.ph = m.y;
+          S.pg = m.z;
+          S.pnF = m.w;
+          S.pnG = A.nG[gp];
+          S.peoff = A.eoff[gp];
+          S.pfb = A.fin_b[gp];
+          S.pfe = A.fin_e[gp];
         } else {
-#pragma unroll
-          for (int q = 0; q < PPT; ++q) {
-            float l, h;
-            opacity<NV>(R, du0[q], du1[q], l, h);
-            alo[q] = keep[q] ? ((flags & F_STRADDLE) ? 0.f : l) : 0.f;
-            ahi[q] = keep[q] ? h : 0.f;
-          }
+          S.pmf = 0;
+          S.pfb = S.pfe = 0;
+        }
+        S.r2 = H->r2;
+        const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
+        for (int l = 0; l < ts; ++l) {
+          const double x = tx * ts + l + 0.5, y = ty * ts + l + 0.5;
+          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+          const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+          cx2[j * ts + l] = __dmul_rn(dx, dx);
+          cy2[j * ts + l] = __dmul_rn(dy, dy);
         }
       }
+      __syncthreads();
+      // ---- walk the batch in (kappa, index) order
+      for (int j = 0; j < nb; ++j) {
+        const SRec<NV>& R = srec[j];
+        const int flags = R.flags, pmf = R.pmf;
+        const int qpos = b0 + j;  // tile-local position
+        float alo[PPT], ahi[PPT];
+        bool keep[PPT];
+        bool any = false;
 #pragma unroll
-      for (int q = 0; q < PPT; ++q) {
-        active += keep[q] ? 1u : 0u;
-        if (pflag & P_STORE) {
-          const int64_t si = (int64_t)R.slot * ts * ts + threadIdx.x + q * nthr;
-          A.scratch[si] = make_float4(alo[q], ahi[q], Tb[q], Tl[q]);
+        for (int q = 0; q < PPT; ++q) {
+          keep[q] = in_img[q] && !(__dadd_rn(cx2[j * ts + lx[q]], cy2[j * ts + ly[q]]) > R.r2);
+          any |= keep[q];
+          alo[q] = ahi[q] = 0.f;
         }
-        if (!(pflag & P_EXC)) {
-          const float wb = Tb[q] * ahi[q], wl = Tl[q] * alo[q];
+        if (__any_sync(FULLM, any)) {
+          if (flags & F_FAIL) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            ahc[q][c] = fmaf(wb, R.chi[c], ahc[q][c]);
-            alc[q][c] = fmaf(wl, R.clo[c], alc[q][c]);
+            for (int q = 0; q < PPT; ++q) {
+              alo[q] = 0.f;
+              ahi[q] = keep[q] ? R.o[1] : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              float l, h;
+              opacity<NV>(R, du0[q], du1[q], l, h);
+              alo[q] = keep[q] ? ((flags & F_STRADDLE) ? 0.f : l) : 0.f;
+              ahi[q] = keep[q] ? h : 0.f;
+            }
           }
         }
-        Tb[q] = fmaf(-Tb[q], alo[q], Tb[q]);
-        Tl[q] = fmaf(-Tl[q], ahi[q], Tl[q]);
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          active += keep[q] ? 1u : 0u;
+          const int pix = threadIdx.x + q * nthr;
+          if (pmf & PM_STORE)
+            ring[(size_t)(qpos & rmask) * npix + pix] =
+                make_float4(Tb[q], 1.f - alo[q], 1.f - ahi[q], (pmf & PM_EG) ? Tl[q] * alo[q] : 0.f);
+          // upper: T_hi over before(q) \ E_F(q).  Dense windows (mostly E_F): multiply the
+          // window [h, q) skipping E_F.  Sparse windows: divide the running product by the
+          // E_F factors when that is numerically safe (both products far from underflow),
+          // else fall back to the window product (H3).
+          float tbv = Tb[q];
+          if (pmf & PM_EF) {
+            bool done = false;
+            const int wlen = qpos - R.ph;
+            if (wlen > 2 * R.pnF + 8) {
+              float dfac = 1.f;
+              for (int e = 0; e < R.pnF; ++e)
+                dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * npix + pix].y;
+              if (dfac >= 1e-20f && Tb[q] >= 1e-25f) {
+                tbv = Tb[q] / dfac;
+                done = true;
+              }
+            }
+            if (!done) {
+              tbv = ring[(size_t)(R.ph & rmask) * npix + pix].x;
+              int e = 0;
+              for (int r = R.ph; r < qpos; ++r) {
+                if (e < R.pnF && A.exc[R.peoff + e] == r) {
+                  ++e;
+                  continue;
+                }
+                tbv *= ring[(size_t)(r & rmask) * npix + pix].y;
+              }
+            }
+          }
+          const float wb = tbv * ahi[q];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ahc[q][c] = fmaf(wb, R.chi[c], ahc[q][c]);
+          // lower: T_lo over before(q) (E_G(q) empty) or deferred to max E_G(q)
+          if (!(pmf & PM_EG)) {
+            const float wl = Tl[q] * alo[q];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) alc[q][c] = fmaf(wl, R.clo[c], alc[q][c]);
+          }
+          Tb[q] = fmaf(-Tb[q], alo[q], Tb[q]);
+          Tl[q] = fmaf(-Tl[q], ahi[q], Tl[q]);
+          // finalise deferred lower contributions of earlier partners whose last later
+          // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
+          for (int f = R.pfb; f < R.pfe; ++f) {
+            const int gq = A.fin_val[f];
+            const int qq = (int)(gq - tb);
+            const int4 m = A.pm[gq];
+            float tl = ring[(size_t)(qq & rmask) * npix + pix].w;
+            const int64_t o2 = A.eoff[gq] + m.w;
+            const int ng2 = A.nG[gq];
+            for (int e = 0; e < ng2; ++e) {
+              const int r = A.exc[o2 + e];
+              tl *= ring[(size_t)(r & rmask) * npix + pix].z;
+            }
+            const HotRec<NV>* H2 = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[gq];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) alc[q][c] = fmaf(tl, H2->clo[c], alc[q][c]);
+          }
+        }
       }
     }
-  }
-  // ---- exception post-pass (positions with uncertain depth partners)
-  if (has_exc) {
-    for (int p = 0; p < K; ++p) {
-      const int64_t gp = tb + p;
-      if (!(A.pflag[gp] & P_EXC)) continue;
-      const int nF = A.nF[gp], nG = A.nG[gp];
-      const int64_t off = A.eoff[gp];
-      const int h = A.hpos[gp];
-      const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[gp];
-      float clo[3], chi[3];
+    // ---- epilogue
+    if (iflags & IT_SINGLE) {
+      // +- N tau, clamp to [0,1], union over sub-boxes (steps 20-22)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        clo[c] = H->clo[c];
-        chi[c] = H->chi[c];
+      for (int q = 0; q < PPT; ++q) {
+        const int px = tx * ts + lx[q], py = ty * ts + ly[q];
+        int64_t o;
+        if (A.tile_slot) {
+          o = ((int64_t)A.tile_slot[tile] * npix + (int64_t)ly[q] * ts + lx[q]) * 3;
+        } else {
+          if (!in_img[q]) continue;
+          o = ((int64_t)py * A.W + px) * 3;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float l = fminf(fmaxf(alc[q][c] - A.ntau, 0.f), 1.f);
+          float h = fminf(fmaxf(ahc[q][c] + A.ntau, 0.f), 1.f);
+          if (!in_img[q]) l = h = 0.f;
+          if (A.first) {
+            A.lo[o + c] = l;
+            A.hi[o + c] = h;
+          } else {
+            A.lo[o + c] = fminf(A.lo[o + c], l);
+            A.hi[o + c] = fmaxf(A.hi[o + c], h);
+          }
+        }
       }
-      const int64_t sp = (int64_t)A.slot[gp] * ts * ts;
-      const int64_t sh = (int64_t)A.slot[tb + h] * ts * ts;
+    } else {
+      // chunk partial: sums relative to the chunk start and the chunk's transmittance
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         const int pix = threadIdx.x + q * nthr;
-        const float4 me = A.scratch[sp + pix];
-        float tbv, tlv = me.w;
-        if (nF == 0) {
-          tbv = me.z;
-        } else {
-          tbv = A.scratch[sh + pix].z;
-          int e = 0;
-          for (int r = h; r < p; ++r) {
-            if (e < nF && A.exc[off + e] == r) {
-              ++e;
-              continue;
-            }
-            tbv = fmaf(-tbv, A.scratch[(int64_t)A.slot[tb + r] * ts * ts + pix].x, tbv);
-          }
-        }
-        for (int e = 0; e < nG; ++e) {
-          const int r = A.exc[off + nF + e];
-          tlv = fmaf(-tlv, A.scratch[(int64_t)A.slot[tb + r] * ts * ts + pix].y, tlv);
-        }
-        const float wb = tbv * me.y, wl = tlv * me.x;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          ahc[q][c] = fmaf(wb, chi[c], ahc[q][c]);
-          alc[q][c] = fmaf(wl, clo[c], alc[q][c]);
-        }
-      }
-    }
-  }
-  // ---- epilogue: +- N tau, clamp to [0,1], union over sub-boxes (steps 20-22)
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    const int px = tx * ts + lx[q], py = ty * ts + ly[q];
-    const bool inside = px < A.W && py < A.H;
-    int64_t o;
-    if (A.tile_slot) {
-      o = ((int64_t)A.tile_slot[tile] * ts * ts + (int64_t)ly[q] * ts + lx[q]) * 3;
-    } else {
-      if (!inside) continue;
-      o = ((int64_t)py * A.W + px) * 3;
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      float l = fminf(fmaxf(alc[q][c] - A.ntau, 0.f), 1.f);
-      float h = fminf(fmaxf(ahc[q][c] + A.ntau, 0.f), 1.f);
-      if (!inside) {
-        l = 0.f;
-        h = 0.f;
-      }
-      if (A.first) {
-        A.lo[o + c] = l;
-        A.hi[o + c] = h;
-      } else {
-        A.lo[o + c] = fminf(A.lo[o + c], l);
-        A.hi[o + c] = fmaxf(A.hi[o + c], h);
+        float4* dst = reinterpret_cast<float4*>(A.partial + ((size_t)islot * npix + pix) * 8);
+        dst[0] = make_float4(ahc[q][0], ahc[q][1], ahc[q][2], Tb[q]);
+        dst[1] = make_float4(alc[q][0], alc[q][1], alc[q][2], Tl[q]);
       }
     }
   }
@@ -339,6 +382,53 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULLM, v, s);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
+}
+
+// front-to-back composition of a tile's chunks: pc = sum_k (prod_{m<k} P_m) S_k
+__global__ void k_merge(TileArgs A) {
+  const int tile = blockIdx.x;
+  const int n = A.item_cnt[tile];
+  if (n <= 1) return;
+  const int ts = A.ts, npix = ts * ts;
+  const int tx = tile % A.ntx, ty = tile / A.ntx;
+  for (int pix = threadIdx.x; pix < npix; pix += blockDim.x) {
+    float Pb = 1.f, Pl = 1.f, h[3] = {0.f, 0.f, 0.f}, l[3] = {0.f, 0.f, 0.f};
+    for (int k = 0; k < n; ++k) {
+      const int64_t it = A.item_off[tile] + k;
+      const float4* src = reinterpret_cast<const float4*>(A.partial + ((size_t)it * npix + pix) * 8);
+      const float4 a = src[0], b = src[1];
+      h[0] = fmaf(Pb, a.x, h[0]);
+      h[1] = fmaf(Pb, a.y, h[1]);
+      h[2] = fmaf(Pb, a.z, h[2]);
+      l[0] = fmaf(Pl, b.x, l[0]);
+      l[1] = fmaf(Pl, b.y, l[1]);
+      l[2] = fmaf(Pl, b.z, l[2]);
+      Pb *= a.w;
+      Pl *= b.w;
+    }
+    const int lx = pix % ts, ly = pix / ts;
+    const int px = tx * ts + lx, py = ty * ts + ly;
+    const bool inside = px < A.W && py < A.H;
+    int64_t o;
+    if (A.tile_slot) {
+      o = ((int64_t)A.tile_slot[tile] * npix + pix) * 3;
+    } else {
+      if (!inside) continue;
+      o = ((int64_t)py * A.W + px) * 3;
+    }
+    for (int c = 0; c < 3; ++c) {
+      float lv = fminf(fmaxf(l[c] - A.ntau, 0.f), 1.f);
+      float hv = fminf(fmaxf(h[c] + A.ntau, 0.f), 1.f);
+      if (!inside) lv = hv = 0.f;
+      if (A.first) {
+        A.lo[o + c] = lv;
+        A.hi[o + c] = hv;
+      } else {
+        A.lo[o + c] = fminf(A.lo[o + c], lv);
+        A.hi[o + c] = fmaxf(A.hi[o + c], hv);
+      }
+    }
+  }
 }
 
 int tile_threads(int ts) { return ts <= 16 ? ts * ts : 256; }
@@ -361,32 +451,53 @@ size_t tile_smem_bytes(int nv, int ts, int bs) {
 }
 
 template <int NV, int PPT>
-static void launch_one(const TileArgs& a, cudaStream_t st) {
-  const size_t smem = smem_for<NV>(a.ts, a.bs);
+static int grid_one(int ts, int bs) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_tile<NV, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
-  k_tile<NV, PPT><<<a.n_list, tile_threads(a.ts), smem, st>>>(a);
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV, PPT>, tile_threads(ts),
+                                                smem_for<NV>(ts, bs));
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(1, per_sm) * nsm;
 }
 
-void launch_tile(int nv, const TileArgs& a, cudaStream_t st) {
-  if (a.n_list <= 0) return;
+int tile_grid(int nv, int ts, int bs) {
+  const bool four = ts == 32;
+  switch (nv) {
+#define CASE(K) \
+  case K:       \
+    return four ? grid_one<K, 4>(ts, bs) : grid_one<K, 1>(ts, bs);
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
+#undef CASE
+    default:
+      return 0;
+  }
+}
+
+void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st) {
+  if (a.n_items <= 0 || grid <= 0) return;
   const bool four = a.ts == 32;
   switch (nv) {
-#define CASE(K)                     \
-  case K:                           \
-    if (four)                       \
-      launch_one<K, 4>(a, st);      \
-    else                            \
-      launch_one<K, 1>(a, st);      \
+#define CASE(K)                                                                          \
+  case K:                                                                                \
+    if (four)                                                                            \
+      k_tile<K, 4><<<grid, tile_threads(a.ts), smem_for<K>(a.ts, a.bs), st>>>(a);        \
+    else                                                                                 \
+      k_tile<K, 1><<<grid, tile_threads(a.ts), smem_for<K>(a.ts, a.bs), st>>>(a);        \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
     default:
       break;
   }
+}
+
+void launch_merge(const TileArgs& a, cudaStream_t st) {
+  k_merge<<<a.ntiles, 256, 0, st>>>(a);
 }
 
 }  // namespace absplat
