@@ -53,12 +53,12 @@ struct as_ctx {
   DevBuf keys, keys2, vals, vals2, tbegin, tend, tcost, tkey, tkey2, tids, tlist, tslot, owner;
   DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
   DevBuf tileh, tilemax, wsP, kapP;
-  DevBuf item_off, items, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
+  DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
   DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
   size_t bytes = 0;
   int64_t launches = 0;
-  int last_items = 0, last_grid = 0, last_R = 1, max_window = 0;
+  int last_items = 0, last_grid = 0, last_R = 1, max_window = 0, last_wmax = 0;
   cudaEvent_t ev[8] = {};
   bool events = false;
 };
@@ -348,6 +348,8 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   const int64_t N = ctx->N;
   const int nv = bi.n_vars;
   unsigned long long* ctr = P<unsigned long long>(ctx->counters);
+  // BS is a performance knob: clamp it to what fits in shared memory at this n
+  while (bs > 1 && tile_smem_bytes(nv, G.ts, bs) > 96 * 1024) bs >>= 1;
   if (pt) CK(cudaEventRecord(ctx->ev[1], st));
   if (do_setup) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
@@ -403,6 +405,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   TileArgs ta{};
   bool has_exc = false;
   int R = 1;
+  ctx->last_wmax = 0;
   if (nv > 0 && M > 0) {
     ensure(ctx, ctx->nF, sizeof(int32_t) * M);
     ensure(ctx, ctx->nG, sizeof(int32_t) * M);
@@ -487,6 +490,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       CK(cudaStreamSynchronize(st));
       while (R <= (int)hw) R <<= 1;
       ctx->max_window = std::max(ctx->max_window, (int)hw);
+      ctx->last_wmax = (int)hw;
       has_exc = true;
       ta.pm = P<int4>(ctx->pflag);
       ta.nG = P<int32_t>(ctx->nG);
@@ -498,13 +502,15 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
   int grid = tile_grid(nv, G.ts, bs);
   const size_t npix = (size_t)G.ts * G.ts;
-  if (has_exc) {  // ring memory: grid x R x npix float4 (cap the total at ~8 GB)
-    const size_t per = (size_t)R * npix * sizeof(float4);
+  if (has_exc) {  // ring memory: grid x R x threads float4 (cap the total at ~8 GB)
+    const size_t per = (size_t)R * tile_threads(G.ts) * sizeof(float4);
     const size_t budget = (size_t)8 << 30;
     if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
     ensure(ctx, ctx->scratch, (size_t)grid * per);
   }
-  const int target = (int)std::max<int64_t>(2 * bs, M / ((int64_t)grid * 6) + 1);
+  const int target = (int)std::max<int64_t>(
+      std::max<int64_t>(2 * bs, 2 * (int64_t)ctx->last_wmax + 2),
+      M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1);
   int64_t* caps = P<int64_t>(ctx->ntot);  // reuse: int64 [ntiles+1]
   ensure(ctx, ctx->ntot, sizeof(int64_t) * (std::max<int64_t>(M, G.ntiles) + 1));
   caps = P<int64_t>(ctx->ntot);
@@ -515,6 +521,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   cub_exclusive_sum(ctx, caps, P<int64_t>(ctx->item_off), G.ntiles + 1);
   const int64_t n_items = read_i64(ctx, P<int64_t>(ctx->item_off) + G.ntiles);
   ensure(ctx, ctx->items, sizeof(int4) * n_items);
+  ensure(ctx, ctx->items2, sizeof(int4) * n_items);
   ensure(ctx, ctx->item_key, sizeof(uint32_t) * n_items);
   ensure(ctx, ctx->item_key2, sizeof(uint32_t) * n_items);
   ensure(ctx, ctx->item_idx, sizeof(int32_t) * n_items);
@@ -523,7 +530,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ensure(ctx, ctx->partial, sizeof(float) * 8 * npix * n_items);
   launch_chunks(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), has_exc ? P<int4>(ctx->pflag) : nullptr,
                 P<int64_t>(ctx->item_off), G.ntiles, target, owner, rank, P<int4>(ctx->items),
-                P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
+                P<int4>(ctx->items2), P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
   LAUNCHED(ctx, 1);
   k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
   LAUNCHED(ctx, 1);
@@ -537,6 +544,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.tbegin = P<int64_t>(ctx->tbegin);
   ta.tend = P<int64_t>(ctx->tend);
   ta.items = P<int4>(ctx->items);
+  ta.items2 = P<int4>(ctx->items2);
   ta.order = P<int32_t>(ctx->item_order);
   ta.n_items = (int)n_items;
   ta.counter = P<int>(ctx->work_counter);
@@ -607,10 +615,6 @@ as_status check_tile_args(as_ctx* ctx, int tile, int batch, int nv) {
   }
   if (batch < 1 || batch > 256) {
     set_err(ctx, "batch must be in [1, 256] (got %d)", batch);
-    return AS_E_ARG;
-  }
-  if (tile_smem_bytes(nv, tile, batch) > 200 * 1024) {
-    set_err(ctx, "batch %d too large for shared memory at n=%d, tile=%d", batch, nv, tile);
     return AS_E_ARG;
   }
   return AS_OK;
@@ -791,7 +795,7 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->diff, &ctx->cover,
                     &ctx->pflag, &ctx->is_store, &ctx->slot, &ctx->scratch, &ctx->img_lo,
                     &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map, &ctx->tileh,
-                    &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->item_off, &ctx->items,
+                    &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->item_off, &ctx->items, &ctx->items2,
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
                     &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e};

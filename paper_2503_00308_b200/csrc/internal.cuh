@@ -21,7 +21,7 @@ constexpr double DMIN = 0.01;   // near plane (G8)
 constexpr int KTAYLOR = 8;      // MatrixInv order
 constexpr double WCAP = 1e12;   // |W| guard -> FAIL (reading O3)
 
-enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4 };
+enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4, F_SKIP = 8 };  // F_SKIP: staging-only
 // per list-position flags (exceptions, a9) and work-item flags
 enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8 };
 enum : int { IT_EXC = 1, IT_SINGLE = 2 };
@@ -283,7 +283,8 @@ void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, in
                       int64_t* caps, cudaStream_t st);
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
                    const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
-                   int4* items, int32_t* item_cnt, uint32_t* item_key, cudaStream_t st);
+                   int4* items, int4* items2, int32_t* item_cnt, uint32_t* item_key,
+                   cudaStream_t st);
 
 struct TileArgs {
   const void* hot;            // HotRec<NV>[N]
@@ -292,6 +293,7 @@ struct TileArgs {
   const int64_t* tend;
   // work items: {tile, begin, end (tile-local positions), flags}, processed in `order`
   const int4* items;
+  const int4* items2;         // {A (scan start), L (scan end), A_next, 0}
   const int32_t* order;       // item indices, longest first
   int n_items;
   int* counter;               // dynamic work counter (zeroed before the launch)
@@ -313,7 +315,7 @@ struct TileArgs {
   const int32_t* fin_val;
   float4* ring;               // [gridDim][R][ts*ts] (T_hi before, 1-a_lo, 1-a_hi, deferred)
   int R;                      // ring length (power of two > max window)
-  float* partial;             // [items][ts*ts][8] chunk partials (multi-chunk tiles)
+  float* partial;             // [items][sub-blocks][64][8] chunk partials (multi-chunk tiles)
   // outputs
   float* lo;                  // row-major [H][W][3] (tile_slot == nullptr) or tile-major
   float* hi;
@@ -322,6 +324,7 @@ struct TileArgs {
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st);
 void launch_merge(const TileArgs& a, cudaStream_t st);
 int tile_threads(int ts);
+int tile_subblocks(int ts);
 int tile_grid(int nv, int ts, int bs);
 size_t tile_smem_bytes(int nv, int ts, int bs);
 

@@ -361,13 +361,19 @@ void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe,
 }
 
 // ------------------------------------------------------------------------- work items
-// Split every tile's list into chunks of about `target` positions, cutting only where no
-// uncertain pair is separated (so each chunk's transmittance scan is self-contained and
-// chunks compose front to back: pc = sum_k (prod_{m<k} P_m) S_k).  One thread per tile.
+// Split every tile's list into chunks of `target` positions.  A chunk [s, e) is scanned
+// over [A, L): the lookback [A, s) covers the E_F windows of its positions (A = min h_p)
+// and the lookahead [e, L) their E_G partners (L = max g_p + 1); those margin positions
+// only feed the chunk's transmittance and exception factors.  Chunks then compose front
+// to back with multiplications only:  pc = sum_k P(<A_k) S_k,  P(<A_{k+1}) = P(<A_k) Rk,
+// where S_k is the chunk's sum relative to A_k and Rk its running product at A_{k+1}
+// (target > 2 * max window keeps A_{k+1} inside chunk k's scan).  One warp per tile.
+//   items[i]  = {tile, s, e, flags | log2(ring length) << 8}
+//   items2[i] = {A, L, A_next, 0}
 __global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
                          const int64_t* item_off, int ntiles, int target, const int32_t* owner,
-                         int rank, int4* items, int32_t* item_cnt, uint32_t* item_key) {
-  // one warp per tile: cut points found with warp ballots over the PM_NOCUT flags
+                         int rank, int4* items, int4* items2, int32_t* item_cnt,
+                         uint32_t* item_key) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= ntiles) return;
@@ -375,48 +381,54 @@ __global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4*
   const int K = (int)(tend[t] - b);
   const int64_t o = item_off[t];
   const int64_t cap = item_off[t + 1] - o;
-  int n = 0, start = 0;
   const bool mine = owner == nullptr || owner[t] == rank;
-  if (mine) do {
-    int end = min(start + target, K);
-    if (pm) {
-      // first position >= end that may start a chunk
-      for (int base = end; base < K; base += 32) {
-        const int i = base + lane;
-        const bool ok = i < K && !(pm[b + i].x & PM_NOCUT);
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (m) {
-          end = base + __ffs(m) - 1;
-          break;
-        }
-        end = K;
-      }
-    }
+  const int n = mine ? (K > 0 ? (K + target - 1) / target : 1) : 0;
+  int prevA = 0;
+  for (int k = n - 1; k >= 0; --k) {  // backwards so A_next is known
+    const int s = k * target, e = min(K, s + target);
+    int A = s, L = e, wmax = 0;
     bool exc = false;
     if (pm)
-      for (int base = start; base < end; base += 32) {
+      for (int base = s; base < e; base += 32) {
         const int i = base + lane;
-        const bool e = i < end && pm[b + i].x != 0;
-        if (__any_sync(0xffffffffu, e)) {
-          exc = true;
-          break;
+        int a = s, l = e, wl = 0;
+        bool ex = false;
+        if (i < e) {
+          const int4 m = pm[b + i];
+          if (m.x != 0) {
+            ex = true;
+            if (m.x & PM_EF) a = min(a, m.y);
+            if (m.x & PM_EG) l = max(l, m.z + 1);
+            wl = max(i - m.y, m.z - i);
+          }
         }
+        for (int sh = 16; sh > 0; sh >>= 1) {
+          a = min(a, __shfl_xor_sync(0xffffffffu, a, sh));
+          l = max(l, __shfl_xor_sync(0xffffffffu, l, sh));
+          wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, sh));
+        }
+        A = min(A, a);
+        L = max(L, l);
+        wmax = max(wmax, wl);
+        exc |= __any_sync(0xffffffffu, ex);
       }
+    int lr = 0;
+    while ((1 << lr) <= wmax) ++lr;
+    const int Anext = (k == n - 1) ? e : prevA;
     if (lane == 0) {
-      items[o + n] = make_int4(t, start, end, exc ? IT_EXC : 0);
-      item_key[o + n] = (uint32_t)(end - start);
+      int fl = (exc ? IT_EXC : 0) | (n == 1 ? IT_SINGLE : 0) | (lr << 8);
+      items[o + k] = make_int4(t, s, e, fl);
+      items2[o + k] = make_int4(A, L, Anext, 0);
+      item_key[o + k] = (uint32_t)(L - A);
     }
-    ++n;
-    start = end;
-  } while (start < K && n < cap);
+    prevA = A;
+  }
   for (int j = n + lane; j < cap; j += 32) {  // unused slots: empty items, sorted last
     items[o + j] = make_int4(-1, 0, 0, 0);
+    items2[o + j] = make_int4(0, 0, 0, 0);
     item_key[o + j] = 0;
   }
-  if (lane == 0) {
-    item_cnt[t] = n;
-    if (n == 1) items[o].w |= IT_SINGLE;
-  }
+  if (lane == 0) item_cnt[t] = n;
 }
 __global__ void k_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
                             int64_t* caps) {
@@ -431,9 +443,10 @@ void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, in
 }
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
                    const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
-                   int4* items, int32_t* item_cnt, uint32_t* item_key, cudaStream_t st) {
+                   int4* items, int4* items2, int32_t* item_cnt, uint32_t* item_key,
+                   cudaStream_t st) {
   k_chunks<<<(ntiles + 3) / 4, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, target, owner,
-                                             rank, items, item_cnt, item_key);
+                                             rank, items, items2, item_cnt, item_key);
 }
 
 // ------------------------------------------------------------------------- untile (a11)

@@ -3,13 +3,14 @@
 // transmittance scan + bounded blend (Alg. 3, interval reading O7), with the
 // finalise/union epilogue.
 //
-// One CTA per image tile (TS x TS pixels, 1 or 4 pixels per thread), tiles launched in
-// descending Gaussian-count order.  The tile's Gaussian list (sorted by (kappa, index)) is
-// streamed through shared memory in batches of BS: the staging step turns each Gaussian's
-// fp64 record into tile-centred fp32 forms (B = u_c D2 - DU at the tile centre u_c, so the
-// per-pixel x = B + (u - u_c) D2 avoids the d^2 u - d up cancellation; H2) and
-// fp64 per-row / per-column squared distances for the exact per-pixel cull (reading O1).
-// Every thread then walks the batch for its pixel(s) in order: FP32 on CUDA cores.
+// A work item is one 8x8 pixel block of a tile (64 threads, one pixel each) over one chunk of
+// the tile's Gaussian list (sorted by (kappa, index)).  The list is streamed through shared
+// memory in batches of BS: the staging step turns each Gaussian's fp64 record into
+// block-centred fp32 forms (B = u_c D2 - DU at the block centre u_c, so the per-pixel
+// x = B + (u - u_c) D2 avoids the d^2 u - d up cancellation; H2) and fp64 per-row /
+// per-column squared distances for the exact per-pixel cull (reading O1); Gaussians whose
+// footprint misses the whole block are skipped.  Every thread then walks the batch for its
+// pixel in order: FP32 on CUDA cores.
 //
 // Work is a list of (tile, chunk) items, longest first, pulled by persistent CTAs from an
 // atomic counter (load balance).  A chunk ends only where no uncertain depth
@@ -35,10 +36,17 @@ constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 template <int NV>
 struct alignas(16) SRec {
   static constexpr int C = NV + 1;
-  float xb[2][2][C];  // [a][lo/hi][k]: tile-centred constant part of x_a's forms
-  float d2[2][C];     // [lo/hi][k]
-  float w[6][2][C];   // [a*3+c][lo/hi][k]
-  float wc[6][2];
+  static constexpr int CP = (C + 3) & ~3;  // padded for 16-byte vector loads
+  // x_a lower forms (for the concretised x_lo_a only): B_a + du_a * D2_lo
+  float xb[2][CP];
+  float d2lo[CP];
+  // q_c = mul(x0, W_0c) + mul(x1, W_1c) with the x-side McCormick terms folded into affine
+  // functions of the pixel offset du, and the W-side terms in mid / radius form:
+  //   q_lo,k = plo + du0 q0lo + du1 q1lo + x0 wm0 - |x0| wr0 + x1 wm1 - |x1| wr1
+  //   q_hi,k = phi + du0 q0hi + du1 q1hi + x0 wm0 + |x0| wr0 + x1 wm1 + |x1| wr1
+  float plo[3][CP], phi[3][CP], q0lo[3][CP], q0hi[3][CP], q1lo[3][CP], q1hi[3][CP];
+  float wm0[3][CP], wr0[3][CP], wm1[3][CP], wr1[3][CP];
+  float wc[6][2];           // concretised W (lo, hi), [a*3+c]
   float o[2];
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
@@ -48,58 +56,94 @@ struct alignas(16) SRec {
   double r2;
 };
 
-__device__ __forceinline__ float sel(bool c, float a, float b) { return c ? a : b; }
+// Staging of one Gaussian for a block centred at (ucx, ucy): fp64 arithmetic, one rounding.
+// x_a lower form: u_a D2_lo - DU_a,hi = B_lo,a + du_a D2_lo with B_lo,a = uc_a D2_lo - DU_a,hi
+// (u_a > 0 selects D2's lower side, step 14); upper: B_hi,a + du_a D2_hi.
+// LS(x_a, w) = w >= 0 ? w x_lo,a : w x_hi,a  and  US(x_a, w) = w >= 0 ? w x_hi,a : w x_lo,a
+// (R1 with the constant w = conc W), both affine in du_a.
+template <int NV>
+__device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, double ucx,
+                                            double ucy) {
+  constexpr int C = NV + 1;
+  const double uc[2] = {ucx, ucy};
+  double wl[6], wh[6];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    wl[e] = H->wc[e][0];
+    wh[e] = H->wc[e][1];
+    S.wc[e][0] = H->wc[e][0];
+    S.wc[e][1] = H->wc[e][1];
+  }
+#pragma unroll 1
+  for (int k = 0; k < C; ++k) {
+    const double d2l = H->d2[0][k], d2h = H->d2[1][k];
+    double blo[2], bhi[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      blo[a] = uc[a] * d2l - H->du[a][1][k];
+      bhi[a] = uc[a] * d2h - H->du[a][0][k];
+      S.xb[a][k] = (float)blo[a];
+    }
+    S.d2lo[k] = (float)d2l;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+      S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
+      S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
+      S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
+      S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
+      S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
+      S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
+      const double a0 = H->w[c][0][k], b0 = H->w[c][1][k];
+      const double a1 = H->w[3 + c][0][k], b1 = H->w[3 + c][1][k];
+      S.wm0[c][k] = (float)(0.5 * (a0 + b0));
+      S.wr0[c][k] = (float)(0.5 * (b0 - a0));
+      S.wm1[c][k] = (float)(0.5 * (a1 + b1));
+      S.wr1[c][k] = (float)(0.5 * (b1 - a1));
+    }
+  }
+}
 
-// steps 14-17 for one pixel: returns (a_lo, a_hi)
+// steps 14-17 for one pixel at offset (du0, du1) from the block centre: (a_lo, a_hi)
 template <int NV>
 __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1, float& alo,
                                         float& ahi) {
   constexpr int C = NV + 1;
-  // 14: x_a = Add(Mul(d,d,u_a), -Mul(d, up_a)) in tile-centred form
-  float xl0[C], xh0[C], xl1[C], xh1[C];
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    xl0[k] = fmaf(du0, R.d2[0][k], R.xb[0][0][k]);
-    xh0[k] = fmaf(du0, R.d2[1][k], R.xb[0][1][k]);
-    xl1[k] = fmaf(du1, R.d2[0][k], R.xb[1][0][k]);
-    xh1[k] = fmaf(du1, R.d2[1][k], R.xb[1][1][k]);
-  }
-  float x0l = xl0[NV], x0h = xh0[NV], x1l = xl1[NV], x1h = xh1[NV];
+  // 14: concretised lower bound of x_a = Add(Mul(d,d,u_a), -Mul(d, up_a))
+  float x0 = fmaf(du0, R.d2lo[NV], R.xb[0][NV]);
+  float x1 = fmaf(du1, R.d2lo[NV], R.xb[1][NV]);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    x0l -= fabsf(xl0[k]);
-    x0h += fabsf(xh0[k]);
-    x1l -= fabsf(xl1[k]);
-    x1h += fabsf(xh1[k]);
+    x0 -= fabsf(fmaf(du0, R.d2lo[k], R.xb[0][k]));
+    x1 -= fabsf(fmaf(du1, R.d2lo[k], R.xb[1][k]));
   }
-  (void)x0h;
-  (void)x1h;
-  // 15-16: q_c = mul(x0, W_0c) + mul(x1, W_1c); s = sum_c sq(q_c)
+  const float ax0 = fabsf(x0), ax1 = fabsf(x1);
+  // 15-16: q_c = mul(x0, W_0c) + mul(x1, W_1c) (R1); s = sum_c sq(q_c) (R2)
   float sl[C], sh[C];
 #pragma unroll
   for (int k = 0; k < C; ++k) sl[k] = sh[k] = 0.f;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     float ql[C], qh[C];
-    const float w0l = R.wc[c][0], w0h = R.wc[c][1];
-    const float w1l = R.wc[3 + c][0], w1h = R.wc[3 + c][1];
-    const bool a0 = w0l >= 0.f, b0 = x0l >= 0.f, c0 = w0h >= 0.f;
-    const bool a1 = w1l >= 0.f, b1 = x1l >= 0.f, c1 = w1h >= 0.f;
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      float lo = w0l * sel(a0, xl0[k], xh0[k]);
-      lo = fmaf(x0l, sel(b0, R.w[c][0][k], R.w[c][1][k]), lo);
-      lo = fmaf(w1l, sel(a1, xl1[k], xh1[k]), lo);
-      lo = fmaf(x1l, sel(b1, R.w[3 + c][0][k], R.w[3 + c][1][k]), lo);
-      float hi = w0h * sel(c0, xh0[k], xl0[k]);
-      hi = fmaf(x0l, sel(b0, R.w[c][1][k], R.w[c][0][k]), hi);
-      hi = fmaf(w1h, sel(c1, xh1[k], xl1[k]), hi);
-      hi = fmaf(x1l, sel(b1, R.w[3 + c][1][k], R.w[3 + c][0][k]), hi);
+      float lo = fmaf(du0, R.q0lo[c][k], R.plo[c][k]);
+      lo = fmaf(du1, R.q1lo[c][k], lo);
+      lo = fmaf(x0, R.wm0[c][k], lo);
+      lo = fmaf(-ax0, R.wr0[c][k], lo);
+      lo = fmaf(x1, R.wm1[c][k], lo);
+      lo = fmaf(-ax1, R.wr1[c][k], lo);
+      float hi = fmaf(du0, R.q0hi[c][k], R.phi[c][k]);
+      hi = fmaf(du1, R.q1hi[c][k], hi);
+      hi = fmaf(x0, R.wm0[c][k], hi);
+      hi = fmaf(ax0, R.wr0[c][k], hi);
+      hi = fmaf(x1, R.wm1[c][k], hi);
+      hi = fmaf(ax1, R.wr1[c][k], hi);
       ql[k] = lo;
       qh[k] = hi;
     }
-    ql[NV] -= fmaf(x0l, w0l, x1l * w1l);
-    qh[NV] -= fmaf(x0l, w0h, x1l * w1h);
+    ql[NV] -= fmaf(x0, R.wc[c][0], x1 * R.wc[3 + c][0]);
+    qh[NV] -= fmaf(x0, R.wc[c][1], x1 * R.wc[3 + c][1]);
     float qmin = ql[NV], qmax = qh[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -111,8 +155,8 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
     const bool pa = tp >= 0.f, pb = sm >= 0.f;
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      sl[k] = fmaf(tp, sel(pa, ql[k], qh[k]), sl[k]);
-      sh[k] = fmaf(sm, sel(pb, qh[k], ql[k]), sh[k]);
+      sl[k] = fmaf(tp, pa ? ql[k] : qh[k], sl[k]);
+      sh[k] = fmaf(sm, pb ? qh[k] : ql[k], sh[k]);
     }
     sl[NV] -= p * p;
     sh[NV] -= qmin * qmax;
@@ -130,95 +174,69 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 }
 }  // namespace
 
-template <int NV, int PPT>
-__global__ void __launch_bounds__(256) k_tile(TileArgs A) {
+constexpr int SB = 8;            // sub-block edge (pixels)
+constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
+
+template <int NV>
+__global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_item;
+  __shared__ int s_work;
   const int ts = A.ts;
-  const int npix = ts * ts;
-  const int nthr = blockDim.x;
+  const int nsb = ts / SB;          // sub-blocks per tile edge
+  const int nsub = nsb * nsb;
   const int BS = A.bs;
   SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
-  double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][ts]
-  double* cy2 = cx2 + (size_t)BS * ts;                 // [BS][ts]
+  double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][SB]
+  double* cy2 = cx2 + (size_t)BS * SB;                 // [BS][SB]
   const bool has_exc = A.pm != nullptr;
-  float4* ring = has_exc ? A.ring + (size_t)blockIdx.x * A.R * npix : nullptr;
-  const int rmask = A.R - 1;
+  float4* ring = has_exc ? A.ring + (size_t)blockIdx.x * A.R * SBP : nullptr;
+  const int pix = threadIdx.x;
+  const int lx = pix % SB, ly = pix / SB;
+  const float du0 = (float)lx + 0.5f - 0.5f * SB;  // offset from the block centre
+  const float du1 = (float)ly + 0.5f - 0.5f * SB;
   unsigned active = 0;
+  const int nwork = A.n_items * nsub;
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(A.counter, 1);
+    if (threadIdx.x == 0) s_work = atomicAdd(A.counter, 1);
     __syncthreads();
-    const int iidx = s_item;
+    const int w = s_work;
     __syncthreads();
-    if (iidx >= A.n_items) break;
-    const int islot = A.order[iidx];
+    if (w >= nwork) break;
+    const int islot = A.order[w / nsub];
+    const int sub = w % nsub;
     const int4 it = A.items[islot];
     if (it.x < 0) continue;  // padding
     const int tile = it.x, pbeg = it.y, pend = it.z, iflags = it.w;
+    const int4 it2 = A.items2[islot];
+    const int scan0 = it2.x, scan1 = it2.y, anext = it2.z;  // scan [A, L), record at A_next
+    const int rmask = (1 << ((iflags >> 8) & 0xff)) - 1;     // per-item ring length - 1
     const int tx = tile % A.ntx, ty = tile / A.ntx;
+    const int ox = tx * ts + (sub % nsb) * SB, oy = ty * ts + (sub / nsb) * SB;  // block origin
     const int64_t tb = A.tbegin[tile];
-    const double ucx = tx * ts + 0.5 * ts, ucy = ty * ts + 0.5 * ts;  // tile centre
+    const double ucx = ox + 0.5 * SB, ucy = oy + 0.5 * SB;  // block centre
     const bool iexc = has_exc && (iflags & IT_EXC);
+    const bool in_img = (ox + lx < A.W) && (oy + ly < A.H);
+    const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + SB), (double)A.W) - 0.5;
+    const double by0 = oy + 0.5, by1 = fmin((double)(oy + SB), (double)A.H) - 0.5;
+    const bool block_live = ox < A.W && oy < A.H;
+    float Tb = 1.f, Tl = 1.f, ahc[3] = {0.f, 0.f, 0.f}, alc[3] = {0.f, 0.f, 0.f};
+    float recb = 1.f, recl = 1.f;  // running products at A_next (chunk composition)
+    bool rec = false;
 
-    int lx[PPT], ly[PPT];
-    bool in_img[PPT];
-    float du0[PPT], du1[PPT];
-    float Tb[PPT], Tl[PPT], ahc[PPT][3], alc[PPT][3];
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      const int l = threadIdx.x + q * nthr;
-      lx[q] = l % ts;
-      ly[q] = l / ts;
-      in_img[q] = (tx * ts + lx[q] < A.W) && (ty * ts + ly[q] < A.H);
-      du0[q] = (float)lx[q] + 0.5f - 0.5f * ts;
-      du1[q] = (float)ly[q] + 0.5f - 0.5f * ts;
-      Tb[q] = Tl[q] = 1.f;
-      ahc[q][0] = ahc[q][1] = ahc[q][2] = 0.f;
-      alc[q][0] = alc[q][1] = alc[q][2] = 0.f;
-    }
-
-    for (int b0 = pbeg; b0 < pend; b0 += BS) {
-      const int nb = min(BS, pend - b0);
+    for (int b0 = scan0; b0 < scan1; b0 += BS) {
+      const int nb = min(BS, scan1 - b0);
       __syncthreads();
-      // ---- staging: fp64 record -> tile-centred fp32 forms + cull tables + metadata
-      for (int j = threadIdx.x; j < nb; j += nthr) {
+      // ---- staging: fp64 record -> block-centred fp32 forms + cull tables + metadata
+      for (int j = threadIdx.x; j < nb; j += SBP) {
         const int64_t gp = tb + b0 + j;
         const int32_t g = A.vals[gp];
         const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
         SRec<NV>& S = srec[j];
-#pragma unroll
-        for (int k = 0; k <= NV; ++k) {
-          const double d2l = H->d2[0][k], d2h = H->d2[1][k];
-          // x_a lower = u_a D2_lo - DU_a,hi ; upper = u_a D2_hi - DU_a,lo  (u_a > 0)
-          S.xb[0][0][k] = (float)(ucx * d2l - H->du[0][1][k]);
-          S.xb[0][1][k] = (float)(ucx * d2h - H->du[0][0][k]);
-          S.xb[1][0][k] = (float)(ucy * d2l - H->du[1][1][k]);
-          S.xb[1][1][k] = (float)(ucy * d2h - H->du[1][0][k]);
-          S.d2[0][k] = (float)d2l;
-          S.d2[1][k] = (float)d2h;
-        }
-#pragma unroll
-        for (int e = 0; e < 6; ++e) {
-#pragma unroll
-          for (int k = 0; k <= NV; ++k) {
-            S.w[e][0][k] = H->w[e][0][k];
-            S.w[e][1][k] = H->w[e][1][k];
-          }
-          S.wc[e][0] = H->wc[e][0];
-          S.wc[e][1] = H->wc[e][1];
-        }
-        S.o[0] = H->o[0];
-        S.o[1] = H->o[1];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          S.clo[c] = H->clo[c];
-          S.chi[c] = H->chi[c];
-        }
-        S.flags = H->flags;
+        int pmf = 0;
         if (iexc) {
           const int4 m = A.pm[gp];
-          S.pmf = m.x;
+          pmf = m.x;
           S.ph = m.y;
           S.pg = m.z;
           S.pnF = m.w;
@@ -227,17 +245,37 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
           S.pfb = A.fin_b[gp];
           S.pfe = A.fin_e[gp];
         } else {
-          S.pmf = 0;
           S.pfb = S.pfe = 0;
         }
-        S.r2 = H->r2;
+        S.pmf = pmf;
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
-        for (int l = 0; l < ts; ++l) {
-          const double x = tx * ts + l + 0.5, y = ty * ts + l + 0.5;
-          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
-          const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-          cx2[j * ts + l] = __dmul_rn(dx, dx);
-          cy2[j * ts + l] = __dmul_rn(dy, dy);
+        const double r2 = H->r2;
+        int flags = H->flags;
+        {  // whole-block cull (same exact test as the per-pixel one, on the block rectangle)
+          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
+          const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
+          if (!block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2) flags |= F_SKIP;
+        }
+        S.flags = flags;
+        S.r2 = r2;
+        // colours / opacity are read by the blend even for skipped (a = 0) entries
+        S.o[0] = H->o[0];
+        S.o[1] = H->o[1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          S.clo[c] = H->clo[c];
+          S.chi[c] = H->chi[c];
+        }
+        if (!(flags & F_SKIP)) {
+          stage_forms<NV>(S, H, ucx, ucy);
+#pragma unroll
+          for (int l = 0; l < SB; ++l) {
+            const double x = ox + l + 0.5, y = oy + l + 0.5;
+            const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+            const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+            cx2[j * SB + l] = __dmul_rn(dx, dx);
+            cy2[j * SB + l] = __dmul_rn(dy, dy);
+          }
         }
       }
       __syncthreads();
@@ -246,117 +284,108 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
         const SRec<NV>& R = srec[j];
         const int flags = R.flags, pmf = R.pmf;
         const int qpos = b0 + j;  // tile-local position
-        float alo[PPT], ahi[PPT];
-        bool keep[PPT];
-        bool any = false;
-#pragma unroll
-        for (int q = 0; q < PPT; ++q) {
-          keep[q] = in_img[q] && !(__dadd_rn(cx2[j * ts + lx[q]], cy2[j * ts + ly[q]]) > R.r2);
-          any |= keep[q];
-          alo[q] = ahi[q] = 0.f;
+        if (qpos == anext) {
+          recb = Tb;
+          recl = Tl;
+          rec = true;
         }
-        if (__any_sync(FULLM, any)) {
-          if (flags & F_FAIL) {
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-              alo[q] = 0.f;
-              ahi[q] = keep[q] ? R.o[1] : 0.f;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) {
+        if ((flags & F_SKIP) && pmf == 0) continue;  // a = 0 on the whole block: no effect
+        const bool main = qpos >= pbeg && qpos < pend;  // else lookback / lookahead margin
+        float alo = 0.f, ahi = 0.f;
+        bool keep = false;
+        if (!(flags & F_SKIP)) {
+          keep = in_img && !(__dadd_rn(cx2[j * SB + lx], cy2[j * SB + ly]) > R.r2);
+          if (__any_sync(FULLM, keep)) {
+            if (flags & F_FAIL) {
+              ahi = keep ? R.o[1] : 0.f;
+            } else {
               float l, h;
-              opacity<NV>(R, du0[q], du1[q], l, h);
-              alo[q] = keep[q] ? ((flags & F_STRADDLE) ? 0.f : l) : 0.f;
-              ahi[q] = keep[q] ? h : 0.f;
+              opacity<NV>(R, du0, du1, l, h);
+              alo = keep ? ((flags & F_STRADDLE) ? 0.f : l) : 0.f;
+              ahi = keep ? h : 0.f;
             }
           }
         }
-#pragma unroll
-        for (int q = 0; q < PPT; ++q) {
-          active += keep[q] ? 1u : 0u;
-          const int pix = threadIdx.x + q * nthr;
-          if (pmf & PM_STORE)
-            ring[(size_t)(qpos & rmask) * npix + pix] =
-                make_float4(Tb[q], 1.f - alo[q], 1.f - ahi[q], (pmf & PM_EG) ? Tl[q] * alo[q] : 0.f);
-          // upper: T_hi over before(q) \ E_F(q).  Dense windows (mostly E_F): multiply the
-          // window [h, q) skipping E_F.  Sparse windows: divide the running product by the
-          // E_F factors when that is numerically safe (both products far from underflow),
-          // else fall back to the window product (H3).
-          float tbv = Tb[q];
-          if (pmf & PM_EF) {
-            bool done = false;
-            const int wlen = qpos - R.ph;
-            if (wlen > 2 * R.pnF + 8) {
-              float dfac = 1.f;
-              for (int e = 0; e < R.pnF; ++e)
-                dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * npix + pix].y;
-              if (dfac >= 1e-20f && Tb[q] >= 1e-25f) {
-                tbv = Tb[q] / dfac;
-                done = true;
+        active += (keep && main) ? 1u : 0u;
+        if (pmf & PM_STORE)
+          ring[(size_t)(qpos & rmask) * SBP + pix] =
+              make_float4(Tb, 1.f - alo, 1.f - ahi, (pmf & PM_EG) ? Tl * alo : 0.f);
+        // upper: T_hi over before(q) \ E_F(q).  Dense windows (mostly E_F): multiply the
+        // window [h, q) skipping E_F.  Sparse windows: divide the running product by the
+        // E_F factors when that is numerically safe (both products far from underflow),
+        // else fall back to the window product (H3).
+        float tbv = Tb;
+        if (main && (pmf & PM_EF)) {
+          bool done = false;
+          const int wlen = qpos - R.ph;
+          if (wlen > 2 * R.pnF + 8) {
+            float dfac = 1.f;
+            for (int e = 0; e < R.pnF; ++e)
+              dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * SBP + pix].y;
+            if (dfac >= 1e-20f && Tb >= 1e-25f) {
+              tbv = Tb / dfac;
+              done = true;
+            }
+          }
+          if (!done) {
+            tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
+            int e = 0;
+            for (int r = R.ph; r < qpos; ++r) {
+              if (e < R.pnF && A.exc[R.peoff + e] == r) {
+                ++e;
+                continue;
               }
-            }
-            if (!done) {
-              tbv = ring[(size_t)(R.ph & rmask) * npix + pix].x;
-              int e = 0;
-              for (int r = R.ph; r < qpos; ++r) {
-                if (e < R.pnF && A.exc[R.peoff + e] == r) {
-                  ++e;
-                  continue;
-                }
-                tbv *= ring[(size_t)(r & rmask) * npix + pix].y;
-              }
+              tbv *= ring[(size_t)(r & rmask) * SBP + pix].y;
             }
           }
-          const float wb = tbv * ahi[q];
+        }
+        const float wb = main ? tbv * ahi : 0.f;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) ahc[q][c] = fmaf(wb, R.chi[c], ahc[q][c]);
-          // lower: T_lo over before(q) (E_G(q) empty) or deferred to max E_G(q)
-          if (!(pmf & PM_EG)) {
-            const float wl = Tl[q] * alo[q];
+        for (int c = 0; c < 3; ++c) ahc[c] = fmaf(wb, R.chi[c], ahc[c]);
+        // lower: T_lo over before(q) (E_G(q) empty) or deferred to max E_G(q)
+        if (main && !(pmf & PM_EG)) {
+          const float wl = Tl * alo;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) alc[q][c] = fmaf(wl, R.clo[c], alc[q][c]);
+          for (int c = 0; c < 3; ++c) alc[c] = fmaf(wl, R.clo[c], alc[c]);
+        }
+        Tb = fmaf(-Tb, alo, Tb);
+        Tl = fmaf(-Tl, ahi, Tl);
+        // finalise deferred lower contributions of earlier partners whose last later
+        // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
+        for (int f = R.pfb; f < R.pfe; ++f) {
+          const int gq = A.fin_val[f];
+          const int qq = (int)(gq - tb);
+          if (qq < pbeg || qq >= pend) continue;  // another chunk's position
+          const int4 m = A.pm[gq];
+          float tl = ring[(size_t)(qq & rmask) * SBP + pix].w;
+          const int64_t o2 = A.eoff[gq] + m.w;
+          const int ng2 = A.nG[gq];
+          for (int e = 0; e < ng2; ++e) {
+            const int r = A.exc[o2 + e];
+            tl *= ring[(size_t)(r & rmask) * SBP + pix].z;
           }
-          Tb[q] = fmaf(-Tb[q], alo[q], Tb[q]);
-          Tl[q] = fmaf(-Tl[q], ahi[q], Tl[q]);
-          // finalise deferred lower contributions of earlier partners whose last later
-          // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
-          for (int f = R.pfb; f < R.pfe; ++f) {
-            const int gq = A.fin_val[f];
-            const int qq = (int)(gq - tb);
-            const int4 m = A.pm[gq];
-            float tl = ring[(size_t)(qq & rmask) * npix + pix].w;
-            const int64_t o2 = A.eoff[gq] + m.w;
-            const int ng2 = A.nG[gq];
-            for (int e = 0; e < ng2; ++e) {
-              const int r = A.exc[o2 + e];
-              tl *= ring[(size_t)(r & rmask) * npix + pix].z;
-            }
-            const HotRec<NV>* H2 = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[gq];
+          const HotRec<NV>* H2 = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[gq];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) alc[q][c] = fmaf(tl, H2->clo[c], alc[q][c]);
-          }
+          for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, H2->clo[c], alc[c]);
         }
       }
     }
     // ---- epilogue
     if (iflags & IT_SINGLE) {
       // +- N tau, clamp to [0,1], union over sub-boxes (steps 20-22)
-#pragma unroll
-      for (int q = 0; q < PPT; ++q) {
-        const int px = tx * ts + lx[q], py = ty * ts + ly[q];
-        int64_t o;
-        if (A.tile_slot) {
-          o = ((int64_t)A.tile_slot[tile] * npix + (int64_t)ly[q] * ts + lx[q]) * 3;
-        } else {
-          if (!in_img[q]) continue;
-          o = ((int64_t)py * A.W + px) * 3;
-        }
+      const int px = ox + lx, py = oy + ly;
+      int64_t o = -1;
+      if (A.tile_slot) {
+        o = ((int64_t)A.tile_slot[tile] * ts * ts + (int64_t)(py - ty * ts) * ts + (px - tx * ts)) * 3;
+      } else if (in_img) {
+        o = ((int64_t)py * A.W + px) * 3;
+      }
+      if (o >= 0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          float l = fminf(fmaxf(alc[q][c] - A.ntau, 0.f), 1.f);
-          float h = fminf(fmaxf(ahc[q][c] + A.ntau, 0.f), 1.f);
-          if (!in_img[q]) l = h = 0.f;
+          float l = fminf(fmaxf(alc[c] - A.ntau, 0.f), 1.f);
+          float h = fminf(fmaxf(ahc[c] + A.ntau, 0.f), 1.f);
+          if (!in_img) l = h = 0.f;
           if (A.first) {
             A.lo[o + c] = l;
             A.hi[o + c] = h;
@@ -368,13 +397,13 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
       }
     } else {
       // chunk partial: sums relative to the chunk start and the chunk's transmittance
-#pragma unroll
-      for (int q = 0; q < PPT; ++q) {
-        const int pix = threadIdx.x + q * nthr;
-        float4* dst = reinterpret_cast<float4*>(A.partial + ((size_t)islot * npix + pix) * 8);
-        dst[0] = make_float4(ahc[q][0], ahc[q][1], ahc[q][2], Tb[q]);
-        dst[1] = make_float4(alc[q][0], alc[q][1], alc[q][2], Tl[q]);
+      if (!rec) {
+        recb = Tb;
+        recl = Tl;
       }
+      float4* dst = reinterpret_cast<float4*>(A.partial + (((size_t)islot * nsub + sub) * SBP + pix) * 8);
+      dst[0] = make_float4(ahc[0], ahc[1], ahc[2], recb);
+      dst[1] = make_float4(alc[0], alc[1], alc[2], recl);
     }
   }
   // active (pixel, Gaussian) pairs
@@ -384,18 +413,22 @@ __global__ void __launch_bounds__(256) k_tile(TileArgs A) {
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
 }
 
-// front-to-back composition of a tile's chunks: pc = sum_k (prod_{m<k} P_m) S_k
+// front-to-back composition of a tile's chunks: pc = sum_k P(<A_k) S_k with
+// P(<A_{k+1}) = P(<A_k) R_k (R_k = chunk k's running product at A_{k+1})
 __global__ void k_merge(TileArgs A) {
   const int tile = blockIdx.x;
   const int n = A.item_cnt[tile];
   if (n <= 1) return;
-  const int ts = A.ts, npix = ts * ts;
+  const int ts = A.ts, npix = ts * ts, nsb = ts / SB, nsub = nsb * nsb;
   const int tx = tile % A.ntx, ty = tile / A.ntx;
-  for (int pix = threadIdx.x; pix < npix; pix += blockDim.x) {
+  for (int tp = threadIdx.x; tp < npix; tp += blockDim.x) {
+    const int lx = tp % ts, ly = tp / ts;
+    const int sub = (ly / SB) * nsb + lx / SB, pix = (ly % SB) * SB + (lx % SB);
     float Pb = 1.f, Pl = 1.f, h[3] = {0.f, 0.f, 0.f}, l[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < n; ++k) {
       const int64_t it = A.item_off[tile] + k;
-      const float4* src = reinterpret_cast<const float4*>(A.partial + ((size_t)it * npix + pix) * 8);
+      const float4* src =
+          reinterpret_cast<const float4*>(A.partial + (((size_t)it * nsub + sub) * SBP + pix) * 8);
       const float4 a = src[0], b = src[1];
       h[0] = fmaf(Pb, a.x, h[0]);
       h[1] = fmaf(Pb, a.y, h[1]);
@@ -406,12 +439,11 @@ __global__ void k_merge(TileArgs A) {
       Pb *= a.w;
       Pl *= b.w;
     }
-    const int lx = pix % ts, ly = pix / ts;
     const int px = tx * ts + lx, py = ty * ts + ly;
     const bool inside = px < A.W && py < A.H;
     int64_t o;
     if (A.tile_slot) {
-      o = ((int64_t)A.tile_slot[tile] * npix + pix) * 3;
+      o = ((int64_t)A.tile_slot[tile] * npix + tp) * 3;
     } else {
       if (!inside) continue;
       o = ((int64_t)py * A.W + px) * 3;
@@ -431,11 +463,16 @@ __global__ void k_merge(TileArgs A) {
   }
 }
 
-int tile_threads(int ts) { return ts <= 16 ? ts * ts : 256; }
+int tile_threads(int ts) {
+  (void)ts;
+  return SBP;
+}
+int tile_subblocks(int ts) { return (ts / SB) * (ts / SB); }
 
 template <int NV>
 static size_t smem_for(int ts, int bs) {
-  return (size_t)bs * (sizeof(SRec<NV>) + 2 * ts * sizeof(double));
+  (void)ts;
+  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double));
 }
 
 size_t tile_smem_bytes(int nv, int ts, int bs) {
@@ -450,27 +487,25 @@ size_t tile_smem_bytes(int nv, int ts, int bs) {
   }
 }
 
-template <int NV, int PPT>
+template <int NV>
 static int grid_one(int ts, int bs) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_tile<NV, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tile<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   int per_sm = 0, dev = 0, nsm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV, PPT>, tile_threads(ts),
-                                                smem_for<NV>(ts, bs));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV>, SBP, smem_for<NV>(ts, bs));
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   return std::max(1, per_sm) * nsm;
 }
 
 int tile_grid(int nv, int ts, int bs) {
-  const bool four = ts == 32;
   switch (nv) {
 #define CASE(K) \
   case K:       \
-    return four ? grid_one<K, 4>(ts, bs) : grid_one<K, 1>(ts, bs);
+    return grid_one<K>(ts, bs);
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
     default:
@@ -480,14 +515,10 @@ int tile_grid(int nv, int ts, int bs) {
 
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st) {
   if (a.n_items <= 0 || grid <= 0) return;
-  const bool four = a.ts == 32;
   switch (nv) {
-#define CASE(K)                                                                          \
-  case K:                                                                                \
-    if (four)                                                                            \
-      k_tile<K, 4><<<grid, tile_threads(a.ts), smem_for<K>(a.ts, a.bs), st>>>(a);        \
-    else                                                                                 \
-      k_tile<K, 1><<<grid, tile_threads(a.ts), smem_for<K>(a.ts, a.bs), st>>>(a);        \
+#define CASE(K)                                                    \
+  case K:                                                          \
+    k_tile<K><<<grid, SBP, smem_for<K>(a.ts, a.bs), st>>>(a);      \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
