@@ -54,7 +54,7 @@ struct as_ctx {
   DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
   DevBuf tileh, tilemax, wsP, kapP;
   DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
-  DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e;
+  DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e, finrec, maskF, maskG;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
   size_t bytes = 0;
   int64_t launches = 0;
@@ -474,17 +474,24 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
       ensure(ctx, ctx->fin_b, sizeof(int32_t) * M);
       ensure(ctx, ctx->fin_e, sizeof(int32_t) * M);
+      ensure(ctx, ctx->maskF, sizeof(ulonglong2) * M);
+      ensure(ctx, ctx->maskG, sizeof(ulonglong2) * M);
+      ensure(ctx, ctx->finrec, sizeof(FinRec) * M);
       launch_meta(pa, cstore, ccut, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
-                  P<int32_t>(ctx->finval), st);
+                  P<int32_t>(ctx->finval), P<ulonglong2>(ctx->maskF), P<ulonglong2>(ctx->maskG), st);
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
                       P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
       launch_fin_ranges(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->fin_b),
                         P<int32_t>(ctx->fin_e), st);
       LAUNCHED(ctx, 1);
+      launch_finrec(P<uint32_t>(ctx->finkey2), P<int32_t>(ctx->finval2), pa, P<int4>(ctx->pflag),
+                    P<ulonglong2>(ctx->maskG), ctx->hot.p, P<FinRec>(ctx->finrec), st);
+      LAUNCHED(ctx, 1);
       ta.fin_b = P<int32_t>(ctx->fin_b);
       ta.fin_e = P<int32_t>(ctx->fin_e);
-      ta.fin_val = P<int32_t>(ctx->finval2);
+      ta.fin_rec = P<FinRec>(ctx->finrec);
+      ta.mF = P<ulonglong2>(ctx->maskF);
       unsigned int hw = 0;
       CK(cudaMemcpyAsync(&hw, wmax, sizeof hw, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -798,7 +805,8 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->item_off, &ctx->items, &ctx->items2,
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
-                    &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e};
+                    &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e, &ctx->finrec, &ctx->maskF,
+                    &ctx->maskG};
   for (DevBuf* b : bufs) release(ctx, *b);
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);

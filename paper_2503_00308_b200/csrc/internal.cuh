@@ -23,7 +23,7 @@ constexpr double WCAP = 1e12;   // |W| guard -> FAIL (reading O3)
 
 enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4, F_SKIP = 8 };  // F_SKIP: staging-only
 // per list-position flags (exceptions, a9) and work-item flags
-enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8 };
+enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8, PM_OVF = 16 };
 enum : int { IT_EXC = 1, IT_SINGLE = 2 };
 
 // ------------------------------------------------------------------------- pose / box
@@ -276,8 +276,19 @@ void launch_pairs_prep(const PairArgs& a, cudaStream_t st);
 void launch_pairs_count(const PairArgs& a, cudaStream_t st);
 void launch_pairs_fill(const PairArgs& a, cudaStream_t st);
 void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t st);
+// finalisation record of a position q' with later uncertain partners (sorted by max E_G)
+struct alignas(16) FinRec {
+  int qq, nF, nG, flags;   // tile-local position, |E_F|, |E_G|, PM_* flags
+  long long eoff;          // exc[] offset (E_F then E_G), for PM_OVF
+  long long pad0;
+  ulonglong2 mg;           // E_G(q') as bits over (q', q'+128]
+  float clo[3], pad;       // lower colour of q'
+};
 void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st);
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
+                 ulonglong2* mG, cudaStream_t st);
+void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
+                   const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
 void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe, cudaStream_t st);
 void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
                       int64_t* caps, cudaStream_t st);
@@ -311,8 +322,9 @@ struct TileArgs {
   const int64_t* eoff;        // [M+1]
   const int32_t* exc;         // E_F ascending then E_G ascending, tile-local
   const int32_t* fin_b;       // [M] positions whose deferred T_lo is finalised here:
-  const int32_t* fin_e;       //     fin_val[fin_b[p] .. fin_e[p]) (global positions)
-  const int32_t* fin_val;
+  const int32_t* fin_e;       //     fin_rec[fin_b[p] .. fin_e[p])
+  const FinRec* fin_rec;
+  const ulonglong2* mF;       // [M] E_F bits over [h, h+128)
   float4* ring;               // [gridDim][R][ts*ts] (T_hi before, 1-a_lo, 1-a_hi, deferred)
   int R;                      // ring length (power of two > max window)
   float* partial;             // [items][sub-blocks][64][8] chunk partials (multi-chunk tiles)

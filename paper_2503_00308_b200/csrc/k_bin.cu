@@ -319,19 +319,36 @@ void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t
   k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, dstore, dcut);
 }
 
-// per-position metadata for the tile kernel: {flags, h, g, nF}; max window -> wmax
+// per-position metadata for the tile kernel: {flags, h, g, nF}; max window -> wmax;
+// E_F(p) as a 128-bit mask over [h, h+128) and E_G(p) over (p, p+128] (PM_OVF if longer)
 __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                       unsigned int* wmax, uint32_t* finkey, int32_t* finval) {
+                       unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
+                       ulonglong2* mG) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
   const int nF = A.nF[p], nG = A.nG[p];
   const int64_t b = A.tbegin[A.keys[p]];
   const int loc = (int)(p - b);
   const int h = (nF + nG) ? A.hpos[p] : loc;
-  const int g = nG ? A.exc[A.off[p] + nF + nG - 1] : loc;
+  const int64_t off = (nF + nG) ? A.off[p] : 0;
+  const int g = nG ? A.exc[off + nF + nG - 1] : loc;
+  const bool ovf = (loc - h) > 128 || (g - loc) > 128;
   int fl = (nF ? PM_EF : 0) | (nG ? PM_EG : 0) | (cstore[p] > 0 ? PM_STORE : 0) |
-           (ccut[p] > 0 ? PM_NOCUT : 0);
+           (ccut[p] > 0 ? PM_NOCUT : 0) | (ovf ? PM_OVF : 0);
   pm[p] = make_int4(fl, h, g, nF);
+  unsigned long long f0 = 0, f1 = 0, g0 = 0, g1 = 0;
+  if (!ovf) {
+    for (int e = 0; e < nF; ++e) {
+      const int i = A.exc[off + e] - h;
+      if (i < 64) f0 |= 1ull << i; else f1 |= 1ull << (i - 64);
+    }
+    for (int e = 0; e < nG; ++e) {
+      const int i = A.exc[off + nF + e] - loc - 1;
+      if (i < 64) g0 |= 1ull << i; else g1 |= 1ull << (i - 64);
+    }
+  }
+  mF[p] = make_ulonglong2(f0, f1);
+  mG[p] = make_ulonglong2(g0, g1);
   const unsigned w = (unsigned)max(loc - h, g - loc);
   if (w) atomicMax(wmax, w);
   // deferred lower contribution of p is finalised at its last later partner b + g
@@ -339,9 +356,42 @@ __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, i
   finval[p] = (int32_t)p;
 }
 void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st) {
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
+                 ulonglong2* mG, cudaStream_t st) {
   if (a.M <= 0) return;
-  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval);
+  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval,
+                                                        mF, mG);
+}
+
+// finalisation records in sorted order: everything the tile kernel needs about q'
+template <int NV>
+__global__ void k_finrec(const uint32_t* key, const int32_t* val, PairArgs A, const int4* pm,
+                         const ulonglong2* mG, const void* hot, FinRec* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.M) return;
+  if (key[i] == 0xffffffffu) return;
+  const int32_t gq = val[i];
+  const int64_t b = A.tbegin[A.keys[gq]];
+  const int4 m = pm[gq];
+  const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(hot) + A.vals[gq];
+  FinRec r;
+  r.qq = (int)(gq - b);
+  r.nF = m.w;
+  r.nG = A.nG[gq];
+  r.flags = m.x;
+  r.eoff = A.off[gq];
+  r.mg = mG[gq];
+  r.clo[0] = H->clo[0];
+  r.clo[1] = H->clo[1];
+  r.clo[2] = H->clo[2];
+  r.pad = 0.f;
+  out[i] = r;
+}
+void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
+                   const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st) {
+  if (a.M <= 0) return;
+  const unsigned blocks = (unsigned)((a.M + 255) / 256);
+  NV_SWITCH(a.nv, (k_finrec<NVc><<<blocks, 256, 0, st>>>(key, val, a, pm, mG, hot, out)));
 }
 
 // CSR of the finalisation lists: sorted keys -> [fin_b, fin_e) per position

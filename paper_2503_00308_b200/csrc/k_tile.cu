@@ -53,6 +53,7 @@ struct alignas(16) SRec {
   int pmf, ph, pg, pnF, pnG;  // position metadata (PM_*, h, g, |E_F|, |E_G|)
   int pfb, pfe;             // finalisation list range
   long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
+  unsigned long long mf0, mf1;  // E_F(p) bits over [h, h+128)
   double r2;
 };
 
@@ -63,17 +64,26 @@ struct alignas(16) SRec {
 // (R1 with the constant w = conc W), both affine in du_a.
 template <int NV>
 __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, double ucx,
-                                            double ucy) {
+                                            double ucy, int part) {
   constexpr int C = NV + 1;
   const double uc[2] = {ucx, ucy};
-  double wl[6], wh[6];
+  if (part == 3) {  // x lower forms and concretised W
 #pragma unroll
-  for (int e = 0; e < 6; ++e) {
-    wl[e] = H->wc[e][0];
-    wh[e] = H->wc[e][1];
-    S.wc[e][0] = H->wc[e][0];
-    S.wc[e][1] = H->wc[e][1];
+    for (int e = 0; e < 6; ++e) {
+      S.wc[e][0] = H->wc[e][0];
+      S.wc[e][1] = H->wc[e][1];
+    }
+#pragma unroll 1
+    for (int k = 0; k < C; ++k) {
+      const double d2l = H->d2[0][k];
+      S.xb[0][k] = (float)(uc[0] * d2l - H->du[0][1][k]);
+      S.xb[1][k] = (float)(uc[1] * d2l - H->du[1][1][k]);
+      S.d2lo[k] = (float)d2l;
+    }
+    return;
   }
+  const int c = part;  // channel c of q
+  const double w0l = H->wc[c][0], w0h = H->wc[c][1], w1l = H->wc[3 + c][0], w1h = H->wc[3 + c][1];
 #pragma unroll 1
   for (int k = 0; k < C; ++k) {
     const double d2l = H->d2[0][k], d2h = H->d2[1][k];
@@ -82,25 +92,19 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
     for (int a = 0; a < 2; ++a) {
       blo[a] = uc[a] * d2l - H->du[a][1][k];
       bhi[a] = uc[a] * d2h - H->du[a][0][k];
-      S.xb[a][k] = (float)blo[a];
     }
-    S.d2lo[k] = (float)d2l;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
-      S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
-      S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
-      S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
-      S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
-      S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
-      S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
-      const double a0 = H->w[c][0][k], b0 = H->w[c][1][k];
-      const double a1 = H->w[3 + c][0][k], b1 = H->w[3 + c][1][k];
-      S.wm0[c][k] = (float)(0.5 * (a0 + b0));
-      S.wr0[c][k] = (float)(0.5 * (b0 - a0));
-      S.wm1[c][k] = (float)(0.5 * (a1 + b1));
-      S.wr1[c][k] = (float)(0.5 * (b1 - a1));
-    }
+    S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
+    S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
+    S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
+    S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
+    S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
+    S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
+    const double a0 = H->w[c][0][k], b0 = H->w[c][1][k];
+    const double a1 = H->w[3 + c][0][k], b1 = H->w[3 + c][1][k];
+    S.wm0[c][k] = (float)(0.5 * (a0 + b0));
+    S.wr0[c][k] = (float)(0.5 * (b0 - a0));
+    S.wm1[c][k] = (float)(0.5 * (a1 + b1));
+    S.wr1[c][k] = (float)(0.5 * (b1 - a1));
   }
 }
 
@@ -228,55 +232,62 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
       const int nb = min(BS, scan1 - b0);
       __syncthreads();
       // ---- staging: fp64 record -> block-centred fp32 forms + cull tables + metadata
-      for (int j = threadIdx.x; j < nb; j += SBP) {
+      //      four threads per Gaussian: parts 0-2 stage channel c of q, part 3 the rest
+      for (int jj = threadIdx.x; jj < 4 * nb; jj += SBP) {
+        const int j = jj >> 2, part = jj & 3;
         const int64_t gp = tb + b0 + j;
         const int32_t g = A.vals[gp];
         const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
         SRec<NV>& S = srec[j];
-        int pmf = 0;
-        if (iexc) {
-          const int4 m = A.pm[gp];
-          pmf = m.x;
-          S.ph = m.y;
-          S.pg = m.z;
-          S.pnF = m.w;
-          S.pnG = A.nG[gp];
-          S.peoff = A.eoff[gp];
-          S.pfb = A.fin_b[gp];
-          S.pfe = A.fin_e[gp];
-        } else {
-          S.pfb = S.pfe = 0;
-        }
-        S.pmf = pmf;
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
         const double r2 = H->r2;
-        int flags = H->flags;
+        bool skip;
         {  // whole-block cull (same exact test as the per-pixel one, on the block rectangle)
           const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
           const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
-          if (!block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2) flags |= F_SKIP;
+          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
         }
-        S.flags = flags;
-        S.r2 = r2;
-        // colours / opacity are read by the blend even for skipped (a = 0) entries
-        S.o[0] = H->o[0];
-        S.o[1] = H->o[1];
+        if (part == 3) {
+          int pmf = 0;
+          if (iexc) {
+            const int4 m = A.pm[gp];
+            pmf = m.x;
+            S.ph = m.y;
+            S.pg = m.z;
+            S.pnF = m.w;
+            S.pnG = A.nG[gp];
+            S.peoff = A.eoff[gp];
+            S.pfb = A.fin_b[gp];
+            S.pfe = A.fin_e[gp];
+            const ulonglong2 mf = A.mF[gp];
+            S.mf0 = mf.x;
+            S.mf1 = mf.y;
+          } else {
+            S.pfb = S.pfe = 0;
+          }
+          S.pmf = pmf;
+          S.flags = H->flags | (skip ? F_SKIP : 0);
+          S.r2 = r2;
+          // colours / opacity are read by the blend even for skipped (a = 0) entries
+          S.o[0] = H->o[0];
+          S.o[1] = H->o[1];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          S.clo[c] = H->clo[c];
-          S.chi[c] = H->chi[c];
-        }
-        if (!(flags & F_SKIP)) {
-          stage_forms<NV>(S, H, ucx, ucy);
+          for (int c = 0; c < 3; ++c) {
+            S.clo[c] = H->clo[c];
+            S.chi[c] = H->chi[c];
+          }
+          if (!skip) {
 #pragma unroll
-          for (int l = 0; l < SB; ++l) {
-            const double x = ox + l + 0.5, y = oy + l + 0.5;
-            const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
-            const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-            cx2[j * SB + l] = __dmul_rn(dx, dx);
-            cy2[j * SB + l] = __dmul_rn(dy, dy);
+            for (int l = 0; l < SB; ++l) {
+              const double x = ox + l + 0.5, y = oy + l + 0.5;
+              const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+              const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+              cx2[j * SB + l] = __dmul_rn(dx, dx);
+              cy2[j * SB + l] = __dmul_rn(dy, dy);
+            }
           }
         }
+        if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
       }
       __syncthreads();
       // ---- walk the batch in (kappa, index) order
@@ -316,26 +327,53 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         // else fall back to the window product (H3).
         float tbv = Tb;
         if (main && (pmf & PM_EF)) {
-          bool done = false;
           const int wlen = qpos - R.ph;
-          if (wlen > 2 * R.pnF + 8) {
-            float dfac = 1.f;
-            for (int e = 0; e < R.pnF; ++e)
-              dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * SBP + pix].y;
-            if (dfac >= 1e-20f && Tb >= 1e-25f) {
-              tbv = Tb / dfac;
-              done = true;
-            }
-          }
-          if (!done) {
-            tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
-            int e = 0;
-            for (int r = R.ph; r < qpos; ++r) {
-              if (e < R.pnF && A.exc[R.peoff + e] == r) {
-                ++e;
-                continue;
+          if (!(pmf & PM_OVF)) {
+            // window [h, q) as bits: set = E_F (excluded), clear = multiplied
+            const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+            const unsigned long long v1 =
+                wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+            const int nkeep = wlen - R.pnF;
+            bool done = false;
+            if (nkeep > R.pnF + 2) {  // sparse E_F: divide the running product (guarded)
+              float dfac = 1.f;
+              for (unsigned long long m = R.mf0; m; m &= m - 1)
+                dfac *= ring[(size_t)((R.ph + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+              for (unsigned long long m = R.mf1; m; m &= m - 1)
+                dfac *= ring[(size_t)((R.ph + 64 + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+              if (dfac >= 1e-20f && Tb >= 1e-25f) {
+                tbv = Tb / dfac;
+                done = true;
               }
-              tbv *= ring[(size_t)(r & rmask) * SBP + pix].y;
+            }
+            if (!done) {  // dense E_F: T_hi before h times the kept factors of the window
+              tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
+              for (unsigned long long m = ~R.mf0 & v0; m; m &= m - 1)
+                tbv *= ring[(size_t)((R.ph + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+              for (unsigned long long m = ~R.mf1 & v1; m; m &= m - 1)
+                tbv *= ring[(size_t)((R.ph + 64 + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+            }
+          } else {  // long window: exception lists from global memory
+            bool done = false;
+            if (wlen > 2 * R.pnF + 8) {
+              float dfac = 1.f;
+              for (int e = 0; e < R.pnF; ++e)
+                dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * SBP + pix].y;
+              if (dfac >= 1e-20f && Tb >= 1e-25f) {
+                tbv = Tb / dfac;
+                done = true;
+              }
+            }
+            if (!done) {
+              tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
+              int e = 0;
+              for (int r = R.ph; r < qpos; ++r) {
+                if (e < R.pnF && A.exc[R.peoff + e] == r) {
+                  ++e;
+                  continue;
+                }
+                tbv *= ring[(size_t)(r & rmask) * SBP + pix].y;
+              }
             }
           }
         }
@@ -353,20 +391,21 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         // finalise deferred lower contributions of earlier partners whose last later
         // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
         for (int f = R.pfb; f < R.pfe; ++f) {
-          const int gq = A.fin_val[f];
-          const int qq = (int)(gq - tb);
-          if (qq < pbeg || qq >= pend) continue;  // another chunk's position
-          const int4 m = A.pm[gq];
-          float tl = ring[(size_t)(qq & rmask) * SBP + pix].w;
-          const int64_t o2 = A.eoff[gq] + m.w;
-          const int ng2 = A.nG[gq];
-          for (int e = 0; e < ng2; ++e) {
-            const int r = A.exc[o2 + e];
-            tl *= ring[(size_t)(r & rmask) * SBP + pix].z;
+          const FinRec fr = A.fin_rec[f];
+          if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
+          float tl = ring[(size_t)(fr.qq & rmask) * SBP + pix].w;
+          if (!(fr.flags & PM_OVF)) {
+            for (unsigned long long m = fr.mg.x; m; m &= m - 1)
+              tl *= ring[(size_t)((fr.qq + __ffsll((long long)m)) & rmask) * SBP + pix].z;
+            for (unsigned long long m = fr.mg.y; m; m &= m - 1)
+              tl *= ring[(size_t)((fr.qq + 64 + __ffsll((long long)m)) & rmask) * SBP + pix].z;
+          } else {
+            const int64_t o2 = fr.eoff + fr.nF;
+            for (int e = 0; e < fr.nG; ++e)
+              tl *= ring[(size_t)(A.exc[o2 + e] & rmask) * SBP + pix].z;
           }
-          const HotRec<NV>* H2 = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[gq];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, H2->clo[c], alc[c]);
+          for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, fr.clo[c], alc[c]);
         }
       }
     }
