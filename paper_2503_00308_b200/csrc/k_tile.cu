@@ -33,6 +33,9 @@ namespace {
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 
+constexpr int TL_MAX = 12;       // T_hi window operands precomputed per position
+constexpr int EG_MAX = 8;        // E_G operands precomputed per staged finalisation record
+
 template <int NV>
 struct alignas(16) SRec {
   static constexpr int C = NV + 1;
@@ -54,7 +57,18 @@ struct alignas(16) SRec {
   int pfb, pfe;             // finalisation list range
   long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
   unsigned long long mf0, mf1;  // E_F(p) bits over [h, h+128)
+  // precomputed ring operands of the T_hi window (float offsets of ring slots, without pix)
+  int tmode;                // 0 none, 1 dense (th, tl = kept), 2 sparse (tl = E_F), 3 slow
+  int nT, th, pad2;
+  int tl[TL_MAX];
   double r2;
+};
+// finalisation record staged in shared memory with its E_G ring slots precomputed
+struct FinS {
+  int qslot;                // ring float offset of q' (-1: q' not in this chunk's main range)
+  int n;                    // |E_G(q')| slots below, -1 = too many (slow path)
+  float clo[3];
+  int slot[EG_MAX];
 };
 
 // Staging of one Gaussian for a block centred at (ucx, ucy): fp64 arithmetic, one rounding.
@@ -180,6 +194,33 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 
 constexpr int SB = 8;            // sub-block edge (pixels)
 constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
+constexpr int FIN_S = 2;         // finalisation records staged in shared memory per position
+
+// product of ring component `comp` over the positions base + i for the set bits i of the
+// 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap
+__device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m0,
+                                           unsigned long long m1, int base, int comp, int rmask,
+                                           int pix) {
+  float prod = 1.f;
+  while (m0 | m1) {
+    float v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int idx = -1;
+      if (m0) {
+        idx = base + __ffsll((long long)m0) - 1;
+        m0 &= m0 - 1;
+      } else if (m1) {
+        idx = base + 64 + __ffsll((long long)m1) - 1;
+        m1 &= m1 - 1;
+      }
+      v[t] = idx >= 0 ? rf[((size_t)(idx & rmask) * SBP + pix) * 4 + comp] : 1.f;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) prod *= v[t];
+  }
+  return prod;
+}
 
 template <int NV>
 __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
@@ -192,6 +233,7 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
   SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
   double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][SB]
   double* cy2 = cx2 + (size_t)BS * SB;                 // [BS][SB]
+  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SB);  // [BS][FIN_S]
   const bool has_exc = A.pm != nullptr;
   float4* ring = has_exc ? A.ring + (size_t)blockIdx.x * A.R * SBP : nullptr;
   const int pix = threadIdx.x;
@@ -262,8 +304,52 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
             const ulonglong2 mf = A.mF[gp];
             S.mf0 = mf.x;
             S.mf1 = mf.y;
+            // T_hi window operands as ring slot offsets (uniform for the whole block)
+            const int qpos = b0 + j;
+            int tmode = 0, nT = 0;
+            if ((pmf & PM_EF) && qpos >= pbeg && qpos < pend && !(pmf & PM_OVF)) {
+              const int h = m.y, wlen = qpos - h;
+              const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+              const unsigned long long v1 =
+                  wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+              const bool dense = !(wlen - m.w > m.w + 2);
+              unsigned long long m0 = dense ? (~mf.x & v0) : mf.x;
+              unsigned long long m1 = dense ? (~mf.y & v1) : mf.y;
+              const int cnt = __popcll(m0) + __popcll(m1);
+              if (cnt <= TL_MAX) {
+                tmode = dense ? 1 : 2;
+                for (; m0; m0 &= m0 - 1) S.tl[nT++] = ((h + __ffsll((long long)m0) - 1) & rmask) * SBP * 4;
+                for (; m1; m1 &= m1 - 1) S.tl[nT++] = ((h + 64 + __ffsll((long long)m1) - 1) & rmask) * SBP * 4;
+                S.th = (h & rmask) * SBP * 4;
+              } else {
+                tmode = 3;
+              }
+            }
+            S.tmode = tmode;
+            S.nT = nT;
+            // finalisation records with their E_G ring slots
+            for (int e = 0; e < FIN_S && S.pfb + e < S.pfe; ++e) {
+              const FinRec fr = A.fin_rec[S.pfb + e];
+              FinS& F = fins[j * FIN_S + e];
+              F.qslot = (fr.qq >= pbeg && fr.qq < pend) ? (fr.qq & rmask) * SBP * 4 : -1;
+              F.clo[0] = fr.clo[0];
+              F.clo[1] = fr.clo[1];
+              F.clo[2] = fr.clo[2];
+              int n = 0;
+              if (!(fr.flags & PM_OVF) && __popcll(fr.mg.x) + __popcll(fr.mg.y) <= EG_MAX) {
+                for (unsigned long long mm = fr.mg.x; mm; mm &= mm - 1)
+                  F.slot[n++] = ((fr.qq + __ffsll((long long)mm)) & rmask) * SBP * 4;
+                for (unsigned long long mm = fr.mg.y; mm; mm &= mm - 1)
+                  F.slot[n++] = ((fr.qq + 64 + __ffsll((long long)mm)) & rmask) * SBP * 4;
+              } else {
+                n = -1;
+              }
+              F.n = n;
+            }
           } else {
             S.pfb = S.pfe = 0;
+            S.tmode = 0;
+            S.nT = 0;
           }
           S.pmf = pmf;
           S.flags = H->flags | (skip ? F_SKIP : 0);
@@ -329,29 +415,30 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         if (main && (pmf & PM_EF)) {
           const int wlen = qpos - R.ph;
           if (!(pmf & PM_OVF)) {
-            // window [h, q) as bits: set = E_F (excluded), clear = multiplied
-            const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
-            const unsigned long long v1 =
-                wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
-            const int nkeep = wlen - R.pnF;
+            const float* rf = reinterpret_cast<const float*>(ring) + pix * 4;
             bool done = false;
-            if (nkeep > R.pnF + 2) {  // sparse E_F: divide the running product (guarded)
+            if (R.tmode == 1) {  // dense: T_hi before h times the kept factors
+              float pr = rf[R.th];
+#pragma unroll 4
+              for (int t = 0; t < R.nT; ++t) pr *= rf[R.tl[t] + 1];
+              tbv = pr;
+              done = true;
+            } else if (R.tmode == 2) {  // sparse: divide the running product (guarded, H3)
               float dfac = 1.f;
-              for (unsigned long long m = R.mf0; m; m &= m - 1)
-                dfac *= ring[(size_t)((R.ph + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
-              for (unsigned long long m = R.mf1; m; m &= m - 1)
-                dfac *= ring[(size_t)((R.ph + 64 + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+#pragma unroll 4
+              for (int t = 0; t < R.nT; ++t) dfac *= rf[R.tl[t] + 1];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
               }
             }
-            if (!done) {  // dense E_F: T_hi before h times the kept factors of the window
-              tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
-              for (unsigned long long m = ~R.mf0 & v0; m; m &= m - 1)
-                tbv *= ring[(size_t)((R.ph + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
-              for (unsigned long long m = ~R.mf1 & v1; m; m &= m - 1)
-                tbv *= ring[(size_t)((R.ph + 64 + __ffsll((long long)m) - 1) & rmask) * SBP + pix].y;
+            if (!done) {  // many operands or unsafe division: window product from the bits
+              const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+              const unsigned long long v1 =
+                  wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+              const float* rb = reinterpret_cast<const float*>(ring);
+              tbv = rb[((size_t)(R.ph & rmask) * SBP + pix) * 4 + 0] *
+                    ring_prod(rb, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask, pix);
             }
           } else {  // long window: exception lists from global memory
             bool done = false;
@@ -391,14 +478,35 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         // finalise deferred lower contributions of earlier partners whose last later
         // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
         for (int f = R.pfb; f < R.pfe; ++f) {
+          if (f - R.pfb < FIN_S) {
+            const FinS& F = fins[j * FIN_S + (f - R.pfb)];
+            if (F.qslot < 0) continue;  // another chunk's position
+            const float* rf = reinterpret_cast<const float*>(ring) + pix * 4;
+            float tl = rf[F.qslot + 3];
+            if (F.n >= 0) {
+#pragma unroll 4
+              for (int e = 0; e < F.n; ++e) tl *= rf[F.slot[e] + 2];
+            } else {
+              const FinRec fr = A.fin_rec[f];
+              if (!(fr.flags & PM_OVF)) {
+                tl *= ring_prod(reinterpret_cast<const float*>(ring), fr.mg.x, fr.mg.y, fr.qq + 1, 2,
+                                rmask, pix);
+              } else {
+                const int64_t o2 = fr.eoff + fr.nF;
+                for (int e = 0; e < fr.nG; ++e)
+                  tl *= ring[(size_t)(A.exc[o2 + e] & rmask) * SBP + pix].z;
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, F.clo[c], alc[c]);
+            continue;
+          }
           const FinRec fr = A.fin_rec[f];
           if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
           float tl = ring[(size_t)(fr.qq & rmask) * SBP + pix].w;
           if (!(fr.flags & PM_OVF)) {
-            for (unsigned long long m = fr.mg.x; m; m &= m - 1)
-              tl *= ring[(size_t)((fr.qq + __ffsll((long long)m)) & rmask) * SBP + pix].z;
-            for (unsigned long long m = fr.mg.y; m; m &= m - 1)
-              tl *= ring[(size_t)((fr.qq + 64 + __ffsll((long long)m)) & rmask) * SBP + pix].z;
+            tl *= ring_prod(reinterpret_cast<const float*>(ring), fr.mg.x, fr.mg.y, fr.qq + 1, 2,
+                            rmask, pix);
           } else {
             const int64_t o2 = fr.eoff + fr.nF;
             for (int e = 0; e < fr.nG; ++e)
@@ -511,7 +619,7 @@ int tile_subblocks(int ts) { return (ts / SB) * (ts / SB); }
 template <int NV>
 static size_t smem_for(int ts, int bs) {
   (void)ts;
-  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double));
+  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double) + FIN_S * sizeof(FinS));
 }
 
 size_t tile_smem_bytes(int nv, int ts, int bs) {
