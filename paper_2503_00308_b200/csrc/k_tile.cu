@@ -33,8 +33,8 @@ namespace {
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 
-constexpr int TL_MAX = 12;       // T_hi window operands precomputed per position
-constexpr int EG_MAX = 8;        // E_G operands precomputed per staged finalisation record
+constexpr int TL_MAX = 24;       // T_hi window operands precomputed per position
+constexpr int EG_MAX = 12;        // E_G operands precomputed per staged finalisation record
 
 template <int NV>
 struct alignas(16) SRec {
@@ -64,7 +64,7 @@ struct alignas(16) SRec {
   double r2;
 };
 // finalisation record staged in shared memory with its E_G ring slots precomputed
-struct FinS {
+struct alignas(16) FinS {
   int qslot;                // ring float offset of q' (-1: q' not in this chunk's main range)
   int n;                    // |E_G(q')| slots below, -1 = too many (slow path)
   float clo[3];
@@ -194,7 +194,7 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 
 constexpr int SB = 8;            // sub-block edge (pixels)
 constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
-constexpr int FIN_S = 2;         // finalisation records staged in shared memory per position
+constexpr int FIN_S = 3;         // finalisation records staged in shared memory per position
 
 // product of ring component `comp` over the positions base + i for the set bits i of the
 // 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap
