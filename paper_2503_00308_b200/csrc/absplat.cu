@@ -52,7 +52,7 @@ struct as_ctx {
   DevBuf pose, hot, pair, kkey, kkey2, kval, order, counts, offsets, cub_tmp;
   DevBuf keys, keys2, vals, vals2, tbegin, tend, tcost, tkey, tkey2, tids, tlist, tslot, owner;
   DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
-  DevBuf tileh, tilemax, wsP, kapP;
+  DevBuf tileh, tilemax, wsP, kapP, posD;
   DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
   DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e, finrec, maskF, maskG;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
@@ -413,6 +413,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     ensure(ctx, ctx->eoff, sizeof(int64_t) * (M + 1));
     ensure(ctx, ctx->wsP, sizeof(double) * M);
     ensure(ctx, ctx->kapP, sizeof(double) * M);
+    ensure(ctx, ctx->posD, sizeof(double) * 2 * (nv + 1) * M);
     ensure(ctx, ctx->tileh, sizeof(double) * (NVMAX + 1) * G.ntiles);
     ensure(ctx, ctx->tilemax, sizeof(unsigned long long) * G.ntiles);
     PairArgs pa{};
@@ -435,6 +436,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     pa.tilemax = P<unsigned long long>(ctx->tilemax);
     pa.wsP = P<double>(ctx->wsP);
     pa.kapP = P<double>(ctx->kapP);
+    pa.posD = P<double>(ctx->posD);
     pa.nF = P<int32_t>(ctx->nF);
     pa.nG = P<int32_t>(ctx->nG);
     pa.ntot = P<int64_t>(ctx->ntot);
@@ -802,7 +804,7 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->diff, &ctx->cover,
                     &ctx->pflag, &ctx->is_store, &ctx->slot, &ctx->scratch, &ctx->img_lo,
                     &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map, &ctx->tileh,
-                    &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->item_off, &ctx->items, &ctx->items2,
+                    &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->posD, &ctx->item_off, &ctx->items, &ctx->items2,
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
                     &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e, &ctx->finrec, &ctx->maskF,

@@ -159,6 +159,45 @@ __device__ __forceinline__ PairRec<NV> load_pair(const void* base, int32_t g) {
   return reinterpret_cast<const PairRec<NV>*>(base)[g];
 }
 
+// depth form of position q from the position-ordered copy (d lower then upper coefficients)
+template <int NV>
+struct DForm {
+  double l[NV + 1], u[NV + 1];
+};
+template <int NV>
+__device__ __forceinline__ DForm<NV> load_posd(const double* posD, int64_t q) {
+  DForm<NV> f;
+  const double* D = posD + (size_t)q * 2 * (NV + 1);
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    f.l[k] = D[k];
+    f.u[k] = D[NV + 1 + k];
+  }
+  return f;
+}
+template <int NV>
+__device__ __forceinline__ int ind_class_d(const DForm<NV>& Pi, int32_t i, const DForm<NV>& Pj,
+                                           int32_t j) {
+  double dl = __dsub_rn(Pi.l[NV], Pj.u[NV]);
+  double du = __dsub_rn(Pi.u[NV], Pj.l[NV]);
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    s1 = __dadd_rn(s1, fabs(__dsub_rn(Pi.l[k], Pj.u[k])));
+    s2 = __dadd_rn(s2, fabs(__dsub_rn(Pi.u[k], Pj.l[k])));
+  }
+  dl = __dsub_rn(dl, s1);
+  du = __dadd_rn(du, s2);
+  if (i > j) {
+    if (dl >= 0.0) return 1;
+    if (du < 0.0) return 0;
+  } else {
+    if (dl > 0.0) return 1;
+    if (du <= 0.0) return 0;
+  }
+  return -1;
+}
+
 // Window bound (SURVEY §8(c) step 13 pruning, slope-aware).  For any vector h and
 // m_i = g0 + kappa_i h:  |lA_i - uA_j|_1 <= S'_i + |kappa_i - kappa_j| |h|_1 + S'_j with
 // S'_i = max(|lA_i - m_i|_1, |uA_i - m_i|_1).  A '?' pair (j before i) needs
@@ -210,6 +249,14 @@ __global__ void k_pairs_prep(PairArgs A) {
   const double ws = 0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2);
   A.wsP[p] = ws;
   A.kapP[p] = Pi.kappa;
+  // position-ordered copy of the depth form: the window scans then read neighbours
+  // contiguously instead of gathering PairRec by Gaussian id
+  double* D = A.posD + (size_t)p * 2 * (NV + 1);
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    D[k] = Pi.dl[k];
+    D[NV + 1 + k] = Pi.du[k];
+  }
   atomicMax(&A.tilemax[t], (unsigned long long)__double_as_longlong(ws));
 }
 
@@ -227,7 +274,8 @@ __global__ void k_pairs(PairArgs A) {
   const uint32_t t = A.keys[p];
   const int64_t b = A.tbegin[t], e = A.tend[t];
   const int32_t gi = A.vals[p];
-  const PairRec<NV> Pi = load_pair<NV>(A.pair, gi);
+  const DForm<NV> Pi = load_posd<NV>(A.posD, p);
+  const double ki = A.kapP[p];
   const double M = __longlong_as_double((long long)A.tilemax[t]);
   const double factor = A.tileh[(size_t)t * (NVMAX + 1) + NVMAX];
   const double wsi = A.wsP[p];
@@ -242,10 +290,9 @@ __global__ void k_pairs(PairArgs A) {
   // backward: earlier positions (expected Ind in {1, ?})
   for (int64_t q = p - 1; q >= b; --q) {
     const double kj = A.kapP[q];
-    if (beyond(Pi.kappa - kj, factor, wsi, M, Pi.kappa, kj)) break;
+    if (beyond(ki - kj, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
-    const int c = ind_class<NV>(Pi, gi, Pj, gj);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj);
     if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
       if (c == 0) ++viol;
       if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
@@ -256,10 +303,9 @@ __global__ void k_pairs(PairArgs A) {
   // forward: later positions (expected Ind in {0, ?})
   for (int64_t q = p + 1; q < e; ++q) {
     const double kj = A.kapP[q];
-    if (beyond(kj - Pi.kappa, factor, wsi, M, Pi.kappa, kj)) break;
+    if (beyond(kj - ki, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const PairRec<NV> Pj = load_pair<NV>(A.pair, gj);
-    const int c = ind_class<NV>(Pi, gi, Pj, gj);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj);
     if (c == -1 || c == 1) {
       if (c == 1) ++viol;
       if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);
