@@ -33,6 +33,9 @@ namespace {
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 
+constexpr int SB = 8;            // sub-block edge (pixels)
+constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
+constexpr int FIN_S = 3;         // finalisation records staged in shared memory per position
 constexpr int TL_MAX = 24;       // T_hi window operands precomputed per position
 constexpr int EG_MAX = 12;        // E_G operands precomputed per staged finalisation record
 
@@ -192,15 +195,18 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 }
 }  // namespace
 
-constexpr int SB = 8;            // sub-block edge (pixels)
-constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
-constexpr int FIN_S = 3;         // finalisation records staged in shared memory per position
+
+// Ring layout (per CTA): [slot][component][pixel] floats, so a warp's load of one component
+// is one contiguous 128-byte line.  Components: 0 T_hi before q, 1 (1 - a_lo,q),
+// 2 (1 - a_hi,q), 3 deferred T_lo a_lo,q.  RS = float offset of (slot, comp) without pixel.
+__device__ __forceinline__ int RS(int pos, int comp, int rmask) {
+  return ((pos & rmask) * 4 + comp) * SBP;
+}
 
 // product of ring component `comp` over the positions base + i for the set bits i of the
-// 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap
+// 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap.  rf = ring + pix.
 __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m0,
-                                           unsigned long long m1, int base, int comp, int rmask,
-                                           int pix) {
+                                           unsigned long long m1, int base, int comp, int rmask) {
   float prod = 1.f;
   while (m0 | m1) {
     float v[8];
@@ -214,7 +220,7 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
         idx = base + 64 + __ffsll((long long)m1) - 1;
         m1 &= m1 - 1;
       }
-      v[t] = idx >= 0 ? rf[((size_t)(idx & rmask) * SBP + pix) * 4 + comp] : 1.f;
+      v[t] = idx >= 0 ? rf[RS(idx, comp, rmask)] : 1.f;
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) prod *= v[t];
@@ -235,8 +241,9 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
   double* cy2 = cx2 + (size_t)BS * SB;                 // [BS][SB]
   FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SB);  // [BS][FIN_S]
   const bool has_exc = A.pm != nullptr;
-  float4* ring = has_exc ? A.ring + (size_t)blockIdx.x * A.R * SBP : nullptr;
   const int pix = threadIdx.x;
+  float* rf = has_exc ? reinterpret_cast<float*>(A.ring) + (size_t)blockIdx.x * A.R * SBP * 4 + pix
+                      : nullptr;
   const int lx = pix % SB, ly = pix / SB;
   const float du0 = (float)lx + 0.5f - 0.5f * SB;  // offset from the block centre
   const float du1 = (float)ly + 0.5f - 0.5f * SB;
@@ -404,9 +411,15 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
           }
         }
         active += (keep && main) ? 1u : 0u;
-        if (pmf & PM_STORE)
-          ring[(size_t)(qpos & rmask) * SBP + pix] =
-              make_float4(Tb, 1.f - alo, 1.f - ahi, (pmf & PM_EG) ? Tl * alo : 0.f);
+        if (pmf & PM_STORE) {
+          // (1 - a_hi) is read only through E_G of earlier partners (q has PM_EF), the
+          // deferred lower term only at q's own finalisation (PM_EG)
+          const int rs = RS(qpos, 0, rmask);
+          rf[rs] = Tb;
+          rf[rs + SBP] = 1.f - alo;
+          if (pmf & PM_EF) rf[rs + 2 * SBP] = 1.f - ahi;
+          if (pmf & PM_EG) rf[rs + 3 * SBP] = Tl * alo;
+        }
         // upper: T_hi over before(q) \ E_F(q).  Dense windows (mostly E_F): multiply the
         // window [h, q) skipping E_F.  Sparse windows: divide the running product by the
         // E_F factors when that is numerically safe (both products far from underflow),
@@ -415,18 +428,17 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         if (main && (pmf & PM_EF)) {
           const int wlen = qpos - R.ph;
           if (!(pmf & PM_OVF)) {
-            const float* rf = reinterpret_cast<const float*>(ring) + pix * 4;
             bool done = false;
             if (R.tmode == 1) {  // dense: T_hi before h times the kept factors
               float pr = rf[R.th];
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) pr *= rf[R.tl[t] + 1];
+              for (int t = 0; t < R.nT; ++t) pr *= rf[R.tl[t] + SBP];
               tbv = pr;
               done = true;
             } else if (R.tmode == 2) {  // sparse: divide the running product (guarded, H3)
               float dfac = 1.f;
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) dfac *= rf[R.tl[t] + 1];
+              for (int t = 0; t < R.nT; ++t) dfac *= rf[R.tl[t] + SBP];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
@@ -436,30 +448,28 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
               const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
               const unsigned long long v1 =
                   wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
-              const float* rb = reinterpret_cast<const float*>(ring);
-              tbv = rb[((size_t)(R.ph & rmask) * SBP + pix) * 4 + 0] *
-                    ring_prod(rb, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask, pix);
+              tbv = rf[RS(R.ph, 0, rmask)] * ring_prod(rf, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask);
             }
           } else {  // long window: exception lists from global memory
             bool done = false;
             if (wlen > 2 * R.pnF + 8) {
               float dfac = 1.f;
               for (int e = 0; e < R.pnF; ++e)
-                dfac *= ring[(size_t)(A.exc[R.peoff + e] & rmask) * SBP + pix].y;
+                dfac *= rf[RS(A.exc[R.peoff + e], 1, rmask)];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
               }
             }
             if (!done) {
-              tbv = ring[(size_t)(R.ph & rmask) * SBP + pix].x;
+              tbv = rf[RS(R.ph, 0, rmask)];
               int e = 0;
               for (int r = R.ph; r < qpos; ++r) {
                 if (e < R.pnF && A.exc[R.peoff + e] == r) {
                   ++e;
                   continue;
                 }
-                tbv *= ring[(size_t)(r & rmask) * SBP + pix].y;
+                tbv *= rf[RS(r, 1, rmask)];
               }
             }
           }
@@ -481,20 +491,18 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
           if (f - R.pfb < FIN_S) {
             const FinS& F = fins[j * FIN_S + (f - R.pfb)];
             if (F.qslot < 0) continue;  // another chunk's position
-            const float* rf = reinterpret_cast<const float*>(ring) + pix * 4;
-            float tl = rf[F.qslot + 3];
+            float tl = rf[F.qslot + 3 * SBP];
             if (F.n >= 0) {
 #pragma unroll 4
-              for (int e = 0; e < F.n; ++e) tl *= rf[F.slot[e] + 2];
+              for (int e = 0; e < F.n; ++e) tl *= rf[F.slot[e] + 2 * SBP];
             } else {
               const FinRec fr = A.fin_rec[f];
               if (!(fr.flags & PM_OVF)) {
-                tl *= ring_prod(reinterpret_cast<const float*>(ring), fr.mg.x, fr.mg.y, fr.qq + 1, 2,
-                                rmask, pix);
+                tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
               } else {
                 const int64_t o2 = fr.eoff + fr.nF;
                 for (int e = 0; e < fr.nG; ++e)
-                  tl *= ring[(size_t)(A.exc[o2 + e] & rmask) * SBP + pix].z;
+                  tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
               }
             }
 #pragma unroll
@@ -503,14 +511,13 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
           }
           const FinRec fr = A.fin_rec[f];
           if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
-          float tl = ring[(size_t)(fr.qq & rmask) * SBP + pix].w;
+          float tl = rf[RS(fr.qq, 3, rmask)];
           if (!(fr.flags & PM_OVF)) {
-            tl *= ring_prod(reinterpret_cast<const float*>(ring), fr.mg.x, fr.mg.y, fr.qq + 1, 2,
-                            rmask, pix);
+            tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
           } else {
             const int64_t o2 = fr.eoff + fr.nF;
             for (int e = 0; e < fr.nG; ++e)
-              tl *= ring[(size_t)(A.exc[o2 + e] & rmask) * SBP + pix].z;
+              tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
           }
 #pragma unroll
           for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, fr.clo[c], alc[c]);
