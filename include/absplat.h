@@ -172,6 +172,19 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
 as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, int32_t cap,
                         int32_t* owner);
 
+/* ---- device scratch allocator ----
+ * All device memory the context holds (scene copy, per-Gaussian records, pair lists, sort
+ * buffers, exception metadata, the tile kernel's ring and partial sums) comes from
+ * alloc(user, bytes, stream) and goes back through free(user, ptr, bytes, stream), where
+ * stream is the context stream (cudaStream_t).  Buffers are grow-only and reused across
+ * renders; a buffer is returned to the allocator that produced it.  alloc returning NULL is
+ * AS_E_OOM.  alloc == NULL and free == NULL restore the default (cudaMalloc / cudaFree).
+ * Buffers allocated before the call stay with their allocator until they grow or the
+ * context is destroyed.  The Python binding binds this to torch's caching allocator. */
+typedef void* (*as_alloc_fn)(void* user, size_t bytes, void* stream);
+typedef void (*as_free_fn)(void* user, void* ptr, size_t bytes, void* stream);
+as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, void* user);
+
 /* Concrete render (Alg. 1 + BlendSort, reading G6/G8) at one point of the box: xi[n] in
  * [-1,1]^n are the box variables of the FULL box in order (perturbed axes tx,ty,tz,e0,e1,e2,
  * then group shifts), with the scene's nominal colours and opacities.  img: [H][W][3]

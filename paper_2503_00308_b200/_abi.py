@@ -53,6 +53,9 @@ class AsStats(C.Structure):
 
 
 _lib = None
+# as_alloc_fn / as_free_fn (include/absplat.h)
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 def declared_functions():
@@ -89,6 +92,7 @@ def lib():
         "as_tile_owners": (i32, [P, i32, i32, i32, P, P]),
         "as_lpt_assign": (i32, [i32, P, i32, i32, P]),
         "as_render_concrete": (i32, [P, P, P, i32]),
+        "as_set_allocator": (i32, [P, ALLOC_FN, FREE_FN, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -110,6 +110,39 @@ class Context:
             msg = self._L.as_last_error(self._ctx)
             raise AbsplatError(st, msg.decode() if msg else "")
 
+    # ------------------------------------------------------------------ memory
+    def as_set_allocator(self, alloc=None, free=None):
+        """Route the context's device memory through alloc(nbytes, stream) -> int pointer and
+        free(ptr, nbytes, stream); both None restores cudaMalloc/cudaFree."""
+        if (alloc is None) != (free is None):
+            raise ValueError("alloc and free must both be given or both be None")
+        if alloc is None:
+            cbs = (_abi.ALLOC_FN(), _abi.FREE_FN())
+        else:
+            def _a(user, nbytes, stream):
+                try:
+                    return int(alloc(int(nbytes), int(stream or 0)))
+                except Exception:  # reported as AS_E_OOM by the library
+                    return None
+
+            def _f(user, ptr, nbytes, stream):
+                try:
+                    free(int(ptr), int(nbytes), int(stream or 0))
+                except Exception:
+                    pass
+            cbs = (_abi.ALLOC_FN(_a), _abi.FREE_FN(_f))
+        self._check(self._L.as_set_allocator(self._ctx, cbs[0], cbs[1], None))
+        # buffers keep the free callback they were allocated with: keep every set alive
+        self._alloc_cbs = getattr(self, "_alloc_cbs", []) + [cbs]
+
+    def use_torch_allocator(self):
+        """Bind as_set_allocator to torch's CUDA caching allocator."""
+        import torch
+        dev = self.device
+        self.as_set_allocator(
+            lambda n, s: torch.cuda.caching_allocator_alloc(n, dev, s),
+            lambda p, n, s: torch.cuda.caching_allocator_delete(p))
+
     # ------------------------------------------------------------------ inputs
     def as_load_scene(self, mean, chol, opacity, color):
         keep = [_ptr(a, np.float32) for a in (mean, chol, opacity, color)]

@@ -22,6 +22,8 @@ namespace {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  as_free_fn free_fn = nullptr;  // allocator that produced p (nullptr = cudaMalloc)
+  void* user = nullptr;
 };
 
 struct Err {
@@ -61,6 +63,9 @@ struct as_ctx {
   int last_items = 0, last_grid = 0, last_R = 1, max_window = 0, last_wmax = 0;
   cudaEvent_t ev[8] = {};
   bool events = false;
+  as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
+  as_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
 };
 
 namespace {
@@ -95,26 +100,38 @@ void set_err(as_ctx* c, const char* fmt, ...) {
     }                                                                                       \
   } while (0)
 
-void ensure(as_ctx* ctx, DevBuf& b, size_t bytes) {
-  if (bytes == 0) bytes = 16;
-  if (b.cap >= bytes) return;
-  if (b.p) {
-    CK(cudaFree(b.p));
-    ctx->bytes -= b.cap;
-    b.p = nullptr;
-    b.cap = 0;
-  }
-  size_t want = bytes + bytes / 4;
-  CK(cudaMalloc(&b.p, want));
-  b.cap = want;
-  ctx->bytes += want;
-}
-void release(as_ctx* ctx, DevBuf& b) {
-  if (b.p) cudaFree(b.p);
+void free_buf(as_ctx* ctx, DevBuf& b) {
+  if (!b.p) return;
+  if (b.free_fn)
+    b.free_fn(b.user, b.p, b.cap, ctx->stream);
+  else
+    cudaFree(b.p);
   ctx->bytes -= b.cap;
   b.p = nullptr;
   b.cap = 0;
+  b.free_fn = nullptr;
+  b.user = nullptr;
 }
+void ensure(as_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return;
+  free_buf(ctx, b);
+  size_t want = bytes + bytes / 4;
+  if (ctx->alloc_fn) {
+    b.p = ctx->alloc_fn(ctx->alloc_user, want, ctx->stream);
+    if (!b.p) {
+      set_err(ctx, "allocator hook returned NULL for %zu bytes", want);
+      throw Err{AS_E_OOM};
+    }
+    b.free_fn = ctx->free_fn;
+    b.user = ctx->alloc_user;
+  } else {
+    CK(cudaMalloc(&b.p, want));
+  }
+  b.cap = want;
+  ctx->bytes += want;
+}
+void release(as_ctx* ctx, DevBuf& b) { free_buf(ctx, b); }
 
 template <typename T>
 T* P(DevBuf& b) {
@@ -813,6 +830,18 @@ as_status as_destroy(as_ctx* ctx) {
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   delete ctx;
+  return AS_OK;
+}
+
+as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, void* user) {
+  if (!ctx) return AS_E_ARG;
+  if ((alloc == nullptr) != (free_fn == nullptr)) {
+    set_err(ctx, "as_set_allocator: alloc and free must both be set or both be NULL");
+    return AS_E_ARG;
+  }
+  ctx->alloc_fn = alloc;
+  ctx->free_fn = free_fn;
+  ctx->alloc_user = alloc ? user : nullptr;
   return AS_OK;
 }
 

@@ -177,3 +177,27 @@ def test_edge_cases(ctx, oracle):
     olo, ohi, ost = oracle.render_bounds(w)
     assert st["fails"] == ost["fails"] > 0
     assert max(np.abs(lo - olo).max(), np.abs(hi - ohi).max()) <= TOL
+
+
+def test_torch_allocator_hook():
+    """as_set_allocator bound to torch's caching allocator: identical bounds, the context's
+    device memory is visible to torch while held and returned on close."""
+    import torch
+    from paper_2503_00308_b200 import Context
+    w = make_config("C4", N=3000, res=48)
+    with Context(0) as c0:
+        c0.load_workload(w)
+        lo0, hi0, _ = c0.as_render_bounds(16, 64)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(0)
+    c = Context(0)
+    c.use_torch_allocator()
+    c.load_workload(w)
+    lo, hi, st = c.as_render_bounds(16, 64)
+    held = torch.cuda.memory_allocated(0) - base
+    assert torch.equal(lo, lo0) and torch.equal(hi, hi0)
+    assert held >= st["device_bytes"] > 0
+    del lo, hi
+    c.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(0) - base <= 4096
