@@ -203,6 +203,20 @@ __device__ __forceinline__ int RS(int pos, int comp, int rmask) {
   return ((pos & rmask) * 4 + comp) * SBP;
 }
 
+// Skip ring: bit (p & 255) of s_skip[8] says position p's Gaussian misses the whole block
+// (a = 0 for every pixel, so its factors (1 - a) are exactly 1 and its own contributions
+// exactly 0).  skip_win returns the bits of positions [base, base + 128).
+__device__ __forceinline__ void skip_win(const unsigned* sk, int base, unsigned long long& m0,
+                                         unsigned long long& m1) {
+  unsigned w[4];
+  const int sh = base & 31, wi = base >> 5;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    w[k] = __funnelshift_r(sk[(wi + k) & 7], sk[(wi + k + 1) & 7], sh);
+  m0 = ((unsigned long long)w[1] << 32) | w[0];
+  m1 = ((unsigned long long)w[3] << 32) | w[2];
+}
+
 // product of ring component `comp` over the positions base + i for the set bits i of the
 // 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap.  rf = ring + pix.
 __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m0,
@@ -232,6 +246,7 @@ template <int NV>
 __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
+  __shared__ unsigned s_skip[8];
   const int ts = A.ts;
   const int nsb = ts / SB;          // sub-blocks per tile edge
   const int nsub = nsb * nsb;
@@ -280,6 +295,20 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
     for (int b0 = scan0; b0 < scan1; b0 += BS) {
       const int nb = min(BS, scan1 - b0);
       __syncthreads();
+      // ---- whole-block cull of the batch into the skip ring (same exact test as the
+      //      per-pixel one, on the block rectangle)
+      for (int j = threadIdx.x; j < nb; j += SBP) {
+        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
+        const double dx = fmax(0.0, fmax(__dsub_rn(H->mu[0], bx1), __dsub_rn(bx0, H->mu[2])));
+        const double dy = fmax(0.0, fmax(__dsub_rn(H->mu[1], by1), __dsub_rn(by0, H->mu[3])));
+        const bool skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
+        const int bit = (b0 + j) & 255;
+        if (skip)
+          atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
+        else
+          atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
+      }
+      __syncthreads();
       // ---- staging: fp64 record -> block-centred fp32 forms + cull tables + metadata
       //      four threads per Gaussian: parts 0-2 stage channel c of q, part 3 the rest
       for (int jj = threadIdx.x; jj < 4 * nb; jj += SBP) {
@@ -290,12 +319,8 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         SRec<NV>& S = srec[j];
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
         const double r2 = H->r2;
-        bool skip;
-        {  // whole-block cull (same exact test as the per-pixel one, on the block rectangle)
-          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
-          const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
-          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
-        }
+        const int sbit = (b0 + j) & 255;
+        const bool skip = (s_skip[sbit >> 5] >> (sbit & 31)) & 1u;
         if (part == 3) {
           int pmf = 0;
           if (iexc) {
@@ -314,15 +339,22 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
             // T_hi window operands as ring slot offsets (uniform for the whole block)
             const int qpos = b0 + j;
             int tmode = 0, nT = 0;
-            if ((pmf & PM_EF) && qpos >= pbeg && qpos < pend && !(pmf & PM_OVF)) {
+            if ((pmf & PM_EF) && !skip && qpos >= pbeg && qpos < pend && !(pmf & PM_OVF)) {
+              // (a skipped q contributes nothing: no T_hi needed)
               const int h = m.y, wlen = qpos - h;
               const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
               const unsigned long long v1 =
                   wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
-              const bool dense = !(wlen - m.w > m.w + 2);
-              unsigned long long m0 = dense ? (~mf.x & v0) : mf.x;
-              unsigned long long m1 = dense ? (~mf.y & v1) : mf.y;
-              const int cnt = __popcll(m0) + __popcll(m1);
+              // factors of skipped positions are exactly 1: leave them out of both lists
+              unsigned long long k0, k1;
+              skip_win(s_skip, h, k0, k1);
+              const unsigned long long e0 = mf.x & ~k0, e1 = mf.y & ~k1;
+              const unsigned long long f0 = ~mf.x & ~k0 & v0, f1 = ~mf.y & ~k1 & v1;
+              const int nef = __popcll(e0) + __popcll(e1), nkept = __popcll(f0) + __popcll(f1);
+              const bool dense = !(nkept > nef + 2);
+              unsigned long long m0 = dense ? f0 : e0;
+              unsigned long long m1 = dense ? f1 : e1;
+              const int cnt = dense ? nkept : nef;
               if (cnt <= TL_MAX) {
                 tmode = dense ? 1 : 2;
                 for (; m0; m0 &= m0 - 1) S.tl[nT++] = ((h + __ffsll((long long)m0) - 1) & rmask) * SBP * 4;
@@ -338,19 +370,32 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
             for (int e = 0; e < FIN_S && S.pfb + e < S.pfe; ++e) {
               const FinRec fr = A.fin_rec[S.pfb + e];
               FinS& F = fins[j * FIN_S + e];
-              F.qslot = (fr.qq >= pbeg && fr.qq < pend) ? (fr.qq & rmask) * SBP * 4 : -1;
+              const bool qmain = fr.qq >= pbeg && fr.qq < pend;
               F.clo[0] = fr.clo[0];
               F.clo[1] = fr.clo[1];
               F.clo[2] = fr.clo[2];
               int n = 0;
-              if (!(fr.flags & PM_OVF) && __popcll(fr.mg.x) + __popcll(fr.mg.y) <= EG_MAX) {
-                for (unsigned long long mm = fr.mg.x; mm; mm &= mm - 1)
-                  F.slot[n++] = ((fr.qq + __ffsll((long long)mm)) & rmask) * SBP * 4;
-                for (unsigned long long mm = fr.mg.y; mm; mm &= mm - 1)
-                  F.slot[n++] = ((fr.qq + 64 + __ffsll((long long)mm)) & rmask) * SBP * 4;
+              bool qskip = false;
+              if (qmain && !(fr.flags & PM_OVF)) {
+                // q' within 128 positions: its skip bit is still in the ring.  A skipped q'
+                // has a_lo = 0 (nothing to finalise); skipped E_G members have factor 1.
+                const int qb = fr.qq & 255;
+                qskip = (s_skip[qb >> 5] >> (qb & 31)) & 1u;
+                unsigned long long k0, k1;
+                skip_win(s_skip, fr.qq + 1, k0, k1);
+                const unsigned long long g0 = fr.mg.x & ~k0, g1 = fr.mg.y & ~k1;
+                if (__popcll(g0) + __popcll(g1) <= EG_MAX) {
+                  for (unsigned long long mm = g0; mm; mm &= mm - 1)
+                    F.slot[n++] = ((fr.qq + __ffsll((long long)mm)) & rmask) * SBP * 4;
+                  for (unsigned long long mm = g1; mm; mm &= mm - 1)
+                    F.slot[n++] = ((fr.qq + 64 + __ffsll((long long)mm)) & rmask) * SBP * 4;
+                } else {
+                  n = -1;
+                }
               } else {
                 n = -1;
               }
+              F.qslot = (qmain && !qskip) ? (fr.qq & rmask) * SBP * 4 : -1;
               F.n = n;
             }
           } else {
@@ -425,7 +470,7 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         // E_F factors when that is numerically safe (both products far from underflow),
         // else fall back to the window product (H3).
         float tbv = Tb;
-        if (main && (pmf & PM_EF)) {
+        if (main && (pmf & PM_EF) && !(flags & F_SKIP)) {
           const int wlen = qpos - R.ph;
           if (!(pmf & PM_OVF)) {
             bool done = false;
