@@ -82,27 +82,28 @@ struct alignas(16) FinS {
 template <int NV>
 __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, double ucx,
                                             double ucy, int part) {
+  // four threads per Gaussian; thread `part` stages coefficients k = part, part + 4, ... of
+  // every channel, so all of its record loads are independent and issue together
   constexpr int C = NV + 1;
+  constexpr int KP = (C + 3) / 4;
   const double uc[2] = {ucx, ucy};
-  if (part == 3) {  // x lower forms and concretised W
+  double wl[6], wh[6];  // concretised W, [a*3+c]
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    wl[e] = H->wc[e][0];
+    wh[e] = H->wc[e][1];
+  }
+  if (part == 3) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
-      S.wc[e][0] = H->wc[e][0];
-      S.wc[e][1] = H->wc[e][1];
+      S.wc[e][0] = (float)wl[e];
+      S.wc[e][1] = (float)wh[e];
     }
-#pragma unroll 1
-    for (int k = 0; k < C; ++k) {
-      const double d2l = H->d2[0][k];
-      S.xb[0][k] = (float)(uc[0] * d2l - H->du[0][1][k]);
-      S.xb[1][k] = (float)(uc[1] * d2l - H->du[1][1][k]);
-      S.d2lo[k] = (float)d2l;
-    }
-    return;
   }
-  const int c = part;  // channel c of q
-  const double w0l = H->wc[c][0], w0h = H->wc[c][1], w1l = H->wc[3 + c][0], w1h = H->wc[3 + c][1];
 #pragma unroll 1
-  for (int k = 0; k < C; ++k) {
+  for (int i = 0; i < KP; ++i) {
+    const int k = part + 4 * i;
+    if (k >= C) break;
     const double d2l = H->d2[0][k], d2h = H->d2[1][k];
     double blo[2], bhi[2];
 #pragma unroll
@@ -110,18 +111,31 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
       blo[a] = uc[a] * d2l - H->du[a][1][k];
       bhi[a] = uc[a] * d2h - H->du[a][0][k];
     }
-    S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
-    S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
-    S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
-    S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
-    S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
-    S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
-    const double a0 = H->w[c][0][k], b0 = H->w[c][1][k];
-    const double a1 = H->w[3 + c][0][k], b1 = H->w[3 + c][1][k];
-    S.wm0[c][k] = (float)(0.5 * (a0 + b0));
-    S.wr0[c][k] = (float)(0.5 * (b0 - a0));
-    S.wm1[c][k] = (float)(0.5 * (a1 + b1));
-    S.wr1[c][k] = (float)(0.5 * (b1 - a1));
+    float wa[6], wb[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      wa[e] = H->w[e][0][k];
+      wb[e] = H->w[e][1][k];
+    }
+    // x lower forms
+    S.xb[0][k] = (float)blo[0];
+    S.xb[1][k] = (float)blo[1];
+    S.d2lo[k] = (float)d2l;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+      S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
+      S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
+      S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
+      S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
+      S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
+      S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
+      const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
+      S.wm0[c][k] = (float)(0.5 * (a0 + b0));
+      S.wr0[c][k] = (float)(0.5 * (b0 - a0));
+      S.wm1[c][k] = (float)(0.5 * (a1 + b1));
+      S.wr1[c][k] = (float)(0.5 * (b1 - a1));
+    }
   }
 }
 
