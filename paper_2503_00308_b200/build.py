@@ -20,7 +20,7 @@ SOURCES = ["absplat.cu", "k_setup.cu", "k_bin.cu", "k_tile.cu", "k_concrete.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE,
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr"] + os.environ.get("ABSPLAT_NVCC_EXTRA", "").split()
 
 
 def _deps_mtime() -> float:

@@ -491,8 +491,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ensure(ctx, ctx->finkey2, sizeof(uint32_t) * M);
       ensure(ctx, ctx->finval, sizeof(int32_t) * M);
       ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
-      ensure(ctx, ctx->fin_b, sizeof(int32_t) * M);
-      ensure(ctx, ctx->fin_e, sizeof(int32_t) * M);
+      ensure(ctx, ctx->fin_b, sizeof(int32_t) * (M + 1));
       ensure(ctx, ctx->maskF, sizeof(ulonglong2) * M);
       ensure(ctx, ctx->maskG, sizeof(ulonglong2) * M);
       ensure(ctx, ctx->finrec, sizeof(FinRec) * M);
@@ -501,14 +500,12 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
                       P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
-      launch_fin_ranges(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->fin_b),
-                        P<int32_t>(ctx->fin_e), st);
+      launch_fin_start(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->fin_b), st);
       LAUNCHED(ctx, 1);
       launch_finrec(P<uint32_t>(ctx->finkey2), P<int32_t>(ctx->finval2), pa, P<int4>(ctx->pflag),
                     P<ulonglong2>(ctx->maskG), ctx->hot.p, P<FinRec>(ctx->finrec), st);
       LAUNCHED(ctx, 1);
-      ta.fin_b = P<int32_t>(ctx->fin_b);
-      ta.fin_e = P<int32_t>(ctx->fin_e);
+      ta.finstart = P<int32_t>(ctx->fin_b);
       ta.fin_rec = P<FinRec>(ctx->finrec);
       ta.mF = P<ulonglong2>(ctx->maskF);
       unsigned int hw = 0;

@@ -290,7 +290,7 @@ void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, 
                  ulonglong2* mG, cudaStream_t st);
 void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
                    const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
-void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe, cudaStream_t st);
+void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st);
 void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
                       int64_t* caps, cudaStream_t st);
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
@@ -322,8 +322,7 @@ struct TileArgs {
   const int32_t* nG;          // [M]
   const int64_t* eoff;        // [M+1]
   const int32_t* exc;         // E_F ascending then E_G ascending, tile-local
-  const int32_t* fin_b;       // [M] positions whose deferred T_lo is finalised here:
-  const int32_t* fin_e;       //     fin_rec[fin_b[p] .. fin_e[p])
+  const int32_t* finstart;    // [M+1] fin_rec[finstart[p] .. finstart[p+1]) finalise at p
   const FinRec* fin_rec;
   const ulonglong2* mF;       // [M] E_F bits over [h, h+128)
   float4* ring;               // [gridDim][R][ts*ts] (T_hi before, 1-a_lo, 1-a_hi, deferred)

@@ -440,20 +440,26 @@ void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, c
   NV_SWITCH(a.nv, (k_finrec<NVc><<<blocks, 256, 0, st>>>(key, val, a, pm, mG, hot, out)));
 }
 
-// CSR of the finalisation lists: sorted keys -> [fin_b, fin_e) per position
-__global__ void k_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe) {
+// CSR of the finalisation lists over ALL positions: fin_rec[fs[p] .. fs[p+1]) are the
+// records finalised at p (fs[p] = lower bound of p in the sorted keys; no-fin keys sort last
+// as 0xffffffff and count as M).  Thread i fills fs over the key gap (key[i-1], key[i]].
+__global__ void k_fin_start(const uint32_t* key, int64_t M, int32_t* fs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  const uint32_t k = key[i];
-  if (k == 0xffffffffu) return;
-  if (i == 0 || key[i - 1] != k) fb[k] = (int32_t)i;
-  if (i == M - 1 || key[i + 1] != k) fe[k] = (int32_t)(i + 1);
+  if (i > M) return;
+  auto K = [&](int64_t j) -> int64_t {
+    const uint32_t k = key[j];
+    return k == 0xffffffffu ? M : (int64_t)k;
+  };
+  const int64_t lo = i == 0 ? -1 : K(i - 1);
+  const int64_t hi = i == M ? M : K(i);
+  for (int64_t p = lo + 1; p <= hi; ++p) fs[p] = (int32_t)i;
 }
-void launch_fin_ranges(const uint32_t* key, int64_t M, int32_t* fb, int32_t* fe, cudaStream_t st) {
-  cudaMemsetAsync(fb, 0, sizeof(int32_t) * M, st);
-  cudaMemsetAsync(fe, 0, sizeof(int32_t) * M, st);
-  if (M <= 0) return;
-  k_fin_ranges<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(key, M, fb, fe);
+void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st) {
+  if (M <= 0) {
+    cudaMemsetAsync(fs, 0, sizeof(int32_t), st);
+    return;
+  }
+  k_fin_start<<<(unsigned)((M + 1 + 255) / 256), 256, 0, st>>>(key, M, fs);
 }
 
 // ------------------------------------------------------------------------- work items

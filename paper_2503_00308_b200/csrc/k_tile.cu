@@ -35,9 +35,9 @@ constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 
 constexpr int SB = 8;            // sub-block edge (pixels)
 constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
-constexpr int FIN_S = 3;         // finalisation records staged in shared memory per position
+constexpr int FB = 48;           // finalisation records staged in shared memory per batch
+constexpr int EG8 = 28;          // E_G operands precomputed per staged finalisation record
 constexpr int TL_MAX = 24;       // T_hi window operands precomputed per position
-constexpr int EG_MAX = 12;        // E_G operands precomputed per staged finalisation record
 
 template <int NV>
 struct alignas(16) SRec {
@@ -57,7 +57,7 @@ struct alignas(16) SRec {
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
   int pmf, ph, pg, pnF, pnG;  // position metadata (PM_*, h, g, |E_F|, |E_G|)
-  int pfb, pfe;             // finalisation list range
+  int pfb, pfe;             // finalisation records [pfb, pfe) relative to the batch's first
   long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
   unsigned long long mf0, mf1;  // E_F(p) bits over [h, h+128)
   // precomputed ring operands of the T_hi window (float offsets of ring slots, without pix)
@@ -66,12 +66,15 @@ struct alignas(16) SRec {
   int tl[TL_MAX];
   double r2;
 };
-// finalisation record staged in shared memory with its E_G ring slots precomputed
+// finalisation record of q' (finalised at g = max E_G(q')) staged in shared memory:
+// T_lo(q') a_lo(q') = w(q') (1 - a_hi,g) prod_{r in E_G(q') \ {g}} (1 - a_hi,r), with the
+// ring positions r = q' + off precomputed (culled positions, factor exactly 1, left out)
 struct alignas(16) FinS {
-  int qslot;                // ring float offset of q' (-1: q' not in this chunk's main range)
-  int n;                    // |E_G(q')| slots below, -1 = too many (slow path)
+  int qq;                   // q' (tile-local); -1: nothing to do in this block / chunk
+  short n;                  // operand count, -1 = slow path (bits or exception lists)
+  short pad;
   float clo[3];
-  int slot[EG_MAX];
+  unsigned char off[EG8];
 };
 
 // Staging of one Gaussian for a block centred at (ucx, ucy): fp64 arithmetic, one rounding.
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
   SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
   double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][SB]
   double* cy2 = cx2 + (size_t)BS * SB;                 // [BS][SB]
-  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SB);  // [BS][FIN_S]
+  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SB);  // [FB]
   const bool has_exc = A.pm != nullptr;
   const int pix = threadIdx.x;
   float* rf = has_exc ? reinterpret_cast<float*>(A.ring) + (size_t)blockIdx.x * A.R * SBP * 4 + pix
@@ -308,6 +311,9 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
 
     for (int b0 = scan0; b0 < scan1; b0 += BS) {
       const int nb = min(BS, scan1 - b0);
+      // finalisation records of the batch: fin_rec[F0, F1) (sorted by finalising position)
+      const int F0 = iexc ? A.finstart[tb + b0] : 0;
+      const int F1 = iexc ? A.finstart[tb + b0 + nb] : 0;
       __syncthreads();
       // ---- whole-block cull of the batch into the skip ring (same exact test as the
       //      per-pixel one, on the block rectangle)
@@ -345,8 +351,8 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
             S.pnF = m.w;
             S.pnG = A.nG[gp];
             S.peoff = A.eoff[gp];
-            S.pfb = A.fin_b[gp];
-            S.pfe = A.fin_e[gp];
+            S.pfb = A.finstart[gp] - F0;
+            S.pfe = A.finstart[gp + 1] - F0;
             const ulonglong2 mf = A.mF[gp];
             S.mf0 = mf.x;
             S.mf1 = mf.y;
@@ -380,38 +386,6 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
             }
             S.tmode = tmode;
             S.nT = nT;
-            // finalisation records with their E_G ring slots
-            for (int e = 0; e < FIN_S && S.pfb + e < S.pfe; ++e) {
-              const FinRec fr = A.fin_rec[S.pfb + e];
-              FinS& F = fins[j * FIN_S + e];
-              const bool qmain = fr.qq >= pbeg && fr.qq < pend;
-              F.clo[0] = fr.clo[0];
-              F.clo[1] = fr.clo[1];
-              F.clo[2] = fr.clo[2];
-              int n = 0;
-              bool qskip = false;
-              if (qmain && !(fr.flags & PM_OVF)) {
-                // q' within 128 positions: its skip bit is still in the ring.  A skipped q'
-                // has a_lo = 0 (nothing to finalise); skipped E_G members have factor 1.
-                const int qb = fr.qq & 255;
-                qskip = (s_skip[qb >> 5] >> (qb & 31)) & 1u;
-                unsigned long long k0, k1;
-                skip_win(s_skip, fr.qq + 1, k0, k1);
-                const unsigned long long g0 = fr.mg.x & ~k0, g1 = fr.mg.y & ~k1;
-                if (__popcll(g0) + __popcll(g1) <= EG_MAX) {
-                  for (unsigned long long mm = g0; mm; mm &= mm - 1)
-                    F.slot[n++] = ((fr.qq + __ffsll((long long)mm)) & rmask) * SBP * 4;
-                  for (unsigned long long mm = g1; mm; mm &= mm - 1)
-                    F.slot[n++] = ((fr.qq + 64 + __ffsll((long long)mm)) & rmask) * SBP * 4;
-                } else {
-                  n = -1;
-                }
-              } else {
-                n = -1;
-              }
-              F.qslot = (qmain && !qskip) ? (fr.qq & rmask) * SBP * 4 : -1;
-              F.n = n;
-            }
           } else {
             S.pfb = S.pfe = 0;
             S.tmode = 0;
@@ -440,6 +414,46 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
           }
         }
         if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+      }
+      // finalisation records of the batch with their ring operands (skip-filtered)
+      for (int t = threadIdx.x; t < min(F1 - F0, FB); t += SBP) {
+        const FinRec fr = A.fin_rec[F0 + t];
+        FinS& F = fins[t];
+        const int qq = fr.qq;
+        F.clo[0] = fr.clo[0];
+        F.clo[1] = fr.clo[1];
+        F.clo[2] = fr.clo[2];
+        F.qq = -1;
+        F.n = 0;
+        if (qq < pbeg || qq >= pend) continue;  // another chunk's position
+        if (fr.flags & PM_OVF) {
+          F.qq = qq;
+          F.n = -1;
+          continue;
+        }
+        // q' within 128 positions of g: its skip bit is still in the ring.  A culled q' has
+        // a_lo = 0 (nothing to finalise); culled positions in E_G(q') have factor 1.
+        const int qb = qq & 255;
+        if ((s_skip[qb >> 5] >> (qb & 31)) & 1u) continue;
+        F.qq = qq;
+        unsigned long long k0, k1;
+        skip_win(s_skip, qq + 1, k0, k1);
+        // g = max E_G(q') is the highest bit; its factor comes from the walk's register
+        unsigned long long g0 = fr.mg.x & ~k0, g1 = fr.mg.y;
+        if (g1) {
+          g1 &= ~(1ull << (63 - __clzll((long long)g1)));
+          g1 &= ~k1;
+        } else {
+          g0 &= ~(1ull << (63 - __clzll((long long)fr.mg.x)));
+        }
+        if (__popcll(g0) + __popcll(g1) > EG8) {
+          F.n = -1;
+          continue;
+        }
+        int n = 0;
+        for (; g0; g0 &= g0 - 1) F.off[n++] = (unsigned char)__ffsll((long long)g0);
+        for (; g1; g1 &= g1 - 1) F.off[n++] = (unsigned char)(64 + __ffsll((long long)g1));
+        F.n = (short)n;
       }
       __syncthreads();
       // ---- walk the batch in (kappa, index) order
@@ -547,39 +561,40 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
         // finalise deferred lower contributions of earlier partners whose last later
         // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
         for (int f = R.pfb; f < R.pfe; ++f) {
-          if (f - R.pfb < FIN_S) {
-            const FinS& F = fins[j * FIN_S + (f - R.pfb)];
-            if (F.qslot < 0) continue;  // another chunk's position
-            float tl = rf[F.qslot + 3 * SBP];
+          float tl;
+          const float* clo;
+          if (f < FB) {
+            const FinS& F = fins[f];
+            if (F.qq < 0) continue;  // another chunk's position, or culled in this block
+            clo = F.clo;
+            tl = rf[RS(F.qq, 3, rmask)];
             if (F.n >= 0) {
+              tl *= 1.f - ahi;  // g itself
 #pragma unroll 4
-              for (int e = 0; e < F.n; ++e) tl *= rf[F.slot[e] + 2 * SBP];
+              for (int e = 0; e < F.n; ++e) tl *= rf[RS(F.qq + F.off[e], 2, rmask)];
             } else {
-              const FinRec fr = A.fin_rec[f];
+              const FinRec& fr = A.fin_rec[F0 + f];
               if (!(fr.flags & PM_OVF)) {
                 tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
               } else {
                 const int64_t o2 = fr.eoff + fr.nF;
-                for (int e = 0; e < fr.nG; ++e)
-                  tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
+                for (int e = 0; e < fr.nG; ++e) tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
               }
             }
-#pragma unroll
-            for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, F.clo[c], alc[c]);
-            continue;
-          }
-          const FinRec fr = A.fin_rec[f];
-          if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
-          float tl = rf[RS(fr.qq, 3, rmask)];
-          if (!(fr.flags & PM_OVF)) {
-            tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
           } else {
-            const int64_t o2 = fr.eoff + fr.nF;
-            for (int e = 0; e < fr.nG; ++e)
-              tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
+            const FinRec& fr = A.fin_rec[F0 + f];
+            if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
+            clo = fr.clo;
+            tl = rf[RS(fr.qq, 3, rmask)];
+            if (!(fr.flags & PM_OVF)) {
+              tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
+            } else {
+              const int64_t o2 = fr.eoff + fr.nF;
+              for (int e = 0; e < fr.nG; ++e) tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
+            }
           }
 #pragma unroll
-          for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, fr.clo[c], alc[c]);
+          for (int c = 0; c < 3; ++c) alc[c] = fmaf(tl, clo[c], alc[c]);
         }
       }
     }
@@ -685,7 +700,7 @@ int tile_subblocks(int ts) { return (ts / SB) * (ts / SB); }
 template <int NV>
 static size_t smem_for(int ts, int bs) {
   (void)ts;
-  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double) + FIN_S * sizeof(FinS));
+  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double)) + FB * sizeof(FinS);
 }
 
 size_t tile_smem_bytes(int nv, int ts, int bs) {
