@@ -37,7 +37,7 @@ constexpr int SB = 8;            // sub-block edge (pixels)
 constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
 constexpr int FB = 48;           // finalisation records staged in shared memory per batch
 constexpr int EG8 = 28;          // E_G operands precomputed per staged finalisation record
-constexpr int TL_MAX = 24;       // T_hi window operands precomputed per position
+constexpr int TL8 = 32;          // T_hi window operands precomputed per position
 
 template <int NV>
 struct alignas(16) SRec {
@@ -60,10 +60,10 @@ struct alignas(16) SRec {
   int pfb, pfe;             // finalisation records [pfb, pfe) relative to the batch's first
   long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
   unsigned long long mf0, mf1;  // E_F(p) bits over [h, h+128)
-  // precomputed ring operands of the T_hi window (float offsets of ring slots, without pix)
-  int tmode;                // 0 none, 1 dense (th, tl = kept), 2 sparse (tl = E_F), 3 slow
-  int nT, th, pad2;
-  int tl[TL_MAX];
+  // precomputed ring operands of the T_hi window: positions h + tlo[t]
+  int tmode;                // 0 none, 1 dense (tlo = kept), 2 sparse (tlo = E_F), 3 slow
+  int nT;
+  unsigned char tlo[TL8];
   double r2;
 };
 // finalisation record of q' (finalised at g = max E_G(q')) staged in shared memory:
@@ -260,7 +260,7 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
 }
 
 template <int NV>
-__global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
+__global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
   __shared__ unsigned s_skip[8];
@@ -375,11 +375,10 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
               unsigned long long m0 = dense ? f0 : e0;
               unsigned long long m1 = dense ? f1 : e1;
               const int cnt = dense ? nkept : nef;
-              if (cnt <= TL_MAX) {
+              if (cnt <= TL8) {
                 tmode = dense ? 1 : 2;
-                for (; m0; m0 &= m0 - 1) S.tl[nT++] = ((h + __ffsll((long long)m0) - 1) & rmask) * SBP * 4;
-                for (; m1; m1 &= m1 - 1) S.tl[nT++] = ((h + 64 + __ffsll((long long)m1) - 1) & rmask) * SBP * 4;
-                S.th = (h & rmask) * SBP * 4;
+                for (; m0; m0 &= m0 - 1) S.tlo[nT++] = (unsigned char)(__ffsll((long long)m0) - 1);
+                for (; m1; m1 &= m1 - 1) S.tlo[nT++] = (unsigned char)(64 + __ffsll((long long)m1) - 1);
               } else {
                 tmode = 3;
               }
@@ -503,15 +502,15 @@ __global__ void __launch_bounds__(SBP, 8) k_tile(TileArgs A) {
           if (!(pmf & PM_OVF)) {
             bool done = false;
             if (R.tmode == 1) {  // dense: T_hi before h times the kept factors
-              float pr = rf[R.th];
+              float pr = rf[RS(R.ph, 0, rmask)];
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) pr *= rf[R.tl[t] + SBP];
+              for (int t = 0; t < R.nT; ++t) pr *= rf[RS(R.ph + R.tlo[t], 1, rmask)];
               tbv = pr;
               done = true;
             } else if (R.tmode == 2) {  // sparse: divide the running product (guarded, H3)
               float dfac = 1.f;
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) dfac *= rf[R.tl[t] + SBP];
+              for (int t = 0; t < R.nT; ++t) dfac *= rf[RS(R.ph + R.tlo[t], 1, rmask)];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
