@@ -232,10 +232,24 @@ __global__ void k_tile_h(PairArgs A) {
   A.tilemax[t] = 0ull;
 }
 
+// warp-aggregated atomics over the lanes currently converged (each converged group elects
+// its lowest lane): one atomic per warp instead of one per thread
+__device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned v) {
+  const unsigned mask = __activemask();
+  v = __reduce_add_sync(mask, v);
+  if ((int)(threadIdx.x & 31) == __ffs(mask) - 1 && v) atomicAdd(dst, (unsigned long long)v);
+}
+__device__ __forceinline__ void warp_max_u32(unsigned* dst, unsigned v) {
+  const unsigned mask = __activemask();
+  v = __reduce_max_sync(mask, v);
+  if ((int)(threadIdx.x & 31) == __ffs(mask) - 1 && v) atomicMax(dst, v);
+}
+
 template <int NV>
 __global__ void k_pairs_prep(PairArgs A) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= A.M) return;
+  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = p0 < A.M;
+  const int64_t p = live ? p0 : A.M - 1;  // dead lanes mirror the last position (no writes)
   const uint32_t t = A.keys[p];
   const PairRec<NV> Pi = load_pair<NV>(A.pair, A.vals[p]);
   const double* h = A.tileh + (size_t)t * (NVMAX + 1);
@@ -247,17 +261,30 @@ __global__ void k_pairs_prep(PairArgs A) {
     s2 += fabs(Pi.du[k] - m);
   }
   const double ws = 0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2);
-  A.wsP[p] = ws;
-  A.kapP[p] = Pi.kappa;
-  // position-ordered copy of the depth form: the window scans then read neighbours
-  // contiguously instead of gathering PairRec by Gaussian id
-  double* D = A.posD + (size_t)p * 2 * (NV + 1);
+  if (live) {
+    A.wsP[p] = ws;
+    A.kapP[p] = Pi.kappa;
+    // position-ordered copy of the depth form: the window scans then read neighbours
+    // contiguously instead of gathering PairRec by Gaussian id
+    double* D = A.posD + (size_t)p * 2 * (NV + 1);
 #pragma unroll
-  for (int k = 0; k <= NV; ++k) {
-    D[k] = Pi.dl[k];
-    D[NV + 1 + k] = Pi.du[k];
+    for (int k = 0; k <= NV; ++k) {
+      D[k] = Pi.dl[k];
+      D[NV + 1 + k] = Pi.du[k];
+    }
   }
-  atomicMax(&A.tilemax[t], (unsigned long long)__double_as_longlong(ws));
+  // tile max of ws (ws >= 0, so its bit pattern orders like the value): positions are
+  // sorted by tile, so equal keys form runs; reduce each run inside the warp first
+  unsigned long long v = (unsigned long long)__double_as_longlong(ws);
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long vo = __shfl_down_sync(0xffffffffu, v, o);
+    const uint32_t to = __shfl_down_sync(0xffffffffu, t, o);
+    if (lane + o < 32 && to == t) v = max(v, vo);
+  }
+  const uint32_t tp = __shfl_up_sync(0xffffffffu, t, 1);
+  if (live && (lane == 0 || tp != t)) atomicMax(&A.tilemax[t], v);
 }
 
 // true when every later/earlier candidate is certainly ordered (the scan can stop)
@@ -316,8 +343,8 @@ __global__ void k_pairs(PairArgs A) {
     A.nF[p] = nF;
     A.nG[p] = nG;
     A.ntot[p] = nF + nG;
-    if (nG) atomicAdd(&A.counters[0], (unsigned long long)nG);
-    if (viol) atomicAdd(&A.counters[1], (unsigned long long)viol);
+    warp_add(&A.counters[0], (unsigned)nG);
+    warp_add(&A.counters[1], (unsigned)viol);
   } else {
     A.hpos[p] = hmin;
   }
@@ -395,8 +422,7 @@ __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, i
   }
   mF[p] = make_ulonglong2(f0, f1);
   mG[p] = make_ulonglong2(g0, g1);
-  const unsigned w = (unsigned)max(loc - h, g - loc);
-  if (w) atomicMax(wmax, w);
+  warp_max_u32(wmax, (unsigned)max(loc - h, g - loc));
   // deferred lower contribution of p is finalised at its last later partner b + g
   finkey[p] = nG ? (uint32_t)(b + g) : 0xffffffffu;
   finval[p] = (int32_t)p;
