@@ -120,11 +120,11 @@ void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------------- k_setup
-// Layout: a half-warp (16 lanes) per Gaussian, lane k holding coefficient k of the lower
-// and the upper affine function of every form (k < NV: slope of xi_k, k == NV: constant,
-// k > NV: zero padding).  Concretisation is a 16-lane shuffle reduction.  This keeps the
+// Layout: 8 lanes (n <= 7) or 16 lanes per Gaussian, lane k holding coefficient k of the
+// lower and the upper affine function of every form (k < NV: slope of xi_k, k == NV:
+// constant, k > NV: zero padding).  Concretisation is a shuffle reduction over the group.  This keeps the
 // ~40 live forms of Alg. 1 + MatrixInv in registers (2 doubles per form per lane) instead
-// of spilling ~10 KB per thread.  All control flow is uniform across the two Gaussians of a
+// of spilling ~10 KB per thread.  All control flow is uniform across the Gaussians of a
 // warp (selects, no data-dependent branches) so the shuffles stay converged.
 namespace {
 constexpr unsigned FULL = 0xffffffffu;
@@ -133,16 +133,22 @@ struct HL {  // this lane's coefficient of a form: lower, upper
   double l, u;
 };
 
+// lanes per Gaussian: 8 when the n + 1 coefficients fit (n <= 7), else 16
+template <int NV>
+constexpr int lanes_for() {
+  return (NV + 1 <= 8) ? 8 : 16;
+}
+
+template <int W>
 __device__ __forceinline__ double hsum(double v) {
-  v += __shfl_xor_sync(FULL, v, 8, 16);
-  v += __shfl_xor_sync(FULL, v, 4, 16);
-  v += __shfl_xor_sync(FULL, v, 2, 16);
-  v += __shfl_xor_sync(FULL, v, 1, 16);
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, W);
   return v;
 }
 
 template <int NV>
 struct Lane {
+  static constexpr int W = lanes_for<NV>();
   int k;
   __device__ __forceinline__ bool slope() const { return k < NV; }
   __device__ __forceinline__ bool cst() const { return k == NV; }
@@ -150,8 +156,8 @@ struct Lane {
   __device__ __forceinline__ void conc(const HL& f, double& mn, double& mx) const {
     const double a = slope() ? -fabs(f.l) : (cst() ? f.l : 0.0);
     const double b = slope() ? fabs(f.u) : (cst() ? f.u : 0.0);
-    mn = hsum(a);
-    mx = hsum(b);
+    mn = hsum<W>(a);
+    mx = hsum<W>(b);
   }
   __device__ __forceinline__ HL constant(double v) const {
     const double c = cst() ? v : 0.0;
@@ -196,6 +202,8 @@ struct Lane {
 template <int NV>
 __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
   __shared__ PoseDev sp;
+  __shared__ unsigned long long s_wsmax;
+  if (threadIdx.x == 0) s_wsmax = 0ull;
   {
     const double* src = reinterpret_cast<const double*>(A.pose);
     double* dst = reinterpret_cast<double*>(&sp);
@@ -203,11 +211,12 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
       dst[k] = src[k];
   }
   __syncthreads();
-  const Lane<NV> L{(int)(threadIdx.x & 15)};
+  constexpr int W = lanes_for<NV>();
+  const Lane<NV> L{(int)(threadIdx.x & (W - 1))};
   const int k = L.k;
-  const int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
   const bool live = gi < A.N;
-  const int64_t i = live ? gi : (A.N - 1);  // dead half-warps mirror the last Gaussian
+  const int64_t i = live ? gi : (A.N - 1);  // dead lane groups mirror the last Gaussian
   const int kc = (k < NV) ? k : NVMAX;      // coefficient slot in the pose tables
   const bool real = k <= NV;
   auto pose_R = [&](int e) -> HL {
@@ -376,11 +385,11 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
   L.conc(d, dl, dh);
   L.conc(up0, u0l, u0h);
   L.conc(up1, u1l, u1h);
-  const double dcl = __shfl_sync(FULL, d.l, NV, 16), dcu = __shfl_sync(FULL, d.u, NV, 16);
+  const double dcl = __shfl_sync(FULL, d.l, NV, W), dcu = __shfl_sync(FULL, d.u, NV, W);
   double s1 = L.slope() ? fabs(d.l - sp.gslope[k]) : 0.0;
   double s2 = L.slope() ? fabs(d.u - sp.gslope[k]) : 0.0;
-  s1 = hsum(s1);
-  s2 = hsum(s2);
+  s1 = hsum<W>(s1);
+  s2 = hsum<W>(s2);
   if (live && real) {
     H->d2[0][k] = D2.l;
     H->d2[1][k] = D2.u;
@@ -443,14 +452,15 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
     PR->ws = ws;
     A.kkey[i] = (fl & F_DROP) ? ~0ull : key_of_double(kappa);
     A.kval[i] = (int32_t)i;
-    if (!(fl & F_DROP)) atomicMax(A.wsmax, (unsigned long long)__double_as_longlong(ws));
+    if (!(fl & F_DROP)) atomicMax(&s_wsmax, (unsigned long long)__double_as_longlong(ws));
   }
-  // block-aggregated counters (one vote per Gaussian: lane 0 of each half-warp)
+  // block-aggregated counters (one vote per Gaussian: lane 0 of each lane group)
   const bool head = live && k == 0;
   const int nf = __syncthreads_count(head && (fl & F_FAIL) && !(fl & F_DROP));
   const int ns = __syncthreads_count(head && (fl & F_STRADDLE));
   const int nd = __syncthreads_count(head && (fl & F_DROP));
   if (threadIdx.x == 0) {
+    if (s_wsmax) atomicMax(A.wsmax, s_wsmax);  // block max (ws >= 0: bits order like values)
     if (nf) atomicAdd(&A.counters[0], (unsigned long long)nf);
     if (ns) atomicAdd(&A.counters[1], (unsigned long long)ns);
     if (nd) atomicAdd(&A.counters[2], (unsigned long long)nd);
@@ -458,8 +468,8 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
 }
 
 void launch_setup(int nv, const SetupArgs& a, cudaStream_t st) {
-  const int threads = 128;  // 8 Gaussians per block
-  const int64_t total = a.N * 16;
+  const int threads = 128;  // 16 (n <= 7) or 8 Gaussians per block
+  const int64_t total = a.N * (nv + 1 <= 8 ? 8 : 16);
   const unsigned blocks = (unsigned)((total + threads - 1) / threads);
   if (a.N <= 0) return;
   switch (nv) {
