@@ -315,22 +315,10 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
       const int F0 = iexc ? A.finstart[tb + b0] : 0;
       const int F1 = iexc ? A.finstart[tb + b0 + nb] : 0;
       __syncthreads();
-      // ---- whole-block cull of the batch into the skip ring (same exact test as the
-      //      per-pixel one, on the block rectangle)
-      for (int j = threadIdx.x; j < nb; j += SBP) {
-        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
-        const double dx = fmax(0.0, fmax(__dsub_rn(H->mu[0], bx1), __dsub_rn(bx0, H->mu[2])));
-        const double dy = fmax(0.0, fmax(__dsub_rn(H->mu[1], by1), __dsub_rn(by0, H->mu[3])));
-        const bool skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
-        const int bit = (b0 + j) & 255;
-        if (skip)
-          atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
-        else
-          atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
-      }
-      __syncthreads();
-      // ---- staging: fp64 record -> block-centred fp32 forms + cull tables + metadata
-      //      four threads per Gaussian: parts 0-2 stage channel c of q, part 3 the rest
+      // ---- phase A: fp64 record -> block-centred fp32 forms, whole-block cull (same exact
+      //      test as the per-pixel one, on the block rectangle) into the skip ring, cull
+      //      tables and position metadata.  Four threads per Gaussian (stage_forms splits
+      //      the coefficients); each evaluates the cull, part 3 records it.
       for (int jj = threadIdx.x; jj < 4 * nb; jj += SBP) {
         const int j = jj >> 2, part = jj & 3;
         const int64_t gp = tb + b0 + j;
@@ -339,9 +327,18 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
         SRec<NV>& S = srec[j];
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
         const double r2 = H->r2;
-        const int sbit = (b0 + j) & 255;
-        const bool skip = (s_skip[sbit >> 5] >> (sbit & 31)) & 1u;
+        bool skip;
+        {
+          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
+          const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
+          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
+        }
         if (part == 3) {
+          const int bit = (b0 + j) & 255;
+          if (skip)
+            atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
+          else
+            atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
           int pmf = 0;
           if (iexc) {
             const int4 m = A.pm[gp];
@@ -356,40 +353,11 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
             const ulonglong2 mf = A.mF[gp];
             S.mf0 = mf.x;
             S.mf1 = mf.y;
-            // T_hi window operands as ring slot offsets (uniform for the whole block)
-            const int qpos = b0 + j;
-            int tmode = 0, nT = 0;
-            if ((pmf & PM_EF) && !skip && qpos >= pbeg && qpos < pend && !(pmf & PM_OVF)) {
-              // (a skipped q contributes nothing: no T_hi needed)
-              const int h = m.y, wlen = qpos - h;
-              const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
-              const unsigned long long v1 =
-                  wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
-              // factors of skipped positions are exactly 1: leave them out of both lists
-              unsigned long long k0, k1;
-              skip_win(s_skip, h, k0, k1);
-              const unsigned long long e0 = mf.x & ~k0, e1 = mf.y & ~k1;
-              const unsigned long long f0 = ~mf.x & ~k0 & v0, f1 = ~mf.y & ~k1 & v1;
-              const int nef = __popcll(e0) + __popcll(e1), nkept = __popcll(f0) + __popcll(f1);
-              const bool dense = !(nkept > nef + 2);
-              unsigned long long m0 = dense ? f0 : e0;
-              unsigned long long m1 = dense ? f1 : e1;
-              const int cnt = dense ? nkept : nef;
-              if (cnt <= TL8) {
-                tmode = dense ? 1 : 2;
-                for (; m0; m0 &= m0 - 1) S.tlo[nT++] = (unsigned char)(__ffsll((long long)m0) - 1);
-                for (; m1; m1 &= m1 - 1) S.tlo[nT++] = (unsigned char)(64 + __ffsll((long long)m1) - 1);
-              } else {
-                tmode = 3;
-              }
-            }
-            S.tmode = tmode;
-            S.nT = nT;
           } else {
             S.pfb = S.pfe = 0;
-            S.tmode = 0;
-            S.nT = 0;
           }
+          S.tmode = 0;
+          S.nT = 0;
           S.pmf = pmf;
           S.flags = H->flags | (skip ? F_SKIP : 0);
           S.r2 = r2;
@@ -413,6 +381,41 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
           }
         }
         if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+      }
+      __syncthreads();
+      // ---- phase B (needs the batch's skip bits): T_hi window operands per position and
+      //      the batch's finalisation records, both skip-filtered
+      if (iexc) {
+        for (int j = threadIdx.x; j < nb; j += SBP) {
+          SRec<NV>& S = srec[j];
+          const int pmf = S.pmf, qpos = b0 + j;
+          // (a skipped q contributes nothing: no T_hi needed)
+          if (!(pmf & PM_EF) || (S.flags & F_SKIP) || qpos < pbeg || qpos >= pend || (pmf & PM_OVF))
+            continue;
+          const int h = S.ph, wlen = qpos - h;
+          const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+          const unsigned long long v1 =
+              wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+          // factors of skipped positions are exactly 1: leave them out of both lists
+          unsigned long long k0, k1;
+          skip_win(s_skip, h, k0, k1);
+          const unsigned long long e0 = S.mf0 & ~k0, e1 = S.mf1 & ~k1;
+          const unsigned long long f0 = ~S.mf0 & ~k0 & v0, f1 = ~S.mf1 & ~k1 & v1;
+          const int nef = __popcll(e0) + __popcll(e1), nkept = __popcll(f0) + __popcll(f1);
+          const bool dense = !(nkept > nef + 2);
+          unsigned long long m0 = dense ? f0 : e0;
+          unsigned long long m1 = dense ? f1 : e1;
+          const int cnt = dense ? nkept : nef;
+          int nT = 0;
+          if (cnt <= TL8) {
+            S.tmode = dense ? 1 : 2;
+            for (; m0; m0 &= m0 - 1) S.tlo[nT++] = (unsigned char)(__ffsll((long long)m0) - 1);
+            for (; m1; m1 &= m1 - 1) S.tlo[nT++] = (unsigned char)(64 + __ffsll((long long)m1) - 1);
+          } else {
+            S.tmode = 3;
+          }
+          S.nT = nT;
+        }
       }
       // finalisation records of the batch with their ring operands (skip-filtered)
       for (int t = threadIdx.x; t < min(F1 - F0, FB); t += SBP) {
