@@ -50,9 +50,11 @@ struct alignas(16) SRec {
   // functions of the pixel offset du, and the W-side terms in mid / radius form:
   //   q_lo,k = plo + du0 q0lo + du1 q1lo + x0 wm0 - |x0| wr0 + x1 wm1 - |x1| wr1
   //   q_hi,k = phi + du0 q0hi + du1 q1hi + x0 wm0 + |x0| wr0 + x1 wm1 + |x1| wr1
-  float plo[3][CP], phi[3][CP], q0lo[3][CP], q0hi[3][CP], q1lo[3][CP], q1hi[3][CP];
+  // stored as mid / radius:  q_lo,k = m - r,  q_hi,k = m + r  with
+  //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
+  float pm[3][CP], pr[3][CP], q0m[3][CP], q0r[3][CP], q1m[3][CP], q1r[3][CP];
   float wm0[3][CP], wr0[3][CP], wm1[3][CP], wr1[3][CP];
-  float wc[6][2];           // concretised W (lo, hi), [a*3+c]
+  float wcm[6], wcd[6];     // concretised W, [a*3+c]: (lo + hi) / 2, (lo - hi) / 2
   float o[2];
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
@@ -99,8 +101,8 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
   if (part == 3) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
-      S.wc[e][0] = (float)wl[e];
-      S.wc[e][1] = (float)wh[e];
+      S.wcm[e] = (float)(0.5 * (wl[e] + wh[e]));
+      S.wcd[e] = (float)(0.5 * (wl[e] - wh[e]));
     }
   }
 #pragma unroll 1
@@ -127,12 +129,16 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
-      S.plo[c][k] = (float)(w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]));
-      S.phi[c][k] = (float)(w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]));
-      S.q0lo[c][k] = (float)(w0l * (w0l >= 0 ? d2l : d2h));
-      S.q1lo[c][k] = (float)(w1l * (w1l >= 0 ? d2l : d2h));
-      S.q0hi[c][k] = (float)(w0h * (w0h >= 0 ? d2h : d2l));
-      S.q1hi[c][k] = (float)(w1h * (w1h >= 0 ? d2h : d2l));
+      const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
+      const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
+      const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q1lo = w1l * (w1l >= 0 ? d2l : d2h);
+      const double q0hi = w0h * (w0h >= 0 ? d2h : d2l), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
+      S.pm[c][k] = (float)(0.5 * (plo + phi));
+      S.pr[c][k] = (float)(0.5 * (phi - plo));
+      S.q0m[c][k] = (float)(0.5 * (q0lo + q0hi));
+      S.q0r[c][k] = (float)(0.5 * (q0hi - q0lo));
+      S.q1m[c][k] = (float)(0.5 * (q1lo + q1hi));
+      S.q1r[c][k] = (float)(0.5 * (q1hi - q1lo));
       const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
       S.wm0[c][k] = (float)(0.5 * (a0 + b0));
       S.wr0[c][k] = (float)(0.5 * (b0 - a0));
@@ -165,23 +171,23 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
     float ql[C], qh[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      float lo = fmaf(du0, R.q0lo[c][k], R.plo[c][k]);
-      lo = fmaf(du1, R.q1lo[c][k], lo);
-      lo = fmaf(x0, R.wm0[c][k], lo);
-      lo = fmaf(-ax0, R.wr0[c][k], lo);
-      lo = fmaf(x1, R.wm1[c][k], lo);
-      lo = fmaf(-ax1, R.wr1[c][k], lo);
-      float hi = fmaf(du0, R.q0hi[c][k], R.phi[c][k]);
-      hi = fmaf(du1, R.q1hi[c][k], hi);
-      hi = fmaf(x0, R.wm0[c][k], hi);
-      hi = fmaf(ax0, R.wr0[c][k], hi);
-      hi = fmaf(x1, R.wm1[c][k], hi);
-      hi = fmaf(ax1, R.wr1[c][k], hi);
-      ql[k] = lo;
-      qh[k] = hi;
+      float m = fmaf(du0, R.q0m[c][k], R.pm[c][k]);
+      m = fmaf(du1, R.q1m[c][k], m);
+      m = fmaf(x0, R.wm0[c][k], m);
+      m = fmaf(x1, R.wm1[c][k], m);
+      float r = fmaf(du0, R.q0r[c][k], R.pr[c][k]);
+      r = fmaf(du1, R.q1r[c][k], r);
+      r = fmaf(ax0, R.wr0[c][k], r);
+      r = fmaf(ax1, R.wr1[c][k], r);
+      if (k == NV) {  // constant: q_lo -= x0 W_lo,0c + x1 W_lo,1c, q_hi -= x0 W_hi,0c + x1 W_hi,1c
+        m = fmaf(-x0, R.wcm[c], m);
+        m = fmaf(-x1, R.wcm[3 + c], m);
+        r = fmaf(x0, R.wcd[c], r);
+        r = fmaf(x1, R.wcd[3 + c], r);
+      }
+      ql[k] = m - r;
+      qh[k] = m + r;
     }
-    ql[NV] -= fmaf(x0, R.wc[c][0], x1 * R.wc[3 + c][0]);
-    qh[NV] -= fmaf(x0, R.wc[c][1], x1 * R.wc[3 + c][1]);
     float qmin = ql[NV], qmax = qh[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
