@@ -802,12 +802,25 @@ void set_threads(int nthreads) {
 }
 
 int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, int mode,
-                      double* lo, double* hi, or_stats* st) {
+                      double* lo, double* hi, or_stats* st, int sb0 = 0, int sb1 = -1) {
   const or_camera& C = P.cam;
   int64_t pairs = 0, active = 0, unc = 0, viol = 0, fails = 0, strad = 0, drop = 0;
   int kmax = 0;
   int nvars = 0;
-  for (int s = 0; s < P.n_sub; ++s) {
+  if (sb1 < 0) sb1 = P.n_sub;
+  if (sb0 >= sb1) {  // empty union: the identities of step 22's min / max
+    const int ntx = (C.W + ts - 1) / ts;
+    for (int tile : tiles) {
+      const int tx = tile % ntx, ty = tile / ntx;
+      for (int py = ty * ts; py < std::min((ty + 1) * ts, (int)C.H); ++py)
+        for (int px = tx * ts; px < std::min((tx + 1) * ts, (int)C.W); ++px)
+          for (int c = 0; c < 3; ++c) {
+            lo[3 * ((size_t)py * C.W + px) + c] = 1.0;
+            hi[3 * ((size_t)py * C.W + px) + c] = 0.0;
+          }
+    }
+  }
+  for (int s = sb0; s < sb1; ++s) {
     SubData S;
     build_subdata(P, s, S);
     nvars = S.B.n;
@@ -844,7 +857,7 @@ int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, i
           finalise((double)P.N, pl, ph);
           size_t o = 3 * ((size_t)py * C.W + px);
           for (int c = 0; c < 3; ++c) {
-            if (s == 0) {
+            if (s == sb0) {
               lo[o + c] = pl[c];
               hi[o + c] = ph[c];
             } else {  // step 22: union over sub-boxes
@@ -864,7 +877,7 @@ int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, i
     st->straddles = strad;
     st->dropped = drop;
     st->kmax = kmax;
-    st->n_sub = P.n_sub;
+    st->n_sub = sb1 > sb0 ? sb1 - sb0 : 0;
     st->n_vars = nvars;
     st->pad = 0;
   }
@@ -1067,6 +1080,20 @@ int or_render_bounds(int64_t N, const float* mean, const float* chol, const floa
   std::vector<int> tiles(ntx * nty);
   for (int k = 0; k < ntx * nty; ++k) tiles[k] = k;
   return render_tiles_impl(P, tile, tiles, mode, lo, hi, stats);
+}
+
+int or_render_subboxes(int64_t N, const float* mean, const float* chol, const float* opacity,
+                       const float* color, const or_camera* cam, const or_pose_box* box,
+                       const or_scene_box* sbox, int32_t tile, int32_t sub_begin, int32_t sub_end,
+                       int32_t nthreads, double* lo, double* hi, or_stats* stats) {
+  Problem P;
+  if (setup_problem(P, N, mean, chol, opacity, color, cam, box, sbox) != 0) return -1;
+  if (tile < 1 || !lo || !hi || sub_begin < 0 || sub_end > P.n_sub || sub_begin > sub_end) return -1;
+  set_threads(nthreads);
+  int ntx = (cam->W + tile - 1) / tile, nty = (cam->H + tile - 1) / tile;
+  std::vector<int> tiles(ntx * nty);
+  for (int k = 0; k < ntx * nty; ++k) tiles[k] = k;
+  return render_tiles_impl(P, tile, tiles, 0, lo, hi, stats, sub_begin, sub_end);
 }
 
 int or_render_tiles(int64_t N, const float* mean, const float* chol, const float* opacity,

@@ -73,6 +73,14 @@ int or_render_bounds(int64_t N, const float* mean, const float* chol, const floa
                      const or_scene_box* sbox, int32_t tile, int32_t mode, int32_t nthreads,
                      double* lo, double* hi, or_stats* stats);
 
+/* Union (step 22) over the sub-boxes [sub_begin, sub_end) only, windowed blend, all
+ * tiles.  An empty range gives the identities of the union's min / max (lo = 1, hi = 0), so
+ * ranges combine by elementwise min / max into the full render (sub-box sharding, §8(e)). */
+int or_render_subboxes(int64_t N, const float* mean, const float* chol, const float* opacity,
+                       const float* color, const or_camera* cam, const or_pose_box* box,
+                       const or_scene_box* sbox, int32_t tile, int32_t sub_begin, int32_t sub_end,
+                       int32_t nthreads, double* lo, double* hi, or_stats* stats);
+
 /* Same semantics at selected pixels only, computed without tiles: every non-dropped
  * Gaussian culled per pixel, direct blend.  `tile` is accepted for symmetry and unused
  * (results do not depend on the tile size, reading O1).  lo/hi: [npix][3]. */

@@ -74,6 +74,8 @@ def lib():
                                       P, C.c_int32, P, P]
         L.or_render_tiles.argtypes = [C.c_int64, P, P, P, P, P, P, P, C.c_int32, C.c_int64, P,
                                       C.c_int32, P, P, P]
+        L.or_render_subboxes.argtypes = [C.c_int64, P, P, P, P, P, P, P, C.c_int32, C.c_int32,
+                                         C.c_int32, C.c_int32, P, P, P]
         L.or_render_concrete.argtypes = [C.c_int64, P, P, P, P, P, C.c_int32, P, P, P,
                                          C.c_int32, C.c_int64, P, P, C.c_int32, P]
         L.or_blend_sort.argtypes = [C.c_int64, P, P, P, P]
@@ -181,6 +183,24 @@ def render_bounds(w, tile=None, mode=0, nthreads=0, camera=None, pose_box=None, 
                                 nthreads, _ptr(lo), _ptr(hi), C.addressof(st))
     if rc != 0:
         raise ValueError(f"or_render_bounds failed ({rc})")
+    return lo, hi, st.asdict()
+
+
+def render_subboxes(w, sub_begin, sub_end, tile=None, nthreads=0):
+    """Union over the sub-boxes [sub_begin, sub_end) only (empty: lo = 1, hi = 0)."""
+    tile = w.tile if tile is None else tile
+    cam = camera_struct(w.camera)
+    box = pose_box_struct(w.pose_box)
+    sb = _SceneBoxHolder(w.scene_box, w.N)
+    mean, chol, op, col = _scene(w)
+    lo = np.zeros((cam.H, cam.W, 3))
+    hi = np.zeros((cam.H, cam.W, 3))
+    st = Stats()
+    rc = lib().or_render_subboxes(w.N, _ptr(mean), _ptr(chol), _ptr(op), _ptr(col),
+                                  C.addressof(cam), C.addressof(box), sb.ref(), tile, sub_begin,
+                                  sub_end, nthreads, _ptr(lo), _ptr(hi), C.addressof(st))
+    if rc != 0:
+        raise ValueError(f"or_render_subboxes failed ({rc})")
     return lo, hi, st.asdict()
 
 

@@ -295,3 +295,37 @@ def test_spiky_gaussians_fail_soundly(oracle):
         e, t, sh = H.pose_of(w, p)
         img = oracle.render_concrete(w, euler=e, t=t)
         assert np.all(lo <= img + 1e-9) and np.all(img <= hi + 1e-9)
+
+
+def test_subbox_ranges_compose_to_the_union(oracle):
+    """Step 22: the abstract image is the elementwise min / max union over sub-boxes,
+    so renders of disjoint sub-box ranges combine exactly into the full render (sub-box
+    sharding, §8(e)); an empty range is the union's identity (lo = 1, hi = 0); and a
+    one-sub-box range equals the render of a box built directly as that sub-box (G18: uniform
+    split, yaw part m of P covers [lo + 2 eps m / P, lo + 2 eps (m + 1) / P])."""
+    w = make_config("C3", N=500, res=32)
+    P = w.n_sub
+    assert P == 8
+    flo, fhi, fst = oracle.render_bounds(w)
+    lo_a, hi_a, st_a = oracle.render_subboxes(w, 0, 3)
+    lo_b, hi_b, st_b = oracle.render_subboxes(w, 3, P)
+    assert st_a["n_sub"] == 3 and st_b["n_sub"] == P - 3
+    assert np.array_equal(np.minimum(lo_a, lo_b), flo)
+    assert np.array_equal(np.maximum(hi_a, hi_b), fhi)
+    assert st_a["pairs"] + st_b["pairs"] == fst["pairs"]
+    lo_e, hi_e, st_e = oracle.render_subboxes(w, 5, 5)
+    assert np.all(lo_e == 1.0) and np.all(hi_e == 0.0) and st_e["pairs"] == 0
+    m = 5
+    one = copy.deepcopy(w)
+    pb = copy.deepcopy(w.pose_box)
+    eps = pb["eps_R"][2]
+    lo_yaw = pb["R_off"][2] - eps
+    pb["R_off"][2] = lo_yaw + 2 * eps * (2 * m + 1) / (2 * P)
+    pb["eps_R"][2] = eps / P
+    pb["parts"] = [1, 1, 1, 1, 1, 1]
+    one.pose_box = pb
+    s_lo, s_hi, _ = oracle.render_subboxes(w, m, m + 1)
+    d_lo, d_hi, _ = oracle.render_bounds(one)
+    assert max(np.abs(s_lo - d_lo).max(), np.abs(s_hi - d_hi).max()) <= 1e-12
+    with pytest.raises(ValueError):
+        oracle.render_subboxes(w, 0, P + 1)
