@@ -138,6 +138,19 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sbox);
 as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, float* hi,
                            int32_t flags, as_stats* stats);
 
+/* ---- sub-box ranges (SURVEY.md §8(e) second sharding axis) ----
+ * The abstract image is the elementwise union (lo = min, hi = max) over the P sub-boxes of
+ * the partitioned input box (step 22).  as_render_subboxes renders the union
+ * over sub-boxes [sub_begin, sub_end) only (0 <= sub_begin <= sub_end <= P; sub-box s is the
+ * multi-index over the partitioned axes, tx fastest, as in as_pose_box.parts); an empty
+ * range writes the union's identities lo = 1, hi = 0.  Disjoint ranges rendered on different
+ * ranks therefore combine with an all-reduce MIN / MAX into the full image, bit for bit.
+ * Arguments otherwise as as_render_bounds.  as_subbox_count returns P for the current box. */
+as_status as_render_subboxes(as_ctx* ctx, int32_t tile, int32_t batch, int32_t sub_begin,
+                             int32_t sub_end, float* lo, float* hi, int32_t flags,
+                             as_stats* stats);
+as_status as_subbox_count(as_ctx* ctx, int32_t* n_sub);
+
 /* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----
  * Every rank holds the full scene and runs the per-Gaussian setup; image tiles are
  * assigned to ranks by a deterministic longest-processing-time rule over per-tile Gaussian

@@ -93,6 +93,8 @@ def lib():
         "as_lpt_assign": (i32, [i32, P, i32, i32, P]),
         "as_render_concrete": (i32, [P, P, P, i32]),
         "as_set_allocator": (i32, [P, ALLOC_FN, FREE_FN, P]),
+        "as_render_subboxes": (i32, [P, i32, i32, i32, i32, P, P, i32, P]),
+        "as_subbox_count": (i32, [P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

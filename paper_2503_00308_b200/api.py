@@ -225,6 +225,23 @@ class Context:
                                              flags, C.byref(st) if st is not None else None))
         return lo, hi, (st.asdict() if st is not None else None)
 
+    def as_render_subboxes(self, sub_begin: int, sub_end: int, tile: int = 16, batch: int = 64,
+                           lo=None, hi=None, stats: bool = True, sync: bool = True):
+        """Union over sub-boxes [sub_begin, sub_end) only (empty range: lo = 1, hi = 0)."""
+        H, W = int(self.camera["H"]), int(self.camera["W"])
+        lo, hi, pl, ph, dev = self._image_out(lo, hi, (H, W, 3))
+        flags = (AS_PTR_DEVICE if dev else 0) | (AS_ASYNC if (dev and not sync) else 0)
+        st = _abi.AsStats() if stats else None
+        self._check(self._L.as_render_subboxes(self._ctx, tile, batch, int(sub_begin),
+                                               int(sub_end), C.c_void_p(pl), C.c_void_p(ph),
+                                               flags, C.byref(st) if st is not None else None))
+        return lo, hi, (st.asdict() if st is not None else None)
+
+    def as_subbox_count(self) -> int:
+        n = C.c_int32(0)
+        self._check(self._L.as_subbox_count(self._ctx, C.byref(n)))
+        return int(n.value)
+
     def n_tiles(self, tile: int) -> int:
         H, W = int(self.camera["H"]), int(self.camera["W"])
         return ((W + tile - 1) // tile) * ((H + tile - 1) // tile)

@@ -1041,8 +1041,46 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
   }
 }
 
+namespace {
+__global__ void k_fill2(float* a, float va, float* b, float vb, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    a[i] = va;
+    b[i] = vb;
+  }
+}
+as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int32_t s1,
+                       float* lo, float* hi, int32_t flags, as_stats* stats);
+}  // namespace
+
 as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, float* hi,
                            int32_t flags, as_stats* stats) {
+  return render_range(ctx, tile, batch, 0, -1, lo, hi, flags, stats);
+}
+
+as_status as_render_subboxes(as_ctx* ctx, int32_t tile, int32_t batch, int32_t sub_begin,
+                             int32_t sub_end, float* lo, float* hi, int32_t flags,
+                             as_stats* stats) {
+  if (sub_begin < 0 || sub_end < sub_begin) {
+    if (ctx) set_err(ctx, "as_render_subboxes: bad range [%d, %d)", sub_begin, sub_end);
+    return AS_E_ARG;
+  }
+  return render_range(ctx, tile, batch, sub_begin, sub_end, lo, hi, flags, stats);
+}
+
+as_status as_subbox_count(as_ctx* ctx, int32_t* n_sub) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  if (!n_sub) return AS_E_ARG;
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  *n_sub = bi.n_sub;
+  return AS_OK;
+}
+
+namespace {
+as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int32_t s1,
+                       float* lo, float* hi, int32_t flags, as_stats* stats) {
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   if (!lo || !hi) {
@@ -1051,6 +1089,11 @@ as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, 
   }
   BoxInfo bi;
   if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if (s1 < 0) s1 = bi.n_sub;
+  if (s1 > bi.n_sub) {
+    set_err(ctx, "sub-box range [%d, %d) beyond the %d sub-boxes", s0, s1, bi.n_sub);
+    return AS_E_ARG;
+  }
   if ((st = check_tile_args(ctx, tile, batch, bi.n_vars)) != AS_OK) return st;
   if ((flags & AS_ASYNC) && !(flags & AS_PTR_DEVICE)) {
     set_err(ctx, "AS_ASYNC requires device outputs");
@@ -1076,10 +1119,14 @@ as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, 
     LAUNCHED(ctx, 1);
     PhaseTimes pt;
     int64_t pairs = 0;
-    for (int sb = 0; sb < bi.n_sub; ++sb) {
+    if (s0 >= s1) {  // empty union: the identities of min / max (step 22)
+      k_fill2<<<(unsigned)((img + 255) / 256), 256, 0, s>>>(dlo, 1.f, dhi, 0.f, (int64_t)img);
+      LAUNCHED(ctx, 1);
+    }
+    for (int sb = s0; sb < s1; ++sb) {
       int64_t M = 0;
       render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                    nullptr, dlo, dhi, sb == 0, M, stats ? &pt : nullptr);
+                    nullptr, dlo, dhi, sb == s0, M, stats ? &pt : nullptr);
       pairs += M;
     }
     if (!(flags & AS_PTR_DEVICE)) {
@@ -1091,7 +1138,9 @@ as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, 
       CK(cudaEventSynchronize(ctx->ev[6]));
       float tot = 0;
       CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
-      fill_stats(ctx, bi, G, G.ntiles, pairs, pt, tot, stats);
+      BoxInfo br = bi;
+      br.n_sub = s1 > s0 ? s1 - s0 : 0;
+      fill_stats(ctx, br, G, G.ntiles, pairs, pt, tot, stats);
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;
@@ -1099,6 +1148,7 @@ as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, 
     return e.st;
   }
 }
+}  // namespace
 
 as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, int32_t cap,
                         int32_t* owner) {

@@ -1,7 +1,14 @@
-"""Tile sharding over GPUs (north_star (3)): one process per GPU, the scene
-replicated on every rank, image tiles assigned by the library's deterministic LPT owner
-map, each rank rendering only its tiles into a compact tile-major buffer, then ONE
-all-gather of the bound tiles (NCCL over NVLink / NVSwitch) and an untile on the root.
+"""Sharding over GPUs (north_star (3)), one process per GPU, the scene
+replicated on every rank.
+
+* Tiles (ShardedRenderer): image tiles assigned by the library's deterministic LPT owner map,
+  each rank rendering only its tiles into a compact tile-major buffer, then ONE all-gather of
+  the bound tiles (NCCL over NVLink / NVSwitch) and an untile on the root.
+* Sub-boxes (SubboxShardedRenderer, the second axis): each rank renders the union over a
+  contiguous range of the partition's sub-boxes for the whole image, then ONE all-reduce MIN
+  on lo and MAX on hi (step 22's union) gives every rank the full image.  No
+  work is replicated (each sub-box has its own per-Gaussian setup), so this is the better
+  axis when the partition has at least as many sub-boxes as ranks (C3: 8).
 
 Gaussians are never split across ranks: blending order is not commutative.
 """
@@ -59,6 +66,40 @@ class ShardedRenderer:
         lo, hi = self.ctx.as_untile(self.tile, self.world, self.cap, gm[:, 1:], gm[:, 0],
                                     g_lo, g_hi)
         return lo, hi, st
+
+
+def subbox_range(n_sub: int, rank: int, world: int):
+    """Contiguous balanced range [b, e) of the n_sub sub-boxes for `rank` (may be empty)."""
+    q, r = divmod(n_sub, world)
+    b = rank * q + min(rank, r)
+    return b, b + q + (1 if rank < r else 0)
+
+
+class SubboxShardedRenderer:
+    """Union over the partition's sub-boxes, split across `world` ranks (all-reduce min/max)."""
+
+    def __init__(self, ctx: Context, rank: int, world: int, group=None, tile: int = 16,
+                 batch: int = 64, device=None):
+        import torch
+        self.ctx, self.rank, self.world, self.group = ctx, rank, world, group
+        self.tile, self.batch = tile, batch
+        self.n_sub = ctx.as_subbox_count()
+        self.range = subbox_range(self.n_sub, rank, world)
+        H, W = int(ctx.camera["H"]), int(ctx.camera["W"])
+        dev = device if device is not None else f"cuda:{ctx.device}"
+        self.lo = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+        self.hi = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+
+    def step(self, stats: bool = False):
+        """One sharded render; every rank returns the full (lo, hi) and its own stats."""
+        import torch.distributed as dist
+        b, e = self.range
+        lo, hi, st = self.ctx.as_render_subboxes(b, e, self.tile, self.batch, self.lo, self.hi,
+                                                 stats=stats)
+        if self.world > 1:
+            dist.all_reduce(self.lo, op=dist.ReduceOp.MIN, group=self.group)
+            dist.all_reduce(self.hi, op=dist.ReduceOp.MAX, group=self.group)
+        return self.lo, self.hi, st
 
 
 def assemble_host(W: int, H: int, tile: int, world: int, cap: int, owned, n_owned, lo_tm, hi_tm):

@@ -2,7 +2,8 @@
 the product's ShardedRenderer driver, the library's LPT owner map and its host untile are
 exercised end to end; per-rank tile rendering is supplied by the fp64 oracle (test
 infrastructure) since there is no GPU here.  The assembled image must equal the oracle's
-single-process image exactly."""
+single-process image exactly.  The second axis (sub-box sharding: ranges of the partition's
+sub-boxes per rank, all-reduce MIN / MAX) is exercised the same way."""
 import os
 import socket
 
@@ -96,3 +97,64 @@ def test_sharded_gloo(world, name, kw, tile):
     assert all(p.exitcode == 0 for p in procs)
     ok_lo, ok_hi = q.get(timeout=5)
     assert ok_lo and ok_hi
+
+
+class OracleSubboxCtx:
+    """Stands in for Context.as_subbox_count / as_render_subboxes on a CPU-only box."""
+
+    def __init__(self, w, oracle):
+        self.w, self.oracle = w, oracle
+        self.camera = w.camera
+        self.device = None
+
+    def as_subbox_count(self):
+        return self.w.n_sub
+
+    def as_render_subboxes(self, b, e, tile, batch, lo, hi, stats=False):
+        olo, ohi, st = self.oracle.render_subboxes(self.w, b, e, tile=tile)
+        lo.copy_(torch.from_numpy(olo.astype(np.float32)))
+        hi.copy_(torch.from_numpy(ohi.astype(np.float32)))
+        return lo, hi, st
+
+
+def _subbox_worker(rank, world, port, kw, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import pyoracle
+        from paper_2503_00308_b200.dist import SubboxShardedRenderer, subbox_range
+        from workloads import make_config
+        w = make_config("C3", **kw)
+        sr = SubboxShardedRenderer(OracleSubboxCtx(w, pyoracle), rank, world, tile=16,
+                                   device="cpu")
+        lo, hi, st = sr.step()
+        olo, ohi, _ = pyoracle.render_bounds(w, tile=16)
+        b, e = subbox_range(w.n_sub, rank, world)
+        q.put((rank, e - b, bool(np.array_equal(lo.numpy(), olo.astype(np.float32))),
+               bool(np.array_equal(hi.numpy(), ohi.astype(np.float32)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [3, 10])
+def test_subbox_sharded_gloo(world):
+    """C3's 8 yaw parts over 3 ranks (3/3/2) and over 10 ranks (two ranks get an empty range
+    and contribute the union's identities); every rank ends with the oracle's full image."""
+    from paper_2503_00308_b200.dist import subbox_range
+    assert [subbox_range(8, r, 3) for r in range(3)] == [(0, 3), (3, 6), (6, 8)]
+    assert sum(e - b for b, e in (subbox_range(8, r, 10) for r in range(10))) == 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    kw = dict(N=400, res=24)
+    procs = [ctx.Process(target=_subbox_worker, args=(r, world, port, kw, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert sum(r[1] for r in res) == 8
+    assert all(r[2] and r[3] for r in res)

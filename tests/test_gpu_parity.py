@@ -201,3 +201,32 @@ def test_torch_allocator_hook():
     c.close()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated(0) - base <= 4096
+
+
+def test_subbox_ranges(ctx, oracle):
+    """as_render_subboxes: each range matches the oracle's range union within 1e-4, disjoint
+    ranges compose by min / max into the full render bit for bit (the all-reduce of sub-box
+    sharding), an empty range is the identity (lo = 1, hi = 0)."""
+    import torch
+    w = make_config("C3", **SMALL["C3"])
+    ctx.load_workload(w)
+    P = ctx.as_subbox_count()
+    assert P == w.n_sub == 8
+    flo, fhi, _ = ctx.as_render_bounds(16, 16)
+    parts = [(0, 3), (3, 5), (5, 8)]
+    los, his = [], []
+    for b, e in parts:
+        lo, hi, st = ctx.as_render_subboxes(b, e, 16, 16)
+        assert st["n_sub"] == e - b
+        olo, ohi, _ = oracle.render_subboxes(w, b, e)
+        err = max(np.abs(lo.cpu().numpy() - olo).max(), np.abs(hi.cpu().numpy() - ohi).max())
+        assert err <= TOL, (b, e, err)
+        los.append(lo)
+        his.append(hi)
+    assert torch.equal(torch.minimum(torch.minimum(los[0], los[1]), los[2]), flo)
+    assert torch.equal(torch.maximum(torch.maximum(his[0], his[1]), his[2]), fhi)
+    lo, hi, _ = ctx.as_render_subboxes(4, 4, 16, 16)
+    assert bool((lo == 1).all()) and bool((hi == 0).all())
+    from paper_2503_00308_b200 import AbsplatError
+    with pytest.raises(AbsplatError):
+        ctx.as_render_subboxes(0, P + 1, 16, 16)
