@@ -3,8 +3,9 @@
 // transmittance scan + bounded blend (Alg. 3, interval reading O7), with the
 // finalise/union epilogue.
 //
-// A work item is one 8x8 pixel block of a tile (64 threads, one pixel each) over one chunk of
-// the tile's Gaussian list (sorted by (kappa, index)).  The list is streamed through shared
+// A work item is one 16x8 pixel block of a tile (128 threads, one pixel each; 8x8 / 64
+// threads for 8-pixel tiles) over one chunk of the tile's Gaussian list (sorted by
+// (kappa, index)).  The list is streamed through shared
 // memory in batches of BS: the staging step turns each Gaussian's fp64 record into
 // block-centred fp32 forms (B = u_c D2 - DU at the block centre u_c, so the per-pixel
 // x = B + (u - u_c) D2 avoids the d^2 u - d up cancellation; H2) and fp64 per-row /
@@ -13,8 +14,9 @@
 // pixel in order: FP32 on CUDA cores.
 //
 // Work is a list of (tile, chunk) items, longest first, pulled by persistent CTAs from an
-// atomic counter (load balance).  A chunk ends only where no uncertain depth
-// pair is split, so chunks of one tile compose front to back in k_merge.
+// atomic counter (load balance).  A chunk is scanned with lookback / lookahead
+// margins covering its positions' exception windows, so chunks of one tile compose front to
+// back in k_merge with multiplications only.
 //
 // Uncertain depth pairs (rotation / scene boxes; step 13) are handled in the walk itself
 // with a per-CTA ring in global memory (L2-resident): position q writes (T_hi before q,
@@ -33,8 +35,20 @@ namespace {
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr float LOG2E_HALF = 0.72134752044448170368f;  // log2(e) / 2
 
-constexpr int SB = 8;            // sub-block edge (pixels)
-constexpr int SBP = SB * SB;     // threads per CTA = pixels per work item
+// A work item is one BX x 8 pixel block (BX = 16, or 8 for 8-pixel tiles), one thread per
+// pixel; every warp covers an 8 x 4 quadrant so the warp-level cull stays compact.
+constexpr int SBY = 8;           // block height
+constexpr int NPART = 4;         // staging threads per Gaussian
+__host__ __device__ __forceinline__ int block_w(int ts) { return ts >= 16 ? 16 : 8; }
+__host__ __device__ __forceinline__ int pix_x(int t, int bx) {
+  return bx == 16 ? ((t >> 5) & 1) * 8 + (t & 7) : (t & 7);
+}
+__host__ __device__ __forceinline__ int pix_y(int t, int bx) {
+  return bx == 16 ? (t >> 6) * 4 + ((t >> 3) & 3) : (t >> 3);
+}
+__host__ __device__ __forceinline__ int pix_of(int x, int y, int bx) {
+  return bx == 16 ? ((y >> 2) * 2 + (x >> 3)) * 32 + (y & 3) * 8 + (x & 7) : y * 8 + x;
+}
 constexpr int FB = 48;           // finalisation records staged in shared memory per batch
 constexpr int EG8 = 28;          // E_G operands precomputed per staged finalisation record
 constexpr int TL8 = 32;          // T_hi window operands precomputed per position
@@ -87,10 +101,10 @@ struct alignas(16) FinS {
 template <int NV>
 __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, double ucx,
                                             double ucy, int part) {
-  // four threads per Gaussian; thread `part` stages coefficients k = part, part + 4, ... of
-  // every channel, so all of its record loads are independent and issue together
+  // NPART threads per Gaussian; thread `part` stages coefficients k = part, part + NPART,
+  // ... of every channel, so all of its record loads are independent and issue together
   constexpr int C = NV + 1;
-  constexpr int KP = (C + 3) / 4;
+  constexpr int KP = (C + NPART - 1) / NPART;
   const double uc[2] = {ucx, ucy};
   double wl[6], wh[6];  // concretised W, [a*3+c]
 #pragma unroll
@@ -98,7 +112,7 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
     wl[e] = H->wc[e][0];
     wh[e] = H->wc[e][1];
   }
-  if (part == 3) {
+  if (part == NPART - 1) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
       S.wcm[e] = (float)(0.5 * (wl[e] + wh[e]));
@@ -107,7 +121,7 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
   }
 #pragma unroll 1
   for (int i = 0; i < KP; ++i) {
-    const int k = part + 4 * i;
+    const int k = part + NPART * i;
     if (k >= C) break;
     const double d2l = H->d2[0][k], d2h = H->d2[1][k];
     double blo[2], bhi[2];
@@ -222,6 +236,7 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 // Ring layout (per CTA): [slot][component][pixel] floats, so a warp's load of one component
 // is one contiguous 128-byte line.  Components: 0 T_hi before q, 1 (1 - a_lo,q),
 // 2 (1 - a_hi,q), 3 deferred T_lo a_lo,q.  RS = float offset of (slot, comp) without pixel.
+template <int SBP>
 __device__ __forceinline__ int RS(int pos, int comp, int rmask) {
   return ((pos & rmask) * 4 + comp) * SBP;
 }
@@ -242,6 +257,7 @@ __device__ __forceinline__ void skip_win(const unsigned* sk, int base, unsigned 
 
 // product of ring component `comp` over the positions base + i for the set bits i of the
 // 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap.  rf = ring + pix.
+template <int SBP>
 __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m0,
                                            unsigned long long m1, int base, int comp, int rmask) {
   float prod = 1.f;
@@ -257,7 +273,7 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
         idx = base + 64 + __ffsll((long long)m1) - 1;
         m1 &= m1 - 1;
       }
-      v[t] = idx >= 0 ? rf[RS(idx, comp, rmask)] : 1.f;
+      v[t] = idx >= 0 ? rf[RS<SBP>(idx, comp, rmask)] : 1.f;
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) prod *= v[t];
@@ -265,26 +281,28 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
   return prod;
 }
 
-template <int NV>
-__global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
+template <int NV, int BX>
+__global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A) {
+  constexpr int SBX = BX;         // block width
+  constexpr int SBP = SBX * SBY;  // threads per CTA = pixels per work item
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
   __shared__ unsigned s_skip[8];
   const int ts = A.ts;
-  const int nsb = ts / SB;          // sub-blocks per tile edge
-  const int nsub = nsb * nsb;
+  const int nsbx = ts / SBX;        // blocks per tile row
+  const int nsub = nsbx * (ts / SBY);
   const int BS = A.bs;
   SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
-  double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][SB]
-  double* cy2 = cx2 + (size_t)BS * SB;                 // [BS][SB]
-  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SB);  // [FB]
+  double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][SBX]
+  double* cy2 = cx2 + (size_t)BS * SBX;                // [BS][SBY]
+  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * SBY);  // [FB]
   const bool has_exc = A.pm != nullptr;
   const int pix = threadIdx.x;
   float* rf = has_exc ? reinterpret_cast<float*>(A.ring) + (size_t)blockIdx.x * A.R * SBP * 4 + pix
                       : nullptr;
-  const int lx = pix % SB, ly = pix / SB;
-  const float du0 = (float)lx + 0.5f - 0.5f * SB;  // offset from the block centre
-  const float du1 = (float)ly + 0.5f - 0.5f * SB;
+  const int lx = pix_x(pix, SBX), ly = pix_y(pix, SBX);
+  const float du0 = (float)lx + 0.5f - 0.5f * SBX;  // offset from the block centre
+  const float du1 = (float)ly + 0.5f - 0.5f * SBY;
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
 
@@ -303,13 +321,13 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
     const int scan0 = it2.x, scan1 = it2.y, anext = it2.z;  // scan [A, L), record at A_next
     const int rmask = (1 << ((iflags >> 8) & 0xff)) - 1;     // per-item ring length - 1
     const int tx = tile % A.ntx, ty = tile / A.ntx;
-    const int ox = tx * ts + (sub % nsb) * SB, oy = ty * ts + (sub / nsb) * SB;  // block origin
+    const int ox = tx * ts + (sub % nsbx) * SBX, oy = ty * ts + (sub / nsbx) * SBY;  // origin
     const int64_t tb = A.tbegin[tile];
-    const double ucx = ox + 0.5 * SB, ucy = oy + 0.5 * SB;  // block centre
+    const double ucx = ox + 0.5 * SBX, ucy = oy + 0.5 * SBY;  // block centre
     const bool iexc = has_exc && (iflags & IT_EXC);
     const bool in_img = (ox + lx < A.W) && (oy + ly < A.H);
-    const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + SB), (double)A.W) - 0.5;
-    const double by0 = oy + 0.5, by1 = fmin((double)(oy + SB), (double)A.H) - 0.5;
+    const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + SBX), (double)A.W) - 0.5;
+    const double by0 = oy + 0.5, by1 = fmin((double)(oy + SBY), (double)A.H) - 0.5;
     const bool block_live = ox < A.W && oy < A.H;
     float Tb = 1.f, Tl = 1.f, ahc[3] = {0.f, 0.f, 0.f}, alc[3] = {0.f, 0.f, 0.f};
     float recb = 1.f, recl = 1.f;  // running products at A_next (chunk composition)
@@ -325,8 +343,8 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
       //      test as the per-pixel one, on the block rectangle) into the skip ring, cull
       //      tables and position metadata.  Four threads per Gaussian (stage_forms splits
       //      the coefficients); each evaluates the cull, part 3 records it.
-      for (int jj = threadIdx.x; jj < 4 * nb; jj += SBP) {
-        const int j = jj >> 2, part = jj & 3;
+      for (int jj = threadIdx.x; jj < NPART * nb; jj += SBP) {
+        const int j = jj / NPART, part = jj % NPART;
         const int64_t gp = tb + b0 + j;
         const int32_t g = A.vals[gp];
         const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
@@ -339,7 +357,7 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
           const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
           skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
         }
-        if (part == 3) {
+        if (part == NPART - 1) {
           const int bit = (b0 + j) & 255;
           if (skip)
             atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
@@ -377,12 +395,16 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
           }
           if (!skip) {
 #pragma unroll
-            for (int l = 0; l < SB; ++l) {
-              const double x = ox + l + 0.5, y = oy + l + 0.5;
+            for (int l = 0; l < SBX; ++l) {
+              const double x = ox + l + 0.5;
               const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+              cx2[j * SBX + l] = __dmul_rn(dx, dx);
+            }
+#pragma unroll
+            for (int l = 0; l < SBY; ++l) {
+              const double y = oy + l + 0.5;
               const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-              cx2[j * SB + l] = __dmul_rn(dx, dx);
-              cy2[j * SB + l] = __dmul_rn(dy, dy);
+              cy2[j * SBY + l] = __dmul_rn(dy, dy);
             }
           }
         }
@@ -479,7 +501,7 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
         float alo = 0.f, ahi = 0.f;
         bool keep = false;
         if (!(flags & F_SKIP)) {
-          keep = in_img && !(__dadd_rn(cx2[j * SB + lx], cy2[j * SB + ly]) > R.r2);
+          keep = in_img && !(__dadd_rn(cx2[j * SBX + lx], cy2[j * SBY + ly]) > R.r2);
           if (__any_sync(FULLM, keep)) {
             if (flags & F_FAIL) {
               ahi = keep ? R.o[1] : 0.f;
@@ -495,7 +517,7 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
         if (pmf & PM_STORE) {
           // (1 - a_hi) is read only through E_G of earlier partners (q has PM_EF), the
           // deferred lower term only at q's own finalisation (PM_EG)
-          const int rs = RS(qpos, 0, rmask);
+          const int rs = RS<SBP>(qpos, 0, rmask);
           rf[rs] = Tb;
           rf[rs + SBP] = 1.f - alo;
           if (pmf & PM_EF) rf[rs + 2 * SBP] = 1.f - ahi;
@@ -511,15 +533,15 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
           if (!(pmf & PM_OVF)) {
             bool done = false;
             if (R.tmode == 1) {  // dense: T_hi before h times the kept factors
-              float pr = rf[RS(R.ph, 0, rmask)];
+              float pr = rf[RS<SBP>(R.ph, 0, rmask)];
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) pr *= rf[RS(R.ph + R.tlo[t], 1, rmask)];
+              for (int t = 0; t < R.nT; ++t) pr *= rf[RS<SBP>(R.ph + R.tlo[t], 1, rmask)];
               tbv = pr;
               done = true;
             } else if (R.tmode == 2) {  // sparse: divide the running product (guarded, H3)
               float dfac = 1.f;
 #pragma unroll 4
-              for (int t = 0; t < R.nT; ++t) dfac *= rf[RS(R.ph + R.tlo[t], 1, rmask)];
+              for (int t = 0; t < R.nT; ++t) dfac *= rf[RS<SBP>(R.ph + R.tlo[t], 1, rmask)];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
@@ -529,28 +551,28 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
               const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
               const unsigned long long v1 =
                   wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
-              tbv = rf[RS(R.ph, 0, rmask)] * ring_prod(rf, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask);
+              tbv = rf[RS<SBP>(R.ph, 0, rmask)] * ring_prod<SBP>(rf, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask);
             }
           } else {  // long window: exception lists from global memory
             bool done = false;
             if (wlen > 2 * R.pnF + 8) {
               float dfac = 1.f;
               for (int e = 0; e < R.pnF; ++e)
-                dfac *= rf[RS(A.exc[R.peoff + e], 1, rmask)];
+                dfac *= rf[RS<SBP>(A.exc[R.peoff + e], 1, rmask)];
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
               }
             }
             if (!done) {
-              tbv = rf[RS(R.ph, 0, rmask)];
+              tbv = rf[RS<SBP>(R.ph, 0, rmask)];
               int e = 0;
               for (int r = R.ph; r < qpos; ++r) {
                 if (e < R.pnF && A.exc[R.peoff + e] == r) {
                   ++e;
                   continue;
                 }
-                tbv *= rf[RS(r, 1, rmask)];
+                tbv *= rf[RS<SBP>(r, 1, rmask)];
               }
             }
           }
@@ -575,30 +597,30 @@ __global__ void __launch_bounds__(SBP, 9) k_tile(TileArgs A) {
             const FinS& F = fins[f];
             if (F.qq < 0) continue;  // another chunk's position, or culled in this block
             clo = F.clo;
-            tl = rf[RS(F.qq, 3, rmask)];
+            tl = rf[RS<SBP>(F.qq, 3, rmask)];
             if (F.n >= 0) {
               tl *= 1.f - ahi;  // g itself
 #pragma unroll 4
-              for (int e = 0; e < F.n; ++e) tl *= rf[RS(F.qq + F.off[e], 2, rmask)];
+              for (int e = 0; e < F.n; ++e) tl *= rf[RS<SBP>(F.qq + F.off[e], 2, rmask)];
             } else {
               const FinRec& fr = A.fin_rec[F0 + f];
               if (!(fr.flags & PM_OVF)) {
-                tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
+                tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
               } else {
                 const int64_t o2 = fr.eoff + fr.nF;
-                for (int e = 0; e < fr.nG; ++e) tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
+                for (int e = 0; e < fr.nG; ++e) tl *= rf[RS<SBP>(A.exc[o2 + e], 2, rmask)];
               }
             }
           } else {
             const FinRec& fr = A.fin_rec[F0 + f];
             if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
             clo = fr.clo;
-            tl = rf[RS(fr.qq, 3, rmask)];
+            tl = rf[RS<SBP>(fr.qq, 3, rmask)];
             if (!(fr.flags & PM_OVF)) {
-              tl *= ring_prod(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
+              tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
             } else {
               const int64_t o2 = fr.eoff + fr.nF;
-              for (int e = 0; e < fr.nG; ++e) tl *= rf[RS(A.exc[o2 + e], 2, rmask)];
+              for (int e = 0; e < fr.nG; ++e) tl *= rf[RS<SBP>(A.exc[o2 + e], 2, rmask)];
             }
           }
 #pragma unroll
@@ -655,11 +677,12 @@ __global__ void k_merge(TileArgs A) {
   const int tile = blockIdx.x;
   const int n = A.item_cnt[tile];
   if (n <= 1) return;
-  const int ts = A.ts, npix = ts * ts, nsb = ts / SB, nsub = nsb * nsb;
+  const int ts = A.ts, npix = ts * ts, SBX = block_w(ts), SBP = SBX * SBY;
+  const int nsbx = ts / SBX, nsub = nsbx * (ts / SBY);
   const int tx = tile % A.ntx, ty = tile / A.ntx;
   for (int tp = threadIdx.x; tp < npix; tp += blockDim.x) {
     const int lx = tp % ts, ly = tp / ts;
-    const int sub = (ly / SB) * nsb + lx / SB, pix = (ly % SB) * SB + (lx % SB);
+    const int sub = (ly / SBY) * nsbx + lx / SBX, pix = pix_of(lx % SBX, ly % SBY, SBX);
     float Pb = 1.f, Pl = 1.f, h[3] = {0.f, 0.f, 0.f}, l[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < n; ++k) {
       const int64_t it = A.item_off[tile] + k;
@@ -699,16 +722,13 @@ __global__ void k_merge(TileArgs A) {
   }
 }
 
-int tile_threads(int ts) {
-  (void)ts;
-  return SBP;
-}
-int tile_subblocks(int ts) { return (ts / SB) * (ts / SB); }
+int tile_threads(int ts) { return block_w(ts) * SBY; }
+int tile_subblocks(int ts) { return (ts / block_w(ts)) * (ts / SBY); }
 
 template <int NV>
 static size_t smem_for(int ts, int bs) {
-  (void)ts;
-  return (size_t)bs * (sizeof(SRec<NV>) + 2 * SB * sizeof(double)) + FB * sizeof(FinS);
+  return (size_t)bs * (sizeof(SRec<NV>) + (block_w(ts) + SBY) * sizeof(double)) +
+         FB * sizeof(FinS);
 }
 
 size_t tile_smem_bytes(int nv, int ts, int bs) {
@@ -723,18 +743,23 @@ size_t tile_smem_bytes(int nv, int ts, int bs) {
   }
 }
 
-template <int NV>
-static int grid_one(int ts, int bs) {
+template <int NV, int BX>
+static int grid_bx(int ts, int bs) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_tile<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tile<NV, BX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   int per_sm = 0, dev = 0, nsm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV>, SBP, smem_for<NV>(ts, bs));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV, BX>, BX * SBY,
+                                                smem_for<NV>(ts, bs));
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   return std::max(1, per_sm) * nsm;
+}
+template <int NV>
+static int grid_one(int ts, int bs) {
+  return block_w(ts) == 16 ? grid_bx<NV, 16>(ts, bs) : grid_bx<NV, 8>(ts, bs);
 }
 
 int tile_grid(int nv, int ts, int bs) {
@@ -749,12 +774,20 @@ int tile_grid(int nv, int ts, int bs) {
   }
 }
 
+template <int NV>
+static void launch_one(const TileArgs& a, int grid, cudaStream_t st) {
+  if (block_w(a.ts) == 16)
+    k_tile<NV, 16><<<grid, 16 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);
+  else
+    k_tile<NV, 8><<<grid, 8 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);
+}
+
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st) {
   if (a.n_items <= 0 || grid <= 0) return;
   switch (nv) {
-#define CASE(K)                                                    \
-  case K:                                                          \
-    k_tile<K><<<grid, SBP, smem_for<K>(a.ts, a.bs), st>>>(a);      \
+#define CASE(K)                    \
+  case K:                          \
+    launch_one<K>(a, grid, st);    \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE

@@ -263,7 +263,7 @@ def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -
         if name == "C2":
             # Fig. 1: "camera shifts horizontally by 10cm" -> camera-x in [0, +0.10] (G10)
             box = _pose_box(eps_t=(0.05, 0, 0), t_off=(0.05, 0, 0), t_frame=1)
-            return _pack("C2", mean, chol, o, c, cam, box, tile=16, batch=16,
+            return _pack("C2", mean, chol, o, c, cam, box, tile=16, batch=24,
                          description="bulldozer-shaped ~100k, 200x200, 10 cm horizontal shift")
         # C5: scene-variation box: blade group moved along +y by [0, 0.05] m (one shared
         # variable), blade red channel [c_r, min(1, c_r + 0.5)], camera-x +-1 cm.
@@ -286,7 +286,7 @@ def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -
         cam = _camera((0.0, -2.0, 1.6), (0.0, 10.0, 1.0), 60.0, W, W)
         box = _pose_box(eps_t=(0.05, 0.05, 0.05), eps_R=(0, 0, math.radians(2.0)),
                         parts=(1, 1, 1, 1, 1, 8))
-        return _pack("C3", mean, chol, o, c, cam, box, tile=16, batch=16,
+        return _pack("C3", mean, chol, o, c, cam, box, tile=16, batch=24,
                      description="outdoor ~300k, 400x400, yaw +-2 deg (8 parts) + t +-5 cm")
     if name == "C4":
         n = 750_000 if N is None else N
@@ -294,6 +294,6 @@ def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -
         mean, chol, o, c = outdoor_scene(4, n)
         cam = _camera((0.0, -2.0, 1.6), (0.0, 10.0, 1.0), 60.0, W, W)
         box = _pose_box(eps_t=(0.01, 0.01, 0.01), eps_R=(math.radians(0.1),) * 3)
-        return _pack("C4", mean, chol, o, c, cam, box, tile=16, batch=16,
+        return _pack("C4", mean, chol, o, c, cam, box, tile=16, batch=24,
                      description="outdoor 750k, 800x800, 6-DoF box (t +-1 cm, Euler +-0.1 deg)")
     raise ValueError(f"unknown config {name!r}")
