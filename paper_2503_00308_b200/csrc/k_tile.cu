@@ -414,7 +414,9 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
       // ---- phase B (needs the batch's skip bits): T_hi window operands per position and
       //      the batch's finalisation records, both skip-filtered
       if (iexc) {
-        for (int j = threadIdx.x; j < nb; j += SBP) {
+        // (warp 0 builds the window lists while the other warps stage the finalisation
+        //  records below)
+        for (int j = threadIdx.x < 32 ? (int)threadIdx.x : nb; j < nb; j += 32) {
           SRec<NV>& S = srec[j];
           const int pmf = S.pmf, qpos = b0 + j;
           // (a skipped q contributes nothing: no T_hi needed)
@@ -446,7 +448,8 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         }
       }
       // finalisation records of the batch with their ring operands (skip-filtered)
-      for (int t = threadIdx.x; t < min(F1 - F0, FB); t += SBP) {
+      for (int t = (int)threadIdx.x - 32; t < min(F1 - F0, FB); t += SBP - 32) {
+        if (t < 0) break;
         const FinRec fr = A.fin_rec[F0 + t];
         FinS& F = fins[t];
         const int qq = fr.qq;
