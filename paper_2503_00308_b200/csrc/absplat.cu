@@ -53,7 +53,7 @@ struct as_ctx {
   // work buffers
   DevBuf pose, hot, pair, kkey, kkey2, kval, order, counts, offsets, cub_tmp;
   DevBuf keys, keys2, vals, vals2, tbegin, tend, tcost, tkey, tkey2, tids, tlist, tslot, owner;
-  DevBuf nF, nG, ntot, eoff, exc, hpos, diff, cover, pflag, is_store, slot, scratch;
+  DevBuf nF, nG, ntot, eoff, exc, hpos, gpos, diff, cover, pflag, is_store, slot, scratch;
   DevBuf tileh, tilemax, wsP, kapP, posD;
   DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
   DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e, finrec, maskF, maskG;
@@ -342,7 +342,7 @@ __global__ void k_slot_map(const int32_t* list, int n, int32_t* slot_of_tile) {
 
 // counters layout (unsigned long long[16])
 enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6, C_UNC = 8,
-       C_VIOL = 9, C_WMAX = 10, C_NCOUNTERS = 16 };
+       C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_NCOUNTERS = 16 };
 
 int64_t read_i64(as_ctx* ctx, const int64_t* dptr) {
   int64_t v = 0;
@@ -459,23 +459,37 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     pa.ntot = P<int64_t>(ctx->ntot);
     pa.counters = ctr + C_UNC;
     CK(cudaMemsetAsync(pa.ntot + M, 0, sizeof(int64_t), st));
+    ensure(ctx, ctx->hpos, sizeof(int32_t) * M);
+    ensure(ctx, ctx->gpos, sizeof(int32_t) * M);
+    ensure(ctx, ctx->maskF, sizeof(ulonglong2) * M);
+    ensure(ctx, ctx->maskG, sizeof(ulonglong2) * M);
+    pa.hpos = P<int32_t>(ctx->hpos);
+    pa.gpos = P<int32_t>(ctx->gpos);
+    pa.mF = P<ulonglong2>(ctx->maskF);
+    pa.mG = P<ulonglong2>(ctx->maskG);
+    pa.subunc = ctr + C_SUBUNC;
+    CK(cudaMemsetAsync(pa.subunc, 0, sizeof(unsigned long long), st));
     launch_pairs_prep(pa, st);
     LAUNCHED(ctx, 2);
-    launch_pairs_count(pa, st);
+    launch_pairs_count(pa, st);  // one classification pass: counts, h, g, 128-bit masks
     LAUNCHED(ctx, 1);
-    cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
-    const int64_t nexc = read_i64(ctx, P<int64_t>(ctx->eoff) + M);
-    if (nexc > 0) {
+    unsigned long long sub_unc = 0;
+    CK(cudaMemcpyAsync(&sub_unc, pa.subunc, sizeof sub_unc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (sub_unc > 0) {
+      // explicit lists only for positions with a partner more than 128 positions away
+      cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
+      const int64_t nexc = read_i64(ctx, P<int64_t>(ctx->eoff) + M);
       pa.off = P<int64_t>(ctx->eoff);
-      ensure(ctx, ctx->exc, sizeof(int32_t) * nexc);
-      ensure(ctx, ctx->hpos, sizeof(int32_t) * M);
+      ensure(ctx, ctx->exc, sizeof(int32_t) * std::max<int64_t>(nexc, 1));
+      pa.exc = P<int32_t>(ctx->exc);
+      if (nexc > 0) {
+        launch_pairs_fill(pa, st);
+        LAUNCHED(ctx, 1);
+      }
       ensure(ctx, ctx->diff, sizeof(int32_t) * 2 * (M + 1));
       ensure(ctx, ctx->cover, sizeof(int32_t) * 2 * (M + 1));
       ensure(ctx, ctx->pflag, sizeof(int4) * M);
-      pa.exc = P<int32_t>(ctx->exc);
-      pa.hpos = P<int32_t>(ctx->hpos);
-      launch_pairs_fill(pa, st);
-      LAUNCHED(ctx, 1);
       int32_t* dstore = P<int32_t>(ctx->diff);
       int32_t* dcut = dstore + (M + 1);
       int32_t* cstore = P<int32_t>(ctx->cover);
@@ -492,11 +506,9 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ensure(ctx, ctx->finval, sizeof(int32_t) * M);
       ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
       ensure(ctx, ctx->fin_b, sizeof(int32_t) * (M + 1));
-      ensure(ctx, ctx->maskF, sizeof(ulonglong2) * M);
-      ensure(ctx, ctx->maskG, sizeof(ulonglong2) * M);
       ensure(ctx, ctx->finrec, sizeof(FinRec) * M);
       launch_meta(pa, cstore, ccut, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
-                  P<int32_t>(ctx->finval), P<ulonglong2>(ctx->maskF), P<ulonglong2>(ctx->maskG), st);
+                  P<int32_t>(ctx->finval), st);
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
                       P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
@@ -815,7 +827,7 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
                     &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
                     &ctx->tids, &ctx->tlist, &ctx->tslot, &ctx->owner, &ctx->nF, &ctx->nG,
-                    &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->diff, &ctx->cover,
+                    &ctx->ntot, &ctx->eoff, &ctx->exc, &ctx->hpos, &ctx->gpos, &ctx->diff, &ctx->cover,
                     &ctx->pflag, &ctx->is_store, &ctx->slot, &ctx->scratch, &ctx->img_lo,
                     &ctx->img_hi, &ctx->counters, &ctx->conc_g, &ctx->untile_map, &ctx->tileh,
                     &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->posD, &ctx->item_off, &ctx->items, &ctx->items2,

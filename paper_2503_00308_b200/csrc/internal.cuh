@@ -271,6 +271,10 @@ struct PairArgs {
   const int64_t* off;     // [M+1] exclusive scan of nF+nG
   int32_t* exc;           // [total] tile-local positions: E_F ascending then E_G ascending
   int32_t* hpos;          // [M] first position of E_F (tile-local) or own position
+  int32_t* gpos;          // [M] last position of E_G (tile-local) or own position
+  ulonglong2* mF;         // [M] E_F bits over [h, h+128) (0 for PM_OVF positions)
+  ulonglong2* mG;         // [M] E_G bits over (p, p+128] (0 for PM_OVF positions)
+  unsigned long long* subunc;  // uncertain (position, partner) entries of this sub-box
   unsigned long long* counters;  // [0] uncertain pairs, [1] order violations
 };
 void launch_pairs_prep(const PairArgs& a, cudaStream_t st);
@@ -286,8 +290,7 @@ struct alignas(16) FinRec {
   float clo[3], pad;       // lower colour of q'
 };
 void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
-                 ulonglong2* mG, cudaStream_t st);
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st);
 void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
                    const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
 void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st);

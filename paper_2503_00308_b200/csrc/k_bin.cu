@@ -294,10 +294,41 @@ __device__ __forceinline__ bool beyond(double dk, double factor, double wsi, dou
   return dk * factor * (1.0 - 1e-9) > bound;
 }
 
-template <int NV, int PASS>  // PASS 0: count, 1: fill
+// 128-bit helpers (lo, hi halves)
+__device__ __forceinline__ void set_bit128(unsigned long long& m0, unsigned long long& m1, int i) {
+  if (i < 64)
+    m0 |= 1ull << i;
+  else
+    m1 |= 1ull << (i - 64);
+}
+__device__ __forceinline__ void shr128(unsigned long long& m0, unsigned long long& m1, int s) {
+  if (s >= 128) {
+    m0 = m1 = 0;
+  } else if (s >= 64) {
+    m0 = m1 >> (s - 64);
+    m1 = 0;
+  } else if (s > 0) {
+    m0 = (m0 >> s) | (m1 << (64 - s));
+    m1 >>= s;
+  }
+}
+
+// PASS 0 (every position): classify the window once; write |E_F|, |E_G|, h = min E_F,
+// g = max E_G (tile-local; the position itself when empty), the 128-bit masks E_F over
+// [h, h + 128) and E_G over (p, p + 128], and ntot = |E_F| + |E_G| only for positions whose
+// partners are more than 128 positions away (PM_OVF: they keep explicit CSR lists).
+// PASS 1 (PM_OVF positions only): fill those lists.
+template <int NV, int PASS>
 __global__ void k_pairs(PairArgs A) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
+  int64_t off = 0;
+  int nFt = 0;
+  if (PASS == 1) {
+    if (A.ntot[p] == 0) return;  // not an overflow position
+    off = A.off[p];
+    nFt = A.nF[p];
+  }
   const uint32_t t = A.keys[p];
   const int64_t b = A.tbegin[t], e = A.tend[t];
   const int32_t gi = A.vals[p];
@@ -307,13 +338,9 @@ __global__ void k_pairs(PairArgs A) {
   const double factor = A.tileh[(size_t)t * (NVMAX + 1) + NVMAX];
   const double wsi = A.wsP[p];
   int nF = 0, nG = 0, viol = 0;
-  int64_t off = 0;
-  int nFt = 0;
-  if (PASS == 1) {
-    off = A.off[p];
-    nFt = A.nF[p];
-  }
-  int hmin = (int)(p - b);
+  int hmin = (int)(p - b), gmax = (int)(p - b);
+  unsigned long long f0 = 0, f1 = 0, g0 = 0, g1 = 0;  // E_F rel. p - 128, E_G rel. p + 1
+  bool ovf = false;
   // backward: earlier positions (expected Ind in {1, ?})
   for (int64_t q = p - 1; q >= b; --q) {
     const double kj = A.kapP[q];
@@ -323,6 +350,12 @@ __global__ void k_pairs(PairArgs A) {
     if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
       if (c == 0) ++viol;
       if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
+      if (PASS == 0) {
+        if (p - q <= 128)
+          set_bit128(f0, f1, (int)(q - p + 128));
+        else
+          ovf = true;
+      }
       hmin = (int)(q - b);
       ++nF;
     }
@@ -336,17 +369,32 @@ __global__ void k_pairs(PairArgs A) {
     if (c == -1 || c == 1) {
       if (c == 1) ++viol;
       if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);
+      if (PASS == 0) {
+        if (q - p <= 128)
+          set_bit128(g0, g1, (int)(q - p - 1));
+        else
+          ovf = true;
+      }
+      gmax = (int)(q - b);
       ++nG;
     }
   }
   if (PASS == 0) {
     A.nF[p] = nF;
     A.nG[p] = nG;
-    A.ntot[p] = nF + nG;
+    A.hpos[p] = hmin;
+    A.gpos[p] = gmax;
+    A.ntot[p] = ovf ? nF + nG : 0;
+    if (ovf) {
+      f0 = f1 = g0 = g1 = 0;
+    } else {  // E_F relative to h: shift by h - (p - 128)
+      shr128(f0, f1, (int)(hmin - (p - b) + 128));
+    }
+    A.mF[p] = make_ulonglong2(f0, f1);
+    A.mG[p] = make_ulonglong2(g0, g1);
     warp_add(&A.counters[0], (unsigned)nG);
     warp_add(&A.counters[1], (unsigned)viol);
-  } else {
-    A.hpos[p] = hmin;
+    warp_add(A.subunc, (unsigned)(nF + nG));
   }
 }
 
@@ -395,44 +443,26 @@ void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t
 // per-position metadata for the tile kernel: {flags, h, g, nF}; max window -> wmax;
 // E_F(p) as a 128-bit mask over [h, h+128) and E_G(p) over (p, p+128] (PM_OVF if longer)
 __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                       unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
-                       ulonglong2* mG) {
+                       unsigned int* wmax, uint32_t* finkey, int32_t* finval) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
   const int nF = A.nF[p], nG = A.nG[p];
   const int64_t b = A.tbegin[A.keys[p]];
   const int loc = (int)(p - b);
-  const int h = (nF + nG) ? A.hpos[p] : loc;
-  const int64_t off = (nF + nG) ? A.off[p] : 0;
-  const int g = nG ? A.exc[off + nF + nG - 1] : loc;
+  const int h = A.hpos[p], g = A.gpos[p];
   const bool ovf = (loc - h) > 128 || (g - loc) > 128;
   int fl = (nF ? PM_EF : 0) | (nG ? PM_EG : 0) | (cstore[p] > 0 ? PM_STORE : 0) |
            (ccut[p] > 0 ? PM_NOCUT : 0) | (ovf ? PM_OVF : 0);
   pm[p] = make_int4(fl, h, g, nF);
-  unsigned long long f0 = 0, f1 = 0, g0 = 0, g1 = 0;
-  if (!ovf) {
-    for (int e = 0; e < nF; ++e) {
-      const int i = A.exc[off + e] - h;
-      if (i < 64) f0 |= 1ull << i; else f1 |= 1ull << (i - 64);
-    }
-    for (int e = 0; e < nG; ++e) {
-      const int i = A.exc[off + nF + e] - loc - 1;
-      if (i < 64) g0 |= 1ull << i; else g1 |= 1ull << (i - 64);
-    }
-  }
-  mF[p] = make_ulonglong2(f0, f1);
-  mG[p] = make_ulonglong2(g0, g1);
   warp_max_u32(wmax, (unsigned)max(loc - h, g - loc));
   // deferred lower contribution of p is finalised at its last later partner b + g
   finkey[p] = nG ? (uint32_t)(b + g) : 0xffffffffu;
   finval[p] = (int32_t)p;
 }
 void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, ulonglong2* mF,
-                 ulonglong2* mG, cudaStream_t st) {
+                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st) {
   if (a.M <= 0) return;
-  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval,
-                                                        mF, mG);
+  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval);
 }
 
 // finalisation records in sorted order: everything the tile kernel needs about q'
