@@ -257,6 +257,52 @@ __device__ __forceinline__ void skip_win(const unsigned* sk, int base, unsigned 
 
 // product of ring component `comp` over the positions base + i for the set bits i of the
 // 128-bit mask (m0, m1); loads are issued in groups of 8 so they overlap.  rf = ring + pix.
+// product of ring component `comp` over the positions list[0 .. n) (an exception list in
+// global memory), in order; list entries and ring values are loaded 8 at a time
+template <int SBP>
+__device__ __noinline__ float exc_prod(const float* rf, const int32_t* list, int n, int comp,
+                                       int rmask) {
+  float prod = 1.f;
+  for (int e0 = 0; e0 < n; e0 += 8) {
+    int idx[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) idx[u] = e0 + u < n ? list[e0 + u] : -1;
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = idx[u] >= 0 ? rf[RS<SBP>(idx[u], comp, rmask)] : 1.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) prod *= v[u];
+  }
+  return prod;
+}
+
+// product of ring component 1 over the window [h, q) minus the sorted list ef[0 .. nf)
+// (T_hi of a long window, dense case), ring values loaded 8 at a time
+template <int SBP>
+__device__ __noinline__ float window_prod(const float* rf, int h, int q, const int32_t* ef, int nf,
+                                          int rmask) {
+  float prod = 1.f;
+  int e = 0;
+  int nextF = nf > 0 ? ef[0] : 0x7fffffff;
+  for (int r0 = h; r0 < q; r0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = r0 + u < q ? rf[RS<SBP>(r0 + u, 1, rmask)] : 1.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u;
+      if (r >= q) break;
+      if (r == nextF) {
+        ++e;
+        nextF = e < nf ? ef[e] : 0x7fffffff;
+      } else {
+        prod *= v[u];
+      }
+    }
+  }
+  return prod;
+}
+
 template <int SBP>
 __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m0,
                                            unsigned long long m1, int base, int comp, int rmask) {
@@ -559,25 +605,15 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
           } else {  // long window: exception lists from global memory
             bool done = false;
             if (wlen > 2 * R.pnF + 8) {
-              float dfac = 1.f;
-              for (int e = 0; e < R.pnF; ++e)
-                dfac *= rf[RS<SBP>(A.exc[R.peoff + e], 1, rmask)];
+              const float dfac = exc_prod<SBP>(rf, A.exc + R.peoff, R.pnF, 1, rmask);
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
               }
             }
-            if (!done) {
-              tbv = rf[RS<SBP>(R.ph, 0, rmask)];
-              int e = 0;
-              for (int r = R.ph; r < qpos; ++r) {
-                if (e < R.pnF && A.exc[R.peoff + e] == r) {
-                  ++e;
-                  continue;
-                }
-                tbv *= rf[RS<SBP>(r, 1, rmask)];
-              }
-            }
+            if (!done)
+              tbv = rf[RS<SBP>(R.ph, 0, rmask)] *
+                    window_prod<SBP>(rf, R.ph, qpos, A.exc + R.peoff, R.pnF, rmask);
           }
         }
         const float wb = main ? tbv * ahi : 0.f;
@@ -610,8 +646,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
               if (!(fr.flags & PM_OVF)) {
                 tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
               } else {
-                const int64_t o2 = fr.eoff + fr.nF;
-                for (int e = 0; e < fr.nG; ++e) tl *= rf[RS<SBP>(A.exc[o2 + e], 2, rmask)];
+                tl *= exc_prod<SBP>(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask);
               }
             }
           } else {
@@ -622,8 +657,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
             if (!(fr.flags & PM_OVF)) {
               tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
             } else {
-              const int64_t o2 = fr.eoff + fr.nF;
-              for (int e = 0; e < fr.nG; ++e) tl *= rf[RS<SBP>(A.exc[o2 + e], 2, rmask)];
+              tl *= exc_prod<SBP>(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask);
             }
           }
 #pragma unroll
