@@ -230,3 +230,16 @@ def test_subbox_ranges(ctx, oracle):
     from paper_2503_00308_b200 import AbsplatError
     with pytest.raises(AbsplatError):
         ctx.as_render_subboxes(0, P + 1, 16, 16)
+
+
+def test_opacity_box_parity(ctx, oracle):
+    """The paper's opacity experiment (§4.6) on C5's blade group: opacity intervals
+    [o', o' + 0.1] with o' = 0.1 o, with C5's pose / shift / colour boxes (reduced size)."""
+    from workloads import opacity_variant
+    w = make_config("C5", **SMALL["C5"])
+    v = opacity_variant(w, w.scene_box["group_of"] >= 0)
+    lo, hi, st = gpu_render(ctx, v)
+    olo, ohi, ost = oracle.render_bounds(v)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= TOL, err
+    assert st["pairs"] == ost["pairs"] and st["active_pairs"] == ost["active_pairs"]

@@ -248,6 +248,50 @@ def test_colour_box_closed_form(oracle):
     assert (hi - lo).max() > 0.1  # the red interval is visible
 
 
+def test_opacity_box_single_gaussian_closed_form(oracle):
+    """Opacity intervals only (zero-width pose), one Gaussian: pc = a c with a = o e^{-s/2}
+    linear in o (Alg. 1 l.10), so lo = render(o_lo) and hi = render(o_hi) exactly."""
+    from workloads import opacity_variant
+    w = zero_box(make_config("C1", N=1, res=16))
+    v = opacity_variant(w, np.ones(1, bool), scale=0.6, delta=0.3)
+    lo, hi, st = oracle.render_bounds(v)
+    assert st["n_vars"] == 0
+    r_lo = oracle.render_concrete(v, opacity=v.scene_box["op_lo"])
+    r_hi = oracle.render_concrete(v, opacity=v.scene_box["op_hi"])
+    slack = v.N * TAU + 1e-12
+    assert np.abs(lo - r_lo).max() <= slack and np.abs(hi - r_hi).max() <= slack
+    assert (hi - lo).max() > 0.05
+
+
+def test_opacity_box_contains_sampled_scenes(oracle):
+    """The paper's opacity experiment (§4.6: opacities scaled by 0.1, +0.1 box) on the
+    C5 blade group together with its pose, shift and colour boxes: Theorem 1 containment at
+    sampled (pose, shift, colour, opacity) points, and looser than without the opacity box."""
+    from workloads import opacity_variant
+    w = small("C5")
+    v = opacity_variant(w, w.scene_box["group_of"] >= 0)
+    lo, hi, st = oracle.render_bounds(v)
+    assert np.all(lo <= hi) and lo.min() >= 0 and hi.max() <= 1
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    sb = v.scene_box
+    for p in H.sample_params(v, rng, n_random=30, corners=True):
+        e, t, shifts = H.pose_of(v, p)
+        a = rng.uniform(size=(v.N, 1))
+        col = (sb["col_lo"] + a * (sb["col_hi"] - sb["col_lo"])).astype(np.float32)
+        b = rng.uniform(size=v.N)
+        op = (sb["op_lo"] + b * (sb["op_hi"] - sb["op_lo"])).astype(np.float32)
+        img = oracle.render_concrete(v, euler=e, t=t, shifts=shifts, color=col, opacity=op)
+        worst = max(worst, (lo - img).max(), (img - hi).max())
+    assert worst <= 1e-9, worst
+    # the same scene with the opacities fixed at their nominal (scaled) values is tighter
+    fixed = copy.deepcopy(v)
+    fixed.scene_box = dict(v.scene_box, op_lo=None, op_hi=None)
+    flo, fhi, _ = oracle.render_bounds(fixed)
+    assert H.mpg(lo, hi) > H.mpg(flo, fhi)
+    assert np.all(lo <= flo + 1e-12) and np.all(hi >= fhi - 1e-12)
+
+
 def test_partitioning_tightens(oracle):
     """Trend: partitioning C tightens the union of bounds."""
     w = small("C3", N=1500, res=24)

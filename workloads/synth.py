@@ -240,6 +240,28 @@ def outdoor_scene(seed: int, N: int, n_trees: int = 60, extent: float = 30.0):
 
 
 # ----------------------------------------------------------------------------- configs
+def opacity_variant(w: Workload, member: np.ndarray, scale: float = 0.1,
+                    delta: float = 0.1) -> Workload:
+    """The paper's opacity experiment (§4.6): the member Gaussians' opacities are scaled
+    by `scale` (capped at 1) and perturbed by +`delta`, i.e. o in [o', min(1, o' + delta)]
+    with the nominal o' = min(1, scale * o).  Other scene-box entries of w are kept."""
+    import copy
+    v = copy.deepcopy(w)
+    o = np.asarray(w.opacity, np.float32).copy()
+    o[member] = np.minimum(np.float32(1.0), np.float32(scale) * o[member])
+    hi = o.copy()
+    hi[member] = np.minimum(np.float32(1.0), o[member] + np.float32(delta))
+    v.opacity = o
+    sb = dict(v.scene_box) if v.scene_box is not None else dict(
+        n_groups=0, group_of=None, dir=None, shift_lo=None, shift_hi=None, parts=[1, 1, 1],
+        col_lo=None, col_hi=None)
+    sb["op_lo"] = o.copy()
+    sb["op_hi"] = hi
+    v.scene_box = sb
+    v.name = w.name + "-opacity"
+    return v
+
+
 def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -> Workload:
     """Build config C1..C5.  N / res override the Gaussian count and image edge (the
     focal length scales with res so the field of view is unchanged) for reduced-size
