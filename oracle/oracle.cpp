@@ -272,6 +272,17 @@ int setup_problem(Problem& P, int64_t N, const float* mean, const float* chol, c
     if (var) ++nvar;
     P.n_sub *= P.axes[a].parts;
   }
+  if (box->n_explicit < 0) return -1;
+  if (box->n_explicit > 0) {  // explicit partition: each sub-box inside the box
+    if (!box->explicit_bounds) return -1;
+    for (int s = 0; s < box->n_explicit; ++s)
+      for (int a = 0; a < 9; ++a) {
+        const double lo = box->explicit_bounds[(s * 9 + a) * 2];
+        const double hi = box->explicit_bounds[(s * 9 + a) * 2 + 1];
+        if (!(lo <= hi) || lo < P.axes[a].lo || hi > P.axes[a].hi) return -1;
+      }
+    P.n_sub = box->n_explicit;
+  }
   if (nvar > NV) return -1;
   if (cam->W <= 0 || cam->H <= 0) return -1;
   return 0;
@@ -281,6 +292,18 @@ int setup_problem(Problem& P, int64_t N, const float* mean, const float* chol, c
 SubBox make_subbox(const Problem& P, int s) {
   SubBox B;
   B.n = 0;
+  if (P.box.n_explicit > 0) {  // explicit partition: centre / half-width of each axis
+    for (int a = 0; a < 9; ++a) {
+      const double lo = P.box.explicit_bounds[(s * 9 + a) * 2];
+      const double hi = P.box.explicit_bounds[(s * 9 + a) * 2 + 1];
+      const double c = 0.5 * (lo + hi);
+      if (P.axes[a].hi > P.axes[a].lo) {  // a variable of the full box (possibly zero width here)
+        B.v[B.n++] = {a, c, 0.5 * (hi - lo)};
+      }
+      B.fixed[a] = c;
+    }
+    return B;
+  }
   int rem = s;
   for (int a = 0; a < 9; ++a) {
     const Axis& ax = P.axes[a];

@@ -35,6 +35,11 @@ typedef struct {
   double R_off[3];   /* centre offset of the Euler box */
   int32_t t_frame;   /* 0 = world axes, 1 = nominal camera axes */
   int32_t parts[6];  /* uniform partition count per pose axis (tx,ty,tz,e0,e1,e2) (G18) */
+  /* Optional explicit partition (NEXT-3 refinement, P:470 (2)): n_explicit > 0 replaces the
+   * uniform grid by n_explicit sub-boxes, bounds [n][9][2] = (lo, hi) per box axis in the
+   * box's own units (t offsets, Euler offsets, group shifts 0..2), each inside the box. */
+  int32_t n_explicit;
+  const double* explicit_bounds;
 } or_pose_box;
 
 typedef struct {

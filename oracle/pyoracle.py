@@ -38,7 +38,8 @@ class Camera(C.Structure):
 
 class PoseBox(C.Structure):
     _fields_ = [("eps_t", C.c_double * 3), ("eps_R", C.c_double * 3), ("t_off", C.c_double * 3),
-                ("R_off", C.c_double * 3), ("t_frame", C.c_int32), ("parts", C.c_int32 * 6)]
+                ("R_off", C.c_double * 3), ("t_frame", C.c_int32), ("parts", C.c_int32 * 6),
+                ("n_explicit", C.c_int32), ("explicit_bounds", C.c_void_p)]
 
 
 class SceneBox(C.Structure):
@@ -121,6 +122,12 @@ def pose_box_struct(box: dict) -> PoseBox:
     b.t_frame = int(box["t_frame"])
     for k in range(6):
         b.parts[k] = int(box["parts"][k])
+    sub = box.get("subboxes")
+    if sub is not None and len(sub) > 0:
+        arr = np.ascontiguousarray(sub, np.float64).reshape(-1, 9, 2)
+        b._keep = arr  # keep alive with the struct
+        b.n_explicit = arr.shape[0]
+        b.explicit_bounds = arr.ctypes.data
     return b
 
 

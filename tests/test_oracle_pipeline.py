@@ -373,3 +373,48 @@ def test_subbox_ranges_compose_to_the_union(oracle):
     assert max(np.abs(s_lo - d_lo).max(), np.abs(s_hi - d_hi).max()) <= 1e-12
     with pytest.raises(ValueError):
         oracle.render_subboxes(w, 0, P + 1)
+
+
+def _uniform_as_explicit(w):
+    """The uniform yaw partition of w written as an explicit sub-box list [P][9][2]."""
+    pb = w.pose_box
+    lo = [pb["t_off"][a] - pb["eps_t"][a] for a in range(3)] + \
+         [pb["R_off"][a] - pb["eps_R"][a] for a in range(3)] + [0.0, 0.0, 0.0]
+    hi = [pb["t_off"][a] + pb["eps_t"][a] for a in range(3)] + \
+         [pb["R_off"][a] + pb["eps_R"][a] for a in range(3)] + [0.0, 0.0, 0.0]
+    P = pb["parts"][5]
+    out = np.zeros((P, 9, 2))
+    for m in range(P):
+        for a in range(9):
+            out[m, a] = (lo[a], hi[a])
+        wd = hi[5] - lo[5]
+        out[m, 5] = (lo[5] + wd * m / P, lo[5] + wd * (m + 1) / P)
+    return out
+
+
+def test_explicit_partition_equals_uniform(oracle):
+    """NEXT-3 (P:470 (2)): an explicit sub-box list describing the uniform partition
+    renders the same union (up to the rounding of the sub-box centres), and a list with one
+    box equal to the whole box renders the unpartitioned image."""
+    w = make_config("C3", N=400, res=24)
+    ulo, uhi, ust = oracle.render_bounds(w)
+    e = copy.deepcopy(w)
+    e.pose_box = dict(w.pose_box, parts=[1, 1, 1, 1, 1, 1], subboxes=_uniform_as_explicit(w))
+    elo, ehi, est = oracle.render_bounds(e)
+    assert est["n_sub"] == ust["n_sub"] == 8 and est["pairs"] == ust["pairs"]
+    assert max(np.abs(elo - ulo).max(), np.abs(ehi - uhi).max()) <= 1e-12
+    one = copy.deepcopy(w)
+    one.pose_box = dict(w.pose_box, parts=[1, 1, 1, 1, 1, 1])
+    olo, ohi, _ = oracle.render_bounds(one)
+    whole = _uniform_as_explicit(w)[:1].copy()
+    whole[0, 5] = (w.pose_box["R_off"][2] - w.pose_box["eps_R"][2],
+                   w.pose_box["R_off"][2] + w.pose_box["eps_R"][2])
+    one.pose_box = dict(one.pose_box, subboxes=whole)
+    xlo, xhi, _ = oracle.render_bounds(one)
+    assert max(np.abs(xlo - olo).max(), np.abs(xhi - ohi).max()) <= 1e-12
+    bad = copy.deepcopy(one)
+    wb = whole.copy()
+    wb[0, 5, 1] += 0.1  # beyond the box
+    bad.pose_box = dict(one.pose_box, subboxes=wb)
+    with pytest.raises(ValueError):
+        oracle.render_bounds(bad)
