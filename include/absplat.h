@@ -151,6 +151,21 @@ as_status as_render_subboxes(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s
                              as_stats* stats);
 as_status as_subbox_count(as_ctx* ctx, int32_t* n_sub);
 
+/* ---- explicit partitions and adaptive refinement (PAPER.md:470 (2):
+ * "iteratively divide the input range until the assertion [rho < 1] is satisfied") ----
+ * as_set_subboxes replaces the uniform grid of as_pose_box.parts by n explicit sub-boxes:
+ * bounds [n][9][2] = (lo, hi) per box axis (tx, ty, tz, e0, e1, e2 in as_pose_box units, then
+ * the group shifts 0..2), each inside the box (AS_E_ARG otherwise; an axis the box does not
+ * perturb must be given as its fixed value).  Host pointer, copied.  n = 0 restores the
+ * uniform grid; as_set_pose_box also clears the list.  Sub-box s of the list is sub-box s of
+ * as_render_subboxes.
+ * as_subbox_fails writes, for every sub-box of the current partition, the number of
+ * (non-dropped) Gaussians whose MatrixInv fails there (det <= 0 or rho >= 1: a in [0, o_hi]),
+ * running only the per-Gaussian setup; fails is host int64[n >= number of sub-boxes].  The
+ * Python driver `paper_2503_00308_b200.refine` bisects failing sub-boxes with these counts. */
+as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds);
+as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
+
 /* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----
  * Every rank holds the full scene and runs the per-Gaussian setup; image tiles are
  * assigned to ranks by a deterministic longest-processing-time rule over per-tile Gaussian

@@ -95,6 +95,8 @@ def lib():
         "as_set_allocator": (i32, [P, ALLOC_FN, FREE_FN, P]),
         "as_render_subboxes": (i32, [P, i32, i32, i32, i32, P, P, i32, P]),
         "as_subbox_count": (i32, [P, P]),
+        "as_set_subboxes": (i32, [P, i32, P]),
+        "as_subbox_fails": (i32, [P, i32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

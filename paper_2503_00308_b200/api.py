@@ -237,6 +237,21 @@ class Context:
                                                flags, C.byref(st) if st is not None else None))
         return lo, hi, (st.asdict() if st is not None else None)
 
+    def as_set_subboxes(self, bounds=None):
+        """Explicit partition: bounds [n, 9, 2] (lo, hi per box axis); None / empty clears."""
+        if bounds is None or len(bounds) == 0:
+            self._check(self._L.as_set_subboxes(self._ctx, 0, None))
+            return
+        b = np.ascontiguousarray(bounds, np.float64).reshape(-1, 9, 2)
+        self._check(self._L.as_set_subboxes(self._ctx, b.shape[0], C.c_void_p(b.ctypes.data)))
+
+    def as_subbox_fails(self):
+        """MatrixInv FAIL count per sub-box of the current partition (setup only)."""
+        n = self.as_subbox_count()
+        out = np.zeros(max(n, 1), np.int64)
+        self._check(self._L.as_subbox_fails(self._ctx, n, C.c_void_p(out.ctypes.data)))
+        return out[:n]
+
     def as_subbox_count(self) -> int:
         n = C.c_int32(0)
         self._check(self._L.as_subbox_count(self._ctx, C.byref(n)))

@@ -63,6 +63,9 @@ struct as_ctx {
   int last_items = 0, last_grid = 0, last_R = 1, max_window = 0, last_wmax = 0;
   cudaEvent_t ev[8] = {};
   bool events = false;
+  // explicit partition (as_set_subboxes): host copy [n][9][2] and its device mirror
+  std::vector<double> sub_host;
+  DevBuf subs;
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
   as_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -209,6 +212,20 @@ as_status make_box(as_ctx* ctx, BoxInfo& bi) {
       ++nv;
     }
     nsub *= bp.parts[a];
+  }
+  if (!ctx->sub_host.empty()) {  // explicit partition: each sub-box inside the box
+    const int ne = (int)(ctx->sub_host.size() / 18);
+    for (int s = 0; s < ne; ++s)
+      for (int a = 0; a < 9; ++a) {
+        const double lo = ctx->sub_host[(s * 9 + a) * 2], hi = ctx->sub_host[(s * 9 + a) * 2 + 1];
+        if (!(lo <= hi) || lo < bp.lo[a] || hi > bp.hi[a]) {
+          set_err(ctx, "explicit sub-box %d axis %d [%g, %g] outside the box [%g, %g]", s, a, lo,
+                  hi, bp.lo[a], bp.hi[a]);
+          return AS_E_ARG;
+        }
+      }
+    nsub = ne;
+    bp.sub = P<double>(ctx->subs);
   }
   if (nsub > 1000000) {
     set_err(ctx, "too many sub-boxes (%lld)", nsub);
@@ -822,7 +839,7 @@ as_status as_destroy(as_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->group_of,
-                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->pose, &ctx->hot,
+                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->subs, &ctx->pose, &ctx->hot,
                     &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
                     &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
@@ -943,6 +960,66 @@ as_status as_set_camera(as_ctx* ctx, const as_camera* cam) {
   return AS_OK;
 }
 
+as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds) {
+  if (!ctx) return AS_E_ARG;
+  if (n < 0 || (n > 0 && !bounds) || n > 1000000) {
+    set_err(ctx, "as_set_subboxes: bad arguments (n = %d)", n);
+    return AS_E_ARG;
+  }
+  std::vector<double> saved;
+  saved.swap(ctx->sub_host);
+  ctx->sub_host.assign(bounds, bounds + (size_t)n * 18);
+  if (ctx->have_box) {
+    BoxInfo bi;
+    const as_status st = make_box(ctx, bi);
+    if (st != AS_OK) {
+      ctx->sub_host.swap(saved);
+      return st;
+    }
+  }
+  try {
+    if (n > 0) {
+      cudaSetDevice(ctx->device);
+      ensure(ctx, ctx->subs, sizeof(double) * 18 * (size_t)n);
+      CK(cudaMemcpyAsync(ctx->subs.p, ctx->sub_host.data(), sizeof(double) * 18 * (size_t)n,
+                         cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  } catch (const Err& e) {
+    ctx->sub_host.swap(saved);
+    return e.st;
+  }
+  return AS_OK;
+}
+
+as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails) {
+  as_status st = check_ready(ctx);
+  if (st != AS_OK) return st;
+  BoxInfo bi;
+  if ((st = make_box(ctx, bi)) != AS_OK) return st;
+  if (!fails || n < bi.n_sub) {
+    set_err(ctx, "as_subbox_fails: need room for %d counts", bi.n_sub);
+    return AS_E_ARG;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    prepare_common(ctx, bi, geometry(ctx, 16));
+    unsigned long long* ctr = P<unsigned long long>(ctx->counters);
+    for (int s = 0; s < bi.n_sub; ++s) {
+      CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_NCOUNTERS, ctx->stream));
+      run_setup(ctx, bi, s);
+      unsigned long long h = 0;
+      CK(cudaMemcpyAsync(&h, ctr + C_FAIL, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      fails[s] = (int64_t)h;
+    }
+    CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_NCOUNTERS, ctx->stream));
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
+}
+
 as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box) {
   if (!ctx) return AS_E_ARG;
   if (!box) {
@@ -952,15 +1029,19 @@ as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box) {
   as_pose_box saved = ctx->box;
   const bool had = ctx->have_box;
   ctx->box = *box;
+  std::vector<double> saved_sub;
+  saved_sub.swap(ctx->sub_host);  // a new box clears an explicit partition
   BoxInfo bi;
   as_status st = make_box(ctx, bi);
   if (st != AS_OK) {
     ctx->box = saved;
     ctx->have_box = had;
+    ctx->sub_host.swap(saved_sub);
     return st;
   }
   if (box->t_frame != 0 && box->t_frame != 1) {
     ctx->box = saved;
+    ctx->sub_host.swap(saved_sub);
     set_err(ctx, "t_frame must be 0 or 1");
     return AS_E_ARG;
   }

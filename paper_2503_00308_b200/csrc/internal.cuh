@@ -39,6 +39,7 @@ struct BoxParams {  // kernel-argument copy of the box (a0)
   double lo[9], hi[9];
   int parts[9];
   int n_sub;
+  const double* sub;  // explicit partition [n_sub][9][2] (device), or nullptr: uniform grid
   int t_frame;
   double euler0[3], t0[3];
   double dir[3][3];

@@ -37,7 +37,7 @@ __device__ void rc2w(const double e[3], int which, double R[9]) {
     for (int j = 0; j < 3; ++j) R[3 * i + j] = T[3 * i] * X[j] + T[3 * i + 1] * X[3 + j] + T[3 * i + 2] * X[6 + j];
 }
 
-// One thread per sub-box: a0 (uniform partition) + a1 (pose forms).
+// One thread per sub-box: a0 (uniform partition or explicit list) + a1 (pose forms).
 __global__ void k_pose(BoxParams bp, PoseDev* out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= bp.n_sub) return;
@@ -48,6 +48,16 @@ __global__ void k_pose(BoxParams bp, PoseDev* out) {
   double fixed[9];
   int rem = s;
   for (int a = 0; a < 9; ++a) {
+    if (bp.sub) {  // explicit partition (NEXT-3 refinement): centre / half-width per axis
+      const double lo = bp.sub[(s * 9 + a) * 2], hi = bp.sub[(s * 9 + a) * 2 + 1];
+      fixed[a] = 0.5 * (lo + hi);
+      if (bp.hi[a] > bp.lo[a]) {  // a variable of the full box (possibly zero width here)
+        axis[n] = a;
+        rr[n] = 0.5 * (hi - lo);
+        ++n;
+      }
+      continue;
+    }
     const int p = bp.parts[a];
     const int m = rem % p;
     rem /= p;
