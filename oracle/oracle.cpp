@@ -273,6 +273,7 @@ int setup_problem(Problem& P, int64_t N, const float* mean, const float* chol, c
     P.n_sub *= P.axes[a].parts;
   }
   if (box->n_explicit < 0) return -1;
+  if (box->k_tol > 0 && (box->k_max < K_TAYLOR || box->k_max > 64)) return -1;
   if (box->n_explicit > 0) {  // explicit partition: each sub-box inside the box
     if (!box->explicit_bounds) return -1;
     for (int s = 0; s < box->n_explicit; ++s)
@@ -402,13 +403,30 @@ struct GRec {
   int flags;
   Form uc[3], d, up[2], Mp[2][3], X[3], conic[4], W[2][3], D2, DU[2];
   double eps, rho;
+  int k;                // Taylor order used by MatrixInv
   double kappa;         // sort key: mid of d's forms at xi = 0 (step 12)
   double mu_lo[2], mu_hi[2], r2;  // footprint (step 11, G12)
   double o_lo, o_hi, c_lo[3], c_hi[3];
 };
 
+// Adaptive order (P:470 (3)): the smallest k >= k0 with Eps(k) = |X0|_F rho^(k+1) / (1 - rho)
+// <= tol, at most kmax (tol <= 0: k0).  rho^(k+1) by repeated multiplication (reproducible).
+int adaptive_k(double nx0, double rho, int k0, double tol, int kmax) {
+  if (!(tol > 0)) return k0;
+  double r = 1.0;
+  for (int i = 0; i < k0 + 1; ++i) r *= rho;
+  int k = k0;
+  while (k < kmax && nx0 * r / (1.0 - rho) > tol) {
+    r *= rho;
+    ++k;
+  }
+  return k;
+}
+
 // MatrixInv (Alg. 4) on forms X[4] (row-major).  Returns 0 / 1 (det<=0) / 2 (rho>=1)
-int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rho) {
+// k < 0 selects the order adaptively: k = adaptive_k(|X0|_F, rho, 8, k_tol, k_max).
+int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rho,
+               double k_tol = 0.0, int k_max = 8, int* k_used = nullptr) {
   // (1) X0 = inverse of the centre matrix of the input set (P:470, P:550 footnote)
   double Xc[4];
   for (int e = 0; e < 4; ++e) {
@@ -439,6 +457,11 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
   }
   rho = std::sqrt(ss);
   if (!(rho < 1.0)) return 2;
+  if (k < 0) {
+    const double nx = std::sqrt(X0[0] * X0[0] + X0[1] * X0[1] + X0[2] * X0[2] + X0[3] * X0[3]);
+    k = adaptive_k(nx, rho, 8, k_tol, k_max);
+  }
+  if (k_used) *k_used = k;
   // l.3  Xa = Mmul(X0, Pow(IXX0, i)), i = 0..k ; Pow as a left fold P^i = P^{i-1} . E
   //      (Mmul of two form matrices uses R1, or R2 when both operands are the same form)
   std::vector<Form> Pw(4), Pn(4);
@@ -546,7 +569,10 @@ GRec gaussian_setup(const Problem& P, const SubBox& B, const Pose& pose, int64_t
   G.X[1] = X01;
   G.X[2] = X11;
   Form Xm[4] = {X00, X01, X01, X11};
-  int st = matrix_inv(Xm, n, K_TAYLOR, G.conic, G.eps, G.rho);
+  G.k = K_TAYLOR;
+  int st = (P.box.k_tol > 0)
+               ? matrix_inv(Xm, n, -1, G.conic, G.eps, G.rho, P.box.k_tol, P.box.k_max, &G.k)
+               : matrix_inv(Xm, n, K_TAYLOR, G.conic, G.eps, G.rho);
   if (st != 0) G.flags |= GF_FAIL;
   // l.9 pieces: W = Mmul(Conic, Mp) (association G4), D2 = Mul(d,d), DU = Mul(d, up)
   if (!(G.flags & GF_FAIL)) {
@@ -1085,7 +1111,7 @@ int32_t or_gaussian_forms(int64_t N, const float* mean, const float* chol, const
     sc[6] = G.mu_hi[0];
     sc[7] = G.mu_hi[1];
     sc[8] = G.r2;
-    sc[9] = 0;
+    sc[9] = G.k;
   }
   *nvars = n;
   return P.n_sub;

@@ -40,6 +40,11 @@ typedef struct {
    * box's own units (t offsets, Euler offsets, group shifts 0..2), each inside the box. */
   int32_t n_explicit;
   const double* explicit_bounds;
+  /* Adaptive Taylor order (NEXT-3, P:470 (3): "increase k until Eps falls below the given
+   * tolerance"): k_tol > 0 picks, per Gaussian, the smallest k >= 8 with Eps <= k_tol, at most
+   * k_max; k_tol <= 0 keeps k = 8 (G14). */
+  double k_tol;
+  int32_t k_max;
 } or_pose_box;
 
 typedef struct {

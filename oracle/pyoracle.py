@@ -39,7 +39,8 @@ class Camera(C.Structure):
 class PoseBox(C.Structure):
     _fields_ = [("eps_t", C.c_double * 3), ("eps_R", C.c_double * 3), ("t_off", C.c_double * 3),
                 ("R_off", C.c_double * 3), ("t_frame", C.c_int32), ("parts", C.c_int32 * 6),
-                ("n_explicit", C.c_int32), ("explicit_bounds", C.c_void_p)]
+                ("n_explicit", C.c_int32), ("explicit_bounds", C.c_void_p),
+                ("k_tol", C.c_double), ("k_max", C.c_int32)]
 
 
 class SceneBox(C.Structure):
@@ -122,6 +123,8 @@ def pose_box_struct(box: dict) -> PoseBox:
     b.t_frame = int(box["t_frame"])
     for k in range(6):
         b.parts[k] = int(box["parts"][k])
+    b.k_tol = float(box.get("k_tol", 0.0))
+    b.k_max = int(box.get("k_max", 8))
     sub = box.get("subboxes")
     if sub is not None and len(sub) > 0:
         arr = np.ascontiguousarray(sub, np.float64).reshape(-1, 9, 2)
@@ -378,7 +381,7 @@ GFIELDS = (["uc0", "uc1", "uc2", "d", "up0", "up1"]
            + ["X00", "X01", "X11", "conic00", "conic01", "conic10", "conic11"]
            + [f"W{a}{c}" for a in range(2) for c in range(3)]
            + ["D2", "DU0", "DU1"])
-GSCALARS = ["flags", "eps", "rho", "kappa", "mu_lo0", "mu_lo1", "mu_hi0", "mu_hi1", "r2", "pad"]
+GSCALARS = ["flags", "eps", "rho", "kappa", "mu_lo0", "mu_lo1", "mu_hi0", "mu_hi1", "r2", "k"]
 
 
 def gaussian_forms(w, sub=0):

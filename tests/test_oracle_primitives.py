@@ -307,3 +307,35 @@ def test_lemma2_random(oracle):
         assert np.allclose(oracle.blend_ind(a[perm], c[perm], d[perm]), pi, atol=1e-12)
         assert np.all(ps <= 1 + 1e-12)
     assert worst <= 1e-12
+
+
+def test_adaptive_taylor_order(oracle):
+    """P:470 (3): "increase k until Eps falls below the given tolerance".  Per Gaussian the
+    order is the smallest k >= 8 with Eps(k) = |X0|_F rho^(k+1) / (1 - rho) <= tol (<= k_max);
+    with a tolerance every Gaussian already meets at k = 8 the render is unchanged bit for
+    bit, and a tighter tolerance raises k only where Eps was above it."""
+    import copy
+    from workloads import make_config
+    w = make_config("C4", N=300, res=24)
+    base = oracle.gaussian_forms(w)
+    live = (base["flags"].astype(int) & 5) == 0  # not dropped, not FAIL
+    assert np.all(base["k"][live] == 8)
+    eps8 = base["eps"][live]
+    # loose tolerance: k stays 8 and the image is identical
+    loose = copy.deepcopy(w)
+    loose.pose_box = dict(w.pose_box, k_tol=float(eps8.max()) * 2, k_max=32)
+    a = oracle.render_bounds(w)
+    b = oracle.render_bounds(loose)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # tight tolerance: Eps <= tol wherever k < k_max, k minimal, and only larger where needed
+    tol = float(np.quantile(eps8, 0.5))
+    tight = copy.deepcopy(w)
+    tight.pose_box = dict(w.pose_box, k_tol=tol, k_max=24)
+    g = oracle.gaussian_forms(tight)
+    k, eps, rho = g["k"][live], g["eps"][live], g["rho"][live]
+    assert np.all((k >= 8) & (k <= 24))
+    assert np.all((eps <= tol * (1 + 1e-12)) | (k == 24))
+    assert np.all((k == 8) | (eps / rho > tol * (1 - 1e-12)))  # Eps(k - 1) > tol
+    assert np.all(k[eps8 <= tol] == 8) and np.any(k > 8)
+    # a higher order never widens the remainder term (rho < 1)
+    assert np.all(g["eps"][live] <= base["eps"][live] * (1 + 1e-12))
