@@ -164,6 +164,11 @@ as_status as_subbox_count(as_ctx* ctx, int32_t* n_sub);
  * running only the per-Gaussian setup; fails is host int64[n >= number of sub-boxes].  The
  * Python driver `paper_2503_00308_b200.refine` bisects failing sub-boxes with these counts. */
 as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds);
+/* Adaptive MatrixInv order (PAPER.md:470 (3): "increase k until Eps falls below the given
+ * tolerance"): with k_tol > 0 every Gaussian uses the smallest k >= 8 whose remainder
+ * Eps = |X0|_F rho^(k+1) / (1 - rho) is <= k_tol, at most k_max (8..64); k_tol <= 0 restores the
+ * fixed k = 8.  Applies to subsequent renders. */
+as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max);
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
 
 /* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----

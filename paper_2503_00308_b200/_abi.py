@@ -97,6 +97,7 @@ def lib():
         "as_subbox_count": (i32, [P, P]),
         "as_set_subboxes": (i32, [P, i32, P]),
         "as_subbox_fails": (i32, [P, i32, P]),
+        "as_set_matrixinv": (i32, [P, C.c_double, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -199,6 +199,9 @@ class Context:
         self.as_set_camera(w.camera)
         self.as_set_pose_box(w.pose_box)
         self.as_set_scene_box(w.scene_box)
+        self.as_set_matrixinv(w.pose_box.get("k_tol", 0.0), w.pose_box.get("k_max", 8))
+        if w.pose_box.get("subboxes") is not None:
+            self.as_set_subboxes(w.pose_box["subboxes"])
 
     # ------------------------------------------------------------------ render
     def _image_out(self, lo, hi, shape):
@@ -244,6 +247,10 @@ class Context:
             return
         b = np.ascontiguousarray(bounds, np.float64).reshape(-1, 9, 2)
         self._check(self._L.as_set_subboxes(self._ctx, b.shape[0], C.c_void_p(b.ctypes.data)))
+
+    def as_set_matrixinv(self, k_tol: float = 0.0, k_max: int = 8):
+        """Adaptive MatrixInv order: smallest k >= 8 with Eps <= k_tol (<= k_max); 0 = fixed 8."""
+        self._check(self._L.as_set_matrixinv(self._ctx, float(k_tol), int(k_max)))
 
     def as_subbox_fails(self):
         """MatrixInv FAIL count per sub-box of the current partition (setup only)."""

@@ -66,6 +66,8 @@ struct as_ctx {
   // explicit partition (as_set_subboxes): host copy [n][9][2] and its device mirror
   std::vector<double> sub_host;
   DevBuf subs;
+  double k_tol = 0.0;  // as_set_matrixinv (adaptive Taylor order)
+  int k_max = 8;
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
   as_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -275,6 +277,8 @@ void run_setup(as_ctx* ctx, const BoxInfo& bi, int s) {
   a.pair = ctx->pair.p;
   a.kkey = P<unsigned long long>(ctx->kkey);
   a.kval = P<int32_t>(ctx->kval);
+  a.k_tol = ctx->k_tol;
+  a.k_max = ctx->k_max;
   a.wsmax = P<unsigned long long>(ctx->counters) + 4;
   a.counters = P<unsigned long long>(ctx->counters);
   launch_setup(bi.n_vars, a, ctx->stream);
@@ -989,6 +993,17 @@ as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds) {
     ctx->sub_host.swap(saved);
     return e.st;
   }
+  return AS_OK;
+}
+
+as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max) {
+  if (!ctx) return AS_E_ARG;
+  if (!std::isfinite(k_tol) || (k_tol > 0 && (k_max < 8 || k_max > 64))) {
+    set_err(ctx, "as_set_matrixinv: k_tol finite, k_max in [8, 64] (got %g, %d)", k_tol, k_max);
+    return AS_E_ARG;
+  }
+  ctx->k_tol = k_tol > 0 ? k_tol : 0.0;
+  ctx->k_max = k_tol > 0 ? k_max : 8;
   return AS_OK;
 }
 

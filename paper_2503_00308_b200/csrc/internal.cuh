@@ -225,6 +225,8 @@ struct SetupArgs {
   int32_t* kval;              // [N] Gaussian index
   unsigned long long* wsmax;  // max over kept Gaussians of w+S (as ordered bits)
   unsigned long long* counters;  // [4]: fails, straddles, dropped, spare
+  double k_tol;               // adaptive MatrixInv order (P:470 (3)): > 0 enables
+  int k_max;
 };
 
 void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st);

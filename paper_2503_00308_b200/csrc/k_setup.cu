@@ -322,6 +322,23 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
   }
   const double rho = sqrt(ss);
   if (!(rho < 1.0)) ok = false;  // Alg. 4 line 2
+  // Taylor order: k = 8 (G14), or adaptively the smallest k >= 8 with
+  // Eps(k) = |X0|_F rho^(k+1) / (1 - rho) <= k_tol, at most k_max (P:470 (3)); the decision
+  // uses the oracle's operation order without FMA contraction
+  int k_own = KTAYLOR;
+  if (A.k_tol > 0.0 && ok) {
+    const double nx = __dsqrt_rn(__dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(X0[0], X0[0]), __dmul_rn(X0[1], X0[1])), __dmul_rn(X0[2], X0[2])),
+        __dmul_rn(X0[3], X0[3])));
+    double r = 1.0;
+    for (int t = 0; t < KTAYLOR + 1; ++t) r = __dmul_rn(r, rho);
+    const double den = __dsub_rn(1.0, rho);
+    while (k_own < A.k_max && __ddiv_rn(__dmul_rn(nx, r), den) > A.k_tol) {
+      r = __dmul_rn(r, rho);
+      ++k_own;
+    }
+  }
+  const int k_warp = __reduce_max_sync(FULL, k_own);  // uniform trip count for the shuffles
   HL P[4], S[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -329,7 +346,8 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
     S[e] = E[e];
   }
 #pragma unroll 1
-  for (int it = 2; it <= KTAYLOR; ++it) {
+  for (int it = 2; it <= k_warp; ++it) {
+    const bool acc = it <= k_own;  // beyond this Gaussian's order: computed, not summed
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       HL q0{0.0, 0.0}, q1{0.0, 0.0};  // row a of P^it = P^{it-1} E (O5)
@@ -347,15 +365,17 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
       }
       P[2 * a + 0] = q0;
       P[2 * a + 1] = q1;
-      S[2 * a + 0].l += q0.l;
-      S[2 * a + 0].u += q0.u;
-      S[2 * a + 1].l += q1.l;
-      S[2 * a + 1].u += q1.u;
+      if (acc) {
+        S[2 * a + 0].l += q0.l;
+        S[2 * a + 0].u += q0.u;
+        S[2 * a + 1].l += q1.l;
+        S[2 * a + 1].u += q1.u;
+      }
     }
   }
   const double nx0 = sqrt(X0[0] * X0[0] + X0[1] * X0[1] + X0[2] * X0[2] + X0[3] * X0[3]);
   const double rs = ok ? rho : 0.0;
-  const double eps = nx0 * pow(rs, (double)(KTAYLOR + 1)) / (1.0 - rs);
+  const double eps = nx0 * pow(rs, (double)(k_own + 1)) / (1.0 - rs);
   HL conic[4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)

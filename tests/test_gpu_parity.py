@@ -243,3 +243,18 @@ def test_opacity_box_parity(ctx, oracle):
     err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
     assert err <= TOL, err
     assert st["pairs"] == ost["pairs"] and st["active_pairs"] == ost["active_pairs"]
+
+
+def test_adaptive_taylor_order_parity(ctx, oracle):
+    """as_set_matrixinv (P:470 (3)): with a tolerance that raises k for about half of the
+    Gaussians, the GPU render matches the oracle's adaptive-k render within 1e-4."""
+    w = make_config("C4", **SMALL["C4"])
+    g = oracle.gaussian_forms(w)
+    live = (g["flags"].astype(int) & 5) == 0
+    w.pose_box = dict(w.pose_box, k_tol=float(np.quantile(g["eps"][live], 0.5)), k_max=24)
+    lo, hi, st = gpu_render(ctx, w)
+    olo, ohi, ost = oracle.render_bounds(w)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= TOL, err
+    assert st["fails"] == ost["fails"]
+    ctx.as_set_matrixinv(0.0)
