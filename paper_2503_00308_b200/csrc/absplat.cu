@@ -56,7 +56,7 @@ struct as_ctx {
   DevBuf nF, nG, ntot, eoff, exc, hpos, gpos, diff, cover, pflag, is_store, slot, scratch;
   DevBuf tileh, tilemax, wsP, kapP, posD;
   DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
-  DevBuf finkey, finkey2, finval, finval2, fin_b, fin_e, finrec, maskF, maskG;
+  DevBuf finkey, finkey2, finval, finval2, finstart, finrec, maskF, maskG;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
   size_t bytes = 0;
   int64_t launches = 0;
@@ -526,19 +526,19 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ensure(ctx, ctx->finkey2, sizeof(uint32_t) * M);
       ensure(ctx, ctx->finval, sizeof(int32_t) * M);
       ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
-      ensure(ctx, ctx->fin_b, sizeof(int32_t) * (M + 1));
+      ensure(ctx, ctx->finstart, sizeof(int32_t) * (M + 1));
       ensure(ctx, ctx->finrec, sizeof(FinRec) * M);
       launch_meta(pa, cstore, ccut, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
                   P<int32_t>(ctx->finval), st);
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
                       P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
-      launch_fin_start(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->fin_b), st);
+      launch_fin_start(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->finstart), st);
       LAUNCHED(ctx, 1);
       launch_finrec(P<uint32_t>(ctx->finkey2), P<int32_t>(ctx->finval2), pa, P<int4>(ctx->pflag),
                     P<ulonglong2>(ctx->maskG), ctx->hot.p, P<FinRec>(ctx->finrec), st);
       LAUNCHED(ctx, 1);
-      ta.finstart = P<int32_t>(ctx->fin_b);
+      ta.finstart = P<int32_t>(ctx->finstart);
       ta.fin_rec = P<FinRec>(ctx->finrec);
       ta.mF = P<ulonglong2>(ctx->maskF);
       unsigned int hw = 0;
@@ -854,7 +854,7 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->tilemax, &ctx->wsP, &ctx->kapP, &ctx->posD, &ctx->item_off, &ctx->items, &ctx->items2,
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
-                    &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->fin_b, &ctx->fin_e, &ctx->finrec, &ctx->maskF,
+                    &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->finstart, &ctx->finrec, &ctx->maskF,
                     &ctx->maskG};
   for (DevBuf* b : bufs) release(ctx, *b);
   for (int k = 0; k < 8; ++k)
