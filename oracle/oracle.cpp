@@ -833,6 +833,74 @@ void blend_direct(const SubData& S, const std::vector<int64_t>& L, const double*
   }
 }
 
+// ---------------------------------------------------------------- NEXT-1: linear blend
+// Effective opacity as an affine form (Alg. 1 l.10 with the linear relations kept):
+// z = -s/2 from the s forms of steps 14-16; Table 2's Exp relaxation (R3) kept linear:
+// lower = tangent at z_lo, e^{z_lo} (1 + z - z_lo), applied to z's lower form; upper = chord
+// over [z_lo, z_hi] (slope m = (e^{z_hi} - e^{z_lo}) / (z_hi - z_lo) >= 0; e^{z_hi} at zero
+// width), applied to z's upper form; times [o_lo, o_hi] >= 0.  FAIL: [0, o_hi]; straddle:
+// lower 0.  Returns false when culled at u (a = 0).
+bool opacity_form(const GRec& G, const double u[2], int n, Form& a) {
+  if (culled(G, u[0], u[0], u[1], u[1])) return false;
+  if (G.flags & GF_FAIL) {
+    a = constant(0.0);
+    a.hi.b = G.o_hi;
+    return true;
+  }
+  Form x[2];
+  for (int c = 0; c < 2; ++c) x[c] = add(scale(G.D2, u[c]), scale(G.DU[c], -1.0));
+  Form sf = constant(0.0);
+  for (int c = 0; c < 3; ++c) {
+    Form q = add(mul(x[0], G.W[0][c], n), mul(x[1], G.W[1][c], n));
+    sf = add(sf, sq(q, n));
+  }
+  double sl, sh;
+  conc(sf, n, sl, sh);
+  sl = std::max(sl, 0.0);
+  const Form z = scale(sf, -0.5);  // z.lo = -s.hi / 2, z.hi = -s.lo / 2
+  const double zl = -0.5 * sh, zh = -0.5 * sl;
+  const double el = std::exp(zl), eh = std::exp(zh);
+  const double m = (zh > zl) ? (eh - el) / (zh - zl) : eh;
+  const Form lower = add_const(scale(z, G.o_lo * el), G.o_lo * el * (1.0 - zl));
+  const Form upper = add_const(scale(z, G.o_hi * m), G.o_hi * (el - m * zl));
+  a.lo = lower.lo;
+  a.hi = upper.hi;
+  if (G.flags & GF_STRADDLE) a.lo = aff_zero();
+  return true;
+}
+
+// BlendInd (Alg. 3) with linear relations along the sorted fold, for a tile list
+// whose pairs are all certain (then F(i) = before(i) and the fold is a prefix):
+// T_0 = 1, pc_c += Mul(T_i, a_i) c_i (R1; c in [c_lo, c_hi] >= 0 scales the lower / upper
+// form), T_{i+1} = Mul(T_i, 1 - a_i) (R1).  Culled Gaussians (a = 0) are skipped.
+void blend_linear(const SubData& S, const std::vector<int64_t>& L, const std::vector<char>& act,
+                  const std::vector<Form>& a, double pc_lo[3], double pc_hi[3]) {
+  const int n = S.B.n;
+  Form T = constant(1.0);
+  Form pc[3] = {constant(0.0), constant(0.0), constant(0.0)};
+  for (size_t p = 0; p < L.size(); ++p) {
+    if (!act[p]) continue;
+    const GRec& G = S.G[L[p]];
+    const Form ta = mul(T, a[p], n);
+    for (int c = 0; c < 3; ++c) {
+      Form t;
+      t.lo = aff_scale(ta.lo, G.c_lo[c]);
+      t.hi = aff_scale(ta.hi, G.c_hi[c]);
+      pc[c] = add(pc[c], t);
+    }
+    Form om;  // 1 - a
+    om.lo = aff_scale(a[p].hi, -1.0);
+    om.lo.b += 1.0;
+    om.hi = aff_scale(a[p].lo, -1.0);
+    om.hi.b += 1.0;
+    T = mul(T, om, n);
+  }
+  for (int c = 0; c < 3; ++c) {
+    pc_lo[c] = aff_min(pc[c].lo, n);
+    pc_hi[c] = aff_max(pc[c].hi, n);
+  }
+}
+
 // steps 20-21 finalise (union step 22 by the caller)
 inline void finalise(double N, double pc_lo[3], double pc_hi[3]) {
   for (int c = 0; c < 3; ++c) {
@@ -885,7 +953,7 @@ int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, i
     for (size_t ti = 0; ti < tiles.size(); ++ti) {
       int tile = tiles[ti];
       TileList T;
-      build_tile_list(P, S, ts, tile, mode == 0, T);
+      build_tile_list(P, S, ts, tile, mode != 1, T);
       const int K = (int)T.L.size();
       pairs += K;
       unc += T.uncertain;
@@ -899,11 +967,25 @@ int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, i
           double u[2] = {px + 0.5, py + 0.5};
           for (int p = 0; p < K; ++p) active += opacity_bounds(S.G[T.L[p]], u, S.B.n, alo[p], ahi[p]);
           double pl[3], ph[3];
-          if (mode == 0)
-            blend_windowed(S, T, alo.data(), ahi.data(), pl, ph);
-          else
+          if (mode == 1)
             blend_direct(S, T.L, alo.data(), ahi.data(), pl, ph);
+          else
+            blend_windowed(S, T, alo.data(), ahi.data(), pl, ph);
           finalise((double)P.N, pl, ph);
+          if (mode == 2 && T.uncertain == 0) {
+            // NEXT-1: linear-relation blend on exception-free lists, intersected with the
+            // interval blend (both sound)
+            std::vector<char> act(K);
+            std::vector<Form> af(K);
+            for (int p = 0; p < K; ++p) act[p] = opacity_form(S.G[T.L[p]], u, S.B.n, af[p]);
+            double ql[3], qh[3];
+            blend_linear(S, T.L, act, af, ql, qh);
+            finalise((double)P.N, ql, qh);
+            for (int c = 0; c < 3; ++c) {
+              pl[c] = std::max(pl[c], ql[c]);
+              ph[c] = std::min(ph[c], qh[c]);
+            }
+          }
           size_t o = 3 * ((size_t)py * C.W + px);
           for (int c = 0; c < 3; ++c) {
             if (s == sb0) {
@@ -1123,7 +1205,7 @@ int or_render_bounds(int64_t N, const float* mean, const float* chol, const floa
                      double* lo, double* hi, or_stats* stats) {
   Problem P;
   if (setup_problem(P, N, mean, chol, opacity, color, cam, box, sbox) != 0) return -1;
-  if (tile < 1 || (mode != 0 && mode != 1) || !lo || !hi) return -1;
+  if (tile < 1 || mode < 0 || mode > 2 || !lo || !hi) return -1;
   set_threads(nthreads);
   int ntx = (cam->W + tile - 1) / tile, nty = (cam->H + tile - 1) / tile;
   std::vector<int> tiles(ntx * nty);

@@ -76,7 +76,9 @@ typedef struct {
 
 /* Abstract render.  lo/hi: [H][W][3] doubles.
  * mode 0 = windowed blend (prefix products + exception windows, step 13 order structure),
- * mode 1 = direct blend (Ind recomputed for every pair at every pixel, Alg. 3 literal).
+ * mode 1 = direct blend (Ind recomputed for every pair at every pixel, Alg. 3 literal),
+ * mode 2 = mode 0 intersected, on tiles whose pairs are all certain, with BlendInd evaluated
+ *          with linear relations along the sorted fold.
  * nthreads <= 0: OpenMP default.  Returns 0 on success, <0 on argument error. */
 int or_render_bounds(int64_t N, const float* mean, const float* chol, const float* opacity,
                      const float* color, const or_camera* cam, const or_pose_box* box,

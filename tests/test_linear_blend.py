@@ -1,0 +1,97 @@
+"""NEXT-1: BlendInd evaluated with linear relations along the sorted fold
+(Alg. 3; §3.3 (4)), on tile lists whose pairs are all certain, intersected
+with the interval blend (oracle mode 2).  Pins: zero-width boxes reproduce the concrete render;
+one Gaussian reproduces the interval blend (the Exp tangent / chord concretise to the interval
+bounds); sampled and brute-force containment (Theorem 1); the result lies inside the interval
+blend's and is strictly tighter on C1; tiles with uncertain pairs keep the interval blend."""
+import copy
+
+import numpy as np
+import pytest
+
+from tests import helpers as H
+from workloads import make_config
+
+TAU = 1e-12
+
+
+def zero_box(w):
+    w = copy.deepcopy(w)
+    for k in ("eps_t", "eps_R", "t_off", "R_off"):
+        w.pose_box[k] = [0.0, 0.0, 0.0]
+    if w.scene_box is not None:
+        w.scene_box = dict(w.scene_box, shift_hi=np.array(w.scene_box["shift_lo"], float))
+    return w
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_zero_width_box_is_concrete(oracle, name):
+    w = zero_box(make_config(name, **({} if name == "C1" else dict(N=1500, res=32))))
+    lo, hi, st = oracle.render_bounds(w, mode=2)
+    ref = oracle.render_concrete(w)
+    slack = w.N * TAU + 1e-12
+    assert np.abs(lo - ref).max() <= slack and np.abs(hi - ref).max() <= slack
+
+
+def test_single_gaussian_equals_interval(oracle):
+    w = make_config("C1", N=1, res=16)
+    w.pose_box["eps_t"] = [0.05, 0.03, 0.0]
+    a = oracle.render_bounds(w, mode=0)
+    b = oracle.render_bounds(w, mode=2)
+    assert max(np.abs(a[0] - b[0]).max(), np.abs(a[1] - b[1]).max()) <= 1e-12
+
+
+@pytest.mark.parametrize("name,nrand", [("C1", 150), ("C2", 30), ("C5", 30)])
+def test_containment_and_inside_interval(oracle, name, nrand):
+    w = make_config(name, **({} if name == "C1" else dict(N=2000, res=40)))
+    ilo, ihi, ist = oracle.render_bounds(w, mode=0)
+    lo, hi, st = oracle.render_bounds(w, mode=2)
+    assert np.all(lo >= ilo) and np.all(hi <= ihi) and np.all(lo <= hi)
+    rng = np.random.default_rng(8)
+    worst = 0.0
+    for p in H.sample_params(w, rng, n_random=nrand, corners=True):
+        e, t, shifts = H.pose_of(w, p)
+        col = None
+        if w.scene_box is not None and w.scene_box["col_lo"] is not None:
+            a = rng.uniform(size=(w.N, 1))
+            col = (w.scene_box["col_lo"] + a * (w.scene_box["col_hi"] - w.scene_box["col_lo"]))
+            col = col.astype(np.float32)
+        img = oracle.render_concrete(w, euler=e, t=t, shifts=shifts, color=col)
+        worst = max(worst, (lo - img).max(), (img - hi).max())
+    assert worst <= 1e-9, worst
+
+
+def test_c1_brute_force_and_tighter(oracle):
+    w = make_config("C1")
+    lo, hi, _ = oracle.render_bounds(w, mode=2)
+    ilo, ihi, _ = oracle.render_bounds(w, mode=0)
+    env_lo = np.full_like(lo, np.inf)
+    env_hi = np.full_like(hi, -np.inf)
+    for tx in np.linspace(-0.01, 0.01, 4001):
+        img = oracle.render_concrete(w, t=[tx, 0.0, 0.0])
+        np.minimum(env_lo, img, out=env_lo)
+        np.maximum(env_hi, img, out=env_hi)
+    assert np.all(lo <= env_lo + 1e-12) and np.all(env_hi <= hi + 1e-12)
+    assert H.mpg(lo, hi) < 0.9 * H.mpg(ilo, ihi)  # the fold keeps the pose correlations
+
+
+def test_uncertain_tiles_keep_interval_blend(oracle):
+    """Tiles whose list has an uncertain pair keep the interval blend exactly; the others may
+    only tighten."""
+    w = make_config("C4", N=2000, res=48)
+    a = oracle.render_bounds(w, mode=0)
+    b = oracle.render_bounds(w, mode=2)
+    ts = w.tile
+    ntx = -(-48 // ts)
+    n_unc = 0
+    for t in range(ntx * ntx):
+        unc = oracle.render_tiles(w, [t])[2]["uncertain_pairs"]
+        ys = slice((t // ntx) * ts, (t // ntx + 1) * ts)
+        xs = slice((t % ntx) * ts, (t % ntx + 1) * ts)
+        if unc > 0:
+            n_unc += 1
+            assert np.array_equal(a[0][ys, xs], b[0][ys, xs])
+            assert np.array_equal(a[1][ys, xs], b[1][ys, xs])
+        else:
+            assert np.all(b[0][ys, xs] >= a[0][ys, xs]) and np.all(b[1][ys, xs] <= a[1][ys, xs])
+    assert n_unc > 0
