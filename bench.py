@@ -235,6 +235,8 @@ def run_ours(args):
     H, W = w.camera["H"], w.camera["W"]
     ctx = Context(dev)
     ctx.load_workload(w)
+    if args.blend == "linear":
+        ctx.as_set_blend(1)
     lo = torch.empty((H, W, 3), dtype=torch.float32, device=f"cuda:{dev}")
     hi = torch.empty_like(lo)
     shard = args.shard
@@ -401,7 +403,7 @@ def run_ours(args):
                           "res": f"{W}x{H}", "n_vars": n, "sub_boxes": P, "tile": tile,
                           "batch": batch, "setup_dtype": "f64",
                           "l2": "flushed before every timed step (512 MiB write)",
-                          "parallelism": parallelism},
+                          "parallelism": parallelism, "blend": args.blend},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": gpu_launches, "launch_kernels": names, "clocks": clocks,
                "bound_width": widths,
@@ -425,6 +427,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--blend", default="interval", choices=["interval", "linear"],
+                    help="linear: + linear-relation BlendInd on exception-free tiles (NEXT-1)")
     ap.add_argument("--shard", default="auto", choices=["auto", "tiles", "subboxes"],
                     help="multi-GPU axis: image tiles (all-gather) or sub-box ranges "
                          "(all-reduce min/max); auto = sub-boxes when P >= world")

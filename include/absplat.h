@@ -171,6 +171,16 @@ as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds);
 as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max);
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
 
+/* ---- blend mode ----
+ * mode 0 (default): the interval blend (reading O7).  mode 1: additionally, on tiles whose
+ * Gaussian list has no uncertain depth pair, BlendInd is evaluated with linear relations
+ * along the sorted fold (a = o Exp(-s/2) with Table 2's tangent / chord kept linear in the box
+ * variables, T and pc as affine forms through McCormick products, Alg. 3) and the
+ * result is intersected with the interval bounds, per sub-box, before the union.  Supported
+ * for boxes with at most 3 variables and full-image renders (as_render_bounds /
+ * as_render_subboxes); AS_E_ARG otherwise. */
+as_status as_set_blend(as_ctx* ctx, int32_t mode);
+
 /* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----
  * Every rank holds the full scene and runs the per-Gaussian setup; image tiles are
  * assigned to ranks by a deterministic longest-processing-time rule over per-tile Gaussian

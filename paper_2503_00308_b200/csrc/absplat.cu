@@ -68,6 +68,10 @@ struct as_ctx {
   DevBuf subs;
   double k_tol = 0.0;  // as_set_matrixinv (adaptive Taylor order)
   int k_max = 8;
+  int blend_mode = 0;  // as_set_blend: 0 interval, 1 + linear on exception-free tiles
+  bool last_has_exc = false;
+  int64_t last_M = 0;
+  DevBuf tmp_lo, tmp_hi, tile_unc, lin_tiles;
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
   as_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -383,6 +387,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
                    const int32_t* tslot, float* lo, float* hi, bool first, int64_t& pairs_out,
                    PhaseTimes* pt) {
   cudaStream_t st = ctx->stream;
+  ctx->last_has_exc = false;
   const int64_t N = ctx->N;
   const int nv = bi.n_vars;
   unsigned long long* ctr = P<unsigned long long>(ctx->counters);
@@ -548,6 +553,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ctx->max_window = std::max(ctx->max_window, (int)hw);
       ctx->last_wmax = (int)hw;
       has_exc = true;
+      ctx->last_has_exc = true;
       ta.pm = P<int4>(ctx->pflag);
       ta.nG = P<int32_t>(ctx->nG);
       ta.eoff = P<int64_t>(ctx->eoff);
@@ -843,7 +849,7 @@ as_status as_destroy(as_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->group_of,
-                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->subs, &ctx->pose, &ctx->hot,
+                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->tile_unc, &ctx->lin_tiles, &ctx->pose, &ctx->hot,
                     &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
                     &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
@@ -993,6 +999,16 @@ as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds) {
     ctx->sub_host.swap(saved);
     return e.st;
   }
+  return AS_OK;
+}
+
+as_status as_set_blend(as_ctx* ctx, int32_t mode) {
+  if (!ctx) return AS_E_ARG;
+  if (mode != 0 && mode != 1) {
+    set_err(ctx, "as_set_blend: mode 0 (interval) or 1 (interval + linear)");
+    return AS_E_ARG;
+  }
+  ctx->blend_mode = mode;
   return AS_OK;
 }
 
@@ -1150,6 +1166,46 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
 }
 
 namespace {
+// NEXT-1: after the interval render of one sub-box into (lo, hi), intersect the exception-free
+// tiles with the linear-relation blend
+void linear_pass(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int batch, float* lo,
+                 float* hi) {
+  cudaStream_t st = ctx->stream;
+  const int64_t M = ctx->last_M;
+  ensure(ctx, ctx->tile_unc, sizeof(int32_t) * G.ntiles);
+  ensure(ctx, ctx->lin_tiles, sizeof(int32_t) * G.ntiles);
+  CK(cudaMemsetAsync(ctx->tile_unc.p, 0, sizeof(int32_t) * G.ntiles, st));
+  if (ctx->last_has_exc)
+    launch_tile_unc(P<int4>(ctx->pflag), P<uint32_t>(ctx->keys2), M, P<int32_t>(ctx->tile_unc), st);
+  std::vector<int32_t> unc(G.ntiles);
+  std::vector<int64_t> tb(G.ntiles), te(G.ntiles);
+  CK(cudaMemcpyAsync(unc.data(), ctx->tile_unc.p, sizeof(int32_t) * G.ntiles,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(tb.data(), ctx->tbegin.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(te.data(), ctx->tend.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int32_t> list;
+  for (int t = 0; t < G.ntiles; ++t)
+    if (!unc[t] && te[t] > tb[t]) list.push_back(t);
+  if (list.empty()) return;
+  CK(cudaMemcpyAsync(ctx->lin_tiles.p, list.data(), sizeof(int32_t) * list.size(),
+                     cudaMemcpyHostToDevice, st));
+  TileArgs ta{};
+  ta.hot = ctx->hot.p;
+  ta.vals = P<int32_t>(ctx->vals2);
+  ta.tbegin = P<int64_t>(ctx->tbegin);
+  ta.tend = P<int64_t>(ctx->tend);
+  ta.ts = G.ts;
+  ta.ntx = G.ntx;
+  ta.W = ctx->cam.W;
+  ta.H = ctx->cam.H;
+  ta.bs = std::min(batch, 16);
+  ta.ntau = (float)((double)ctx->N * TAU);
+  launch_tile_lin(bi.n_vars, ta, P<int32_t>(ctx->lin_tiles), (int)list.size(), lo, hi, st);
+  LAUNCHED(ctx, 1);
+  CK(cudaStreamSynchronize(st));  // list (host) must outlive the copy above
+}
+
 __global__ void k_fill2(float* a, float va, float* b, float vb, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -1203,6 +1259,11 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
     return AS_E_ARG;
   }
   if ((st = check_tile_args(ctx, tile, batch, bi.n_vars)) != AS_OK) return st;
+  if (ctx->blend_mode == 1 && bi.n_vars > NV_LINEAR_MAX) {
+    set_err(ctx, "linear blend supports boxes with at most %d variables (got %d)", NV_LINEAR_MAX,
+            bi.n_vars);
+    return AS_E_ARG;
+  }
   if ((flags & AS_ASYNC) && !(flags & AS_PTR_DEVICE)) {
     set_err(ctx, "AS_ASYNC requires device outputs");
     return AS_E_ARG;
@@ -1231,10 +1292,26 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       k_fill2<<<(unsigned)((img + 255) / 256), 256, 0, s>>>(dlo, 1.f, dhi, 0.f, (int64_t)img);
       LAUNCHED(ctx, 1);
     }
+    const bool linear = ctx->blend_mode == 1;
+    if (linear) {
+      ensure(ctx, ctx->tmp_lo, sizeof(float) * img);
+      ensure(ctx, ctx->tmp_hi, sizeof(float) * img);
+    }
     for (int sb = s0; sb < s1; ++sb) {
       int64_t M = 0;
-      render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                    nullptr, dlo, dhi, sb == s0, M, stats ? &pt : nullptr);
+      if (!linear) {
+        render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
+                      nullptr, dlo, dhi, sb == s0, M, stats ? &pt : nullptr);
+      } else {  // intersection per sub-box, then the union (step 22)
+        float* tl = P<float>(ctx->tmp_lo);
+        float* th = P<float>(ctx->tmp_hi);
+        render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
+                      nullptr, tl, th, true, M, stats ? &pt : nullptr);
+        ctx->last_M = M;
+        linear_pass(ctx, bi, G, batch, tl, th);
+        launch_union(tl, th, dlo, dhi, (int64_t)img, sb == s0, s);
+        LAUNCHED(ctx, 1);
+      }
       pairs += M;
     }
     if (!(flags & AS_PTR_DEVICE)) {
@@ -1305,6 +1382,10 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
   if ((st = check_tile_args(ctx, tile, batch, bi.n_vars)) != AS_OK) return st;
   if (world < 1 || rank < 0 || rank >= world || !lo_tm || !hi_tm || !owned || !n_owned) {
     set_err(ctx, "as_render_shard: bad arguments");
+    return AS_E_ARG;
+  }
+  if (ctx->blend_mode != 0) {
+    set_err(ctx, "as_render_shard: the linear blend is available for full-image renders only");
     return AS_E_ARG;
   }
   try {

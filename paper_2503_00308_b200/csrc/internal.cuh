@@ -341,6 +341,14 @@ struct TileArgs {
 };
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st);
 void launch_merge(const TileArgs& a, cudaStream_t st);
+// NEXT-1 linear blend (n <= 3): intersect exception-free tiles' bounds in lo / hi
+constexpr int NV_LINEAR_MAX = 3;
+void launch_tile_lin(int nv, const TileArgs& a, const int32_t* tiles, int n_tiles, float* lo,
+                     float* hi, cudaStream_t st);
+void launch_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc,
+                     cudaStream_t st);
+void launch_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n, bool first,
+                  cudaStream_t st);
 int tile_threads(int ts);
 int tile_subblocks(int ts);
 int tile_grid(int nv, int ts, int bs);

@@ -230,6 +230,88 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
   alo = R.o[0] * exp2f(-LOG2E_HALF * smax);
   ahi = R.o[1] * exp2f(-LOG2E_HALF * smin);
 }
+
+// steps 14-16 for one pixel, keeping s's lower / upper forms (NEXT-1 linear blend)
+template <int NV>
+__device__ __forceinline__ void opacity_sforms(const SRec<NV>& R, float du0, float du1,
+                                               float (&sl)[NV + 1], float (&sh)[NV + 1]) {
+  constexpr int C = NV + 1;
+  float x0 = fmaf(du0, R.d2lo[NV], R.xb[0][NV]);
+  float x1 = fmaf(du1, R.d2lo[NV], R.xb[1][NV]);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    x0 -= fabsf(fmaf(du0, R.d2lo[k], R.xb[0][k]));
+    x1 -= fabsf(fmaf(du1, R.d2lo[k], R.xb[1][k]));
+  }
+  const float ax0 = fabsf(x0), ax1 = fabsf(x1);
+#pragma unroll
+  for (int k = 0; k < C; ++k) sl[k] = sh[k] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float ql[C], qh[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      float m = fmaf(du0, R.q0m[c][k], R.pm[c][k]);
+      m = fmaf(du1, R.q1m[c][k], m);
+      m = fmaf(x0, R.wm0[c][k], m);
+      m = fmaf(x1, R.wm1[c][k], m);
+      float r = fmaf(du0, R.q0r[c][k], R.pr[c][k]);
+      r = fmaf(du1, R.q1r[c][k], r);
+      r = fmaf(ax0, R.wr0[c][k], r);
+      r = fmaf(ax1, R.wr1[c][k], r);
+      if (k == NV) {
+        m = fmaf(-x0, R.wcm[c], m);
+        m = fmaf(-x1, R.wcm[3 + c], m);
+        r = fmaf(x0, R.wcd[c], r);
+        r = fmaf(x1, R.wcd[3 + c], r);
+      }
+      ql[k] = m - r;
+      qh[k] = m + r;
+    }
+    float qmin = ql[NV], qmax = qh[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      qmin -= fabsf(ql[k]);
+      qmax += fabsf(qh[k]);
+    }
+    const float p = fminf(fmaxf(0.f, qmin), qmax);
+    const float tp = 2.f * p, sm = qmin + qmax;
+    const bool pa = tp >= 0.f, pb = sm >= 0.f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      sl[k] = fmaf(tp, pa ? ql[k] : qh[k], sl[k]);
+      sh[k] = fmaf(sm, pb ? qh[k] : ql[k], sh[k]);
+    }
+    sl[NV] -= p * p;
+    sh[NV] -= qmin * qmax;
+  }
+}
+
+// R1 McCormick product of two forms given as (lo[C], hi[C]) coefficient arrays (slopes then
+// constant), fp32: out = mul(f, g) with the fixed planes of reading G1
+template <int NV>
+__device__ __forceinline__ void form_mul(const float (&fl)[NV + 1], const float (&fh)[NV + 1],
+                                         const float (&gl)[NV + 1], const float (&gh)[NV + 1],
+                                         float (&ol)[NV + 1], float (&oh)[NV + 1]) {
+  float xl = fl[NV], xh = fh[NV], yl = gl[NV], yh = gh[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    xl -= fabsf(fl[k]);
+    xh += fabsf(fh[k]);
+    yl -= fabsf(gl[k]);
+    yh += fabsf(gh[k]);
+  }
+  // lower = LS(f, y_lo) + LS(g, x_lo) - x_lo y_lo ; upper = US(f, y_hi) + US(g, x_lo) - x_lo y_hi
+#pragma unroll
+  for (int k = 0; k <= NV; ++k) {
+    const float lf = yl >= 0.f ? fl[k] : fh[k], lg = xl >= 0.f ? gl[k] : gh[k];
+    const float uf = yh >= 0.f ? fh[k] : fl[k], ug = xl >= 0.f ? gh[k] : gl[k];
+    ol[k] = fmaf(yl, lf, xl * lg);
+    oh[k] = fmaf(yh, uf, xl * ug);
+  }
+  ol[NV] -= xl * yl;
+  oh[NV] -= xl * yh;
+}
 }  // namespace
 
 
@@ -708,6 +790,172 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
 }
 
+// ---------------------------------------------------------------- NEXT-1 linear blend
+// One CTA per (exception-free tile, 8x8 block), one thread per pixel: BlendInd with linear
+// relations along the sorted fold (Alg. 3; oracle blend_linear):
+//   a = o Exp(-s/2) with Table 2's tangent (lower) / chord (upper) kept linear in xi,
+//   pc_c += Mul(T, a) c,  T <- Mul(T, 1 - a)   (R1 McCormick, fp32 forms),
+// finalised (+- N tau, clamp) and intersected with the interval bounds already in img.
+template <int NV>
+__global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tiles, int n_tiles,
+                                                 float* img_lo, float* img_hi) {
+  constexpr int SBX = 8, SBP = 64, C = NV + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ts = A.ts, nsb = ts / SBX, nsub = nsb * nsb;
+  const int BS = A.bs;
+  SRec<NV>* srec = reinterpret_cast<SRec<NV>*>(smem_raw);
+  double* cx2 = reinterpret_cast<double*>(srec + BS);
+  double* cy2 = cx2 + (size_t)BS * SBX;
+  const int w = blockIdx.x;
+  if (w >= n_tiles * nsub) return;
+  const int tile = tiles[w / nsub], sub = w % nsub;
+  const int pix = threadIdx.x, lx = pix & 7, ly = pix >> 3;
+  const float du0 = (float)lx + 0.5f - 0.5f * SBX, du1 = (float)ly + 0.5f - 0.5f * SBY;
+  const int tx = tile % A.ntx, ty = tile / A.ntx;
+  const int ox = tx * ts + (sub % nsb) * SBX, oy = ty * ts + (sub / nsb) * SBY;
+  const double ucx = ox + 0.5 * SBX, ucy = oy + 0.5 * SBY;
+  const bool in_img = (ox + lx < A.W) && (oy + ly < A.H);
+  const bool block_live = ox < A.W && oy < A.H;
+  const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + SBX), (double)A.W) - 0.5;
+  const double by0 = oy + 0.5, by1 = fmin((double)(oy + SBY), (double)A.H) - 0.5;
+  const int64_t tb = A.tbegin[tile];
+  const int K = (int)(A.tend[tile] - tb);
+  float Tl[C], Th[C], pl[3][C], ph[3][C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    Tl[k] = Th[k] = (k == NV) ? 1.f : 0.f;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pl[c][k] = ph[c][k] = 0.f;
+  }
+  for (int b0 = 0; b0 < K; b0 += BS) {
+    const int nb = min(BS, K - b0);
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < NPART * nb; jj += SBP) {
+      const int j = jj / NPART, part = jj % NPART;
+      const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
+      SRec<NV>& S = srec[j];
+      const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
+      const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
+      const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
+      const bool skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
+      if (part == NPART - 1) {
+        S.flags = H->flags | (skip ? F_SKIP : 0);
+        S.r2 = H->r2;
+        S.o[0] = H->o[0];
+        S.o[1] = H->o[1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          S.clo[c] = H->clo[c];
+          S.chi[c] = H->chi[c];
+        }
+        if (!skip) {
+#pragma unroll
+          for (int l = 0; l < SBX; ++l) {
+            const double x = ox + l + 0.5, y = oy + l + 0.5;
+            const double ddx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+            const double ddy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+            cx2[j * SBX + l] = __dmul_rn(ddx, ddx);
+            cy2[j * SBY + l] = __dmul_rn(ddy, ddy);
+          }
+        }
+      }
+      if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+      const SRec<NV>& R = srec[j];
+      const int flags = R.flags;
+      if (flags & F_SKIP) continue;
+      const bool keep = in_img && !(__dadd_rn(cx2[j * SBX + lx], cy2[j * SBY + ly]) > R.r2);
+      if (!keep) continue;  // a = 0 at this pixel: T unchanged, no contribution
+      float al[C], ah[C];
+      if (flags & F_FAIL) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) al[k] = ah[k] = 0.f;
+        ah[NV] = R.o[1];
+      } else {
+        float sl[C], sh[C];
+        opacity_sforms<NV>(R, du0, du1, sl, sh);
+        float smin = sl[NV], smax = sh[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          smin -= fabsf(sl[k]);
+          smax += fabsf(sh[k]);
+        }
+        smin = fmaxf(smin, 0.f);
+        const float zl = -0.5f * smax, zh = -0.5f * smin;
+        const float el = expf(zl), eh = expf(zh);
+        const float m = zh > zl ? (eh - el) / (zh - zl) : eh;
+        const float cl = R.o[0] * el, ch = R.o[1] * m;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          al[k] = cl * (-0.5f * sh[k]);
+          ah[k] = ch * (-0.5f * sl[k]);
+        }
+        al[NV] = cl * (-0.5f * sh[NV] + 1.f - zl);
+        ah[NV] = R.o[1] * fmaf(m, -0.5f * sl[NV] - zl, el);
+        if (flags & F_STRADDLE) {
+#pragma unroll
+          for (int k = 0; k < C; ++k) al[k] = 0.f;
+        }
+      }
+      float tal[C], tah[C];
+      form_mul<NV>(Tl, Th, al, ah, tal, tah);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          pl[c][k] = fmaf(R.clo[c], tal[k], pl[c][k]);
+          ph[c][k] = fmaf(R.chi[c], tah[k], ph[c][k]);
+        }
+      float oml[C], omh[C];  // 1 - a
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        oml[k] = -ah[k];
+        omh[k] = -al[k];
+      }
+      oml[NV] += 1.f;
+      omh[NV] += 1.f;
+      float nl[C], nh[C];
+      form_mul<NV>(Tl, Th, oml, omh, nl, nh);
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        Tl[k] = nl[k];
+        Th[k] = nh[k];
+      }
+    }
+  }
+  if (!in_img) return;
+  const int64_t o = ((int64_t)(oy + ly) * A.W + (ox + lx)) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float l = pl[c][NV], h = ph[c][NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      l -= fabsf(pl[c][k]);
+      h += fabsf(ph[c][k]);
+    }
+    l = fminf(fmaxf(l - A.ntau, 0.f), 1.f);
+    h = fminf(fmaxf(h + A.ntau, 0.f), 1.f);
+    img_lo[o + c] = fmaxf(img_lo[o + c], l);
+    img_hi[o + c] = fminf(img_hi[o + c], h);
+  }
+}
+
+// tiles whose list has an uncertain pair (their bounds keep the interval blend)
+__global__ void k_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < M && (pm[p].x & (PM_EF | PM_EG))) unc[keys[p]] = 1;
+}
+// union of one sub-box image into the result (step 22): copy for the first sub-box
+__global__ void k_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n,
+                        int first) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  lo[i] = first ? slo[i] : fminf(lo[i], slo[i]);
+  hi[i] = first ? shi[i] : fmaxf(hi[i], shi[i]);
+}
+
 // front-to-back composition of a tile's chunks: pc = sum_k P(<A_k) S_k with
 // P(<A_{k+1}) = P(<A_k) R_k (R_k = chunk k's running product at A_{k+1})
 __global__ void k_merge(TileArgs A) {
@@ -831,6 +1079,34 @@ void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st) {
     default:
       break;
   }
+}
+
+template <int NV>
+static size_t smem_lin(int bs) {
+  return (size_t)bs * (sizeof(SRec<NV>) + 2 * 8 * sizeof(double));
+}
+void launch_tile_lin(int nv, const TileArgs& a, const int32_t* tiles, int n_tiles, float* lo,
+                     float* hi, cudaStream_t st) {
+  const int grid = n_tiles * (a.ts / 8) * (a.ts / 8);
+  if (grid <= 0) return;
+  switch (nv) {
+#define CASE(K)                                                                         \
+  case K:                                                                               \
+    k_tile_lin<K><<<grid, 64, smem_lin<K>(a.bs), st>>>(a, tiles, n_tiles, lo, hi);      \
+    break;
+    CASE(0) CASE(1) CASE(2) CASE(3)
+#undef CASE
+    default:
+      break;
+  }
+}
+void launch_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc,
+                     cudaStream_t st) {
+  if (M > 0) k_tile_unc<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(pm, keys, M, unc);
+}
+void launch_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n, bool first,
+                  cudaStream_t st) {
+  if (n > 0) k_union<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(slo, shi, lo, hi, n, first ? 1 : 0);
 }
 
 void launch_merge(const TileArgs& a, cudaStream_t st) {

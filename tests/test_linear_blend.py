@@ -95,3 +95,55 @@ def test_uncertain_tiles_keep_interval_blend(oracle):
         else:
             assert np.all(b[0][ys, xs] >= a[0][ys, xs]) and np.all(b[1][ys, xs] <= a[1][ys, xs])
     assert n_unc > 0
+
+
+# ------------------------------------------------------------------ GPU (through the C ABI)
+@pytest.fixture(scope="module")
+def gctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,kw,parts", [("C1", {}, 1), ("C2", dict(N=3000, res=48), 1),
+                                           ("C2", dict(N=3000, res=48), 2),
+                                           ("C5", dict(N=3000, res=48), 1)])
+def test_gpu_linear_blend_parity(gctx, oracle, name, kw, parts):
+    w = make_config(name, **kw)
+    if parts > 1:
+        w.pose_box["parts"] = [parts, 1, 1, 1, 1, 1]
+    gctx.load_workload(w)
+    gctx.as_set_blend(1)
+    try:
+        lo, hi, st = gctx.as_render_bounds(w.tile, w.batch)
+    finally:
+        gctx.as_set_blend(0)
+    ilo, ihi, _ = gctx.as_render_bounds(w.tile, w.batch)
+    lo, hi = lo.cpu().numpy().astype(np.float64), hi.cpu().numpy().astype(np.float64)
+    olo, ohi, ost = oracle.render_bounds(w, mode=2)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= 1e-4, err
+    il, ih = ilo.cpu().numpy(), ihi.cpu().numpy()
+    assert np.all(lo >= il) and np.all(hi <= ih)  # inside the interval bounds
+    if name == "C1":
+        assert H.mpg(lo, hi) < 0.9 * H.mpg(il, ih)
+
+
+@pytest.mark.gpu
+def test_gpu_linear_blend_limits(gctx):
+    from paper_2503_00308_b200 import AbsplatError
+    w = make_config("C3", N=2000, res=32)  # n = 4
+    gctx.load_workload(w)
+    gctx.as_set_blend(1)
+    try:
+        with pytest.raises(AbsplatError):
+            gctx.as_render_bounds(16, 16)
+    finally:
+        gctx.as_set_blend(0)
+    with pytest.raises(AbsplatError):
+        gctx.as_set_blend(2)
