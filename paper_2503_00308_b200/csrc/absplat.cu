@@ -1188,6 +1188,10 @@ void linear_pass(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int batch, f
   for (int t = 0; t < G.ntiles; ++t)
     if (!unc[t] && te[t] > tb[t]) list.push_back(t);
   if (list.empty()) return;
+  // longest lists first: blocks are scheduled roughly in launch order, so the long tiles do
+  // not form the tail
+  std::stable_sort(list.begin(), list.end(),
+                   [&](int32_t a, int32_t b) { return te[a] - tb[a] > te[b] - tb[b]; });
   CK(cudaMemcpyAsync(ctx->lin_tiles.p, list.data(), sizeof(int32_t) * list.size(),
                      cudaMemcpyHostToDevice, st));
   TileArgs ta{};
