@@ -391,7 +391,9 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   const int64_t N = ctx->N;
   const int nv = bi.n_vars;
   unsigned long long* ctr = P<unsigned long long>(ctx->counters);
-  // BS is a performance knob: clamp it to what fits in shared memory at this n
+  // BS is a performance knob: clamp it to what fits in shared memory at this n, and to 128
+  // (k_tile's 256-position skip ring covers a batch plus the 128 positions before it)
+  bs = std::min(bs, 128);
   while (bs > 1 && tile_smem_bytes(nv, G.ts, bs) > 96 * 1024) bs >>= 1;
   if (pt) CK(cudaEventRecord(ctx->ev[1], st));
   if (do_setup) {
