@@ -81,9 +81,13 @@ def test_parity_full_sampled(ctx, oracle, name):
     Wd, Hd = w.camera["W"], w.camera["H"]
     # random pixels + the brightest-gap pixels (where errors would show)
     gap = (hi - lo).sum(-1)
-    top = np.argsort(gap.reshape(-1))[-16:]
-    px = np.concatenate([rng.integers(0, Wd, 24), top % Wd])
-    py = np.concatenate([rng.integers(0, Hd, 24), top // Wd])
+    top = np.argsort(gap.reshape(-1))[-24:]
+    # random pixels, the widest-gap pixels and the image corners / last row and column
+    # (ragged tiles, chunk boundaries)
+    edge_x = np.array([0, Wd - 1, 0, Wd - 1, Wd // 2, Wd - 1])
+    edge_y = np.array([0, 0, Hd - 1, Hd - 1, Hd - 1, Hd // 2])
+    px = np.concatenate([rng.integers(0, Wd, 64), top % Wd, edge_x])
+    py = np.concatenate([rng.integers(0, Hd, 64), top // Wd, edge_y])
     olo, ohi = oracle.pixel_bounds(w, px, py)
     err = max(np.abs(lo[py, px] - olo).max(), np.abs(hi[py, px] - ohi).max())
     assert err <= TOL, (name, err)
