@@ -202,7 +202,10 @@ def count_launches(step):
         names = {}
         for e in prof.events():
             dt = getattr(e, "device_type", None)
-            if dt is not None and "CUDA" in str(dt) and not e.name.startswith(("Memcpy", "Memset")):
+            # the library's kernels (its own and the CUB sorts / scans it launches); not NCCL's
+            # collectives or torch's
+            if (dt is not None and "CUDA" in str(dt) and not e.name.startswith(("Memcpy", "Memset"))
+                    and "nccl" not in e.name.lower() and "at::" not in e.name):
                 n += 1
                 names[e.name] = names.get(e.name, 0) + 1
         return n, names
@@ -370,12 +373,13 @@ def run_ours(args):
 
     # ---- bound widths (metric part 2) and CPU baseline (rank 0, N=1)
     out = None
+    fin = sr.step(stats=False) if sr is not None else None  # collective: every rank takes part
     if rank == 0:
-        lo_np = lo.cpu().numpy().astype(np.float64) if sr is None else None
         if sr is not None:
-            a, b, _ = sr.step(stats=False)
-            lo_np, hi_np = a.cpu().numpy().astype(np.float64), b.cpu().numpy().astype(np.float64)
+            lo_np = fin[0].cpu().numpy().astype(np.float64)
+            hi_np = fin[1].cpu().numpy().astype(np.float64)
         else:
+            lo_np = lo.cpu().numpy().astype(np.float64)
             hi_np = hi.cpu().numpy().astype(np.float64)
         gap = np.linalg.norm(hi_np - lo_np, axis=-1)
         widths = {"mpg": float(gap.mean()), "xpg": float(gap.max()),
