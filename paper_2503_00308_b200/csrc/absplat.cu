@@ -39,6 +39,7 @@ struct as_ctx {
   // scene
   int64_t N = -1;
   DevBuf mean, chol, opacity, color;
+  DevBuf st_mean, st_chol, st_opacity, st_color;  // as_load_scene staging (validated, swapped)
   // scene box
   int n_groups = 0;
   double dir[3][3] = {};
@@ -367,7 +368,7 @@ __global__ void k_slot_map(const int32_t* list, int n, int32_t* slot_of_tile) {
 
 // counters layout (unsigned long long[16])
 enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6, C_UNC = 8,
-       C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_NCOUNTERS = 16 };
+       C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_SCENE = 12, C_NCOUNTERS = 16 };
 
 int64_t read_i64(as_ctx* ctx, const int64_t* dptr) {
   int64_t v = 0;
@@ -850,7 +851,8 @@ as_status as_destroy(as_ctx* ctx) {
   if (!ctx) return AS_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->group_of,
+  DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->st_mean,
+                    &ctx->st_chol, &ctx->st_opacity, &ctx->st_color, &ctx->group_of,
                     &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->tile_unc, &ctx->lin_tiles, &ctx->pose, &ctx->hot,
                     &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
@@ -883,6 +885,27 @@ as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, v
   return AS_OK;
 }
 
+namespace {
+// scene validation on the device: the smallest invalid Gaussian index and its reason
+// (1 mean / colour not finite or colour outside [0,1], 2 chol not finite, 3 chol diagonal
+// <= 0, 4 opacity outside [0,1]) packed as index * 8 + reason into an atomicMin
+__global__ void k_validate(int64_t N, const float* m, const float* c, const float* o,
+                           const float* col, unsigned long long* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int why = 0;
+  for (int k = 0; k < 3 && !why; ++k)
+    if (!isfinite(m[3 * i + k]) || !isfinite(col[3 * i + k]) || !(col[3 * i + k] >= 0.f) ||
+        !(col[3 * i + k] <= 1.f))
+      why = 1;
+  for (int k = 0; k < 6 && !why; ++k)
+    if (!isfinite(c[6 * i + k])) why = 2;
+  if (!why && (!(c[6 * i] > 0.f) || !(c[6 * i + 2] > 0.f) || !(c[6 * i + 5] > 0.f))) why = 3;
+  if (!why && (!(o[i] >= 0.f) || !(o[i] <= 1.f))) why = 4;
+  if (why) atomicMin(bad, (unsigned long long)i * 8ull + (unsigned long long)why);
+}
+}  // namespace
+
 as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* chol,
                         const float* opacity, const float* color, int32_t flags) {
   if (!ctx) return AS_E_ARG;
@@ -896,56 +919,50 @@ as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* 
   }
   try {
     cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
     const bool dev = flags & AS_PTR_DEVICE;
-    std::vector<float> hm, hc, ho, hcol;
-    const float *m = mean, *c = chol, *o = opacity, *col = color;
-    if (dev) {  // validate from a host copy
-      hm.resize(3 * N);
-      hc.resize(6 * N);
-      ho.resize(N);
-      hcol.resize(3 * N);
-      CK(cudaMemcpyAsync(hm.data(), mean, 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaMemcpyAsync(hc.data(), chol, 24 * N, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaMemcpyAsync(ho.data(), opacity, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaMemcpyAsync(hcol.data(), color, 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      m = hm.data();
-      c = hc.data();
-      o = ho.data();
-      col = hcol.data();
-    }
-    for (int64_t i = 0; i < N; ++i) {
-      for (int k = 0; k < 3; ++k)
-        if (!finite_f(m[3 * i + k]) || !finite_f(col[3 * i + k]) || !(col[3 * i + k] >= 0.f) ||
-            !(col[3 * i + k] <= 1.f)) {
-          set_err(ctx, "Gaussian %lld: mean/colour not finite or colour outside [0,1]", (long long)i);
-          return AS_E_SCENE;
-        }
-      for (int k = 0; k < 6; ++k)
-        if (!finite_f(c[6 * i + k])) {
-          set_err(ctx, "Gaussian %lld: chol not finite", (long long)i);
-          return AS_E_SCENE;
-        }
-      if (!(c[6 * i] > 0.f) || !(c[6 * i + 2] > 0.f) || !(c[6 * i + 5] > 0.f)) {
-        set_err(ctx, "Gaussian %lld: chol diagonal must be > 0", (long long)i);
-        return AS_E_SCENE;
-      }
-      if (!(o[i] >= 0.f) || !(o[i] <= 1.f)) {
-        set_err(ctx, "Gaussian %lld: opacity outside [0,1]", (long long)i);
-        return AS_E_SCENE;
-      }
-    }
-    ensure(ctx, ctx->mean, 12 * std::max<int64_t>(N, 1));
-    ensure(ctx, ctx->chol, 24 * std::max<int64_t>(N, 1));
-    ensure(ctx, ctx->opacity, 4 * std::max<int64_t>(N, 1));
-    ensure(ctx, ctx->color, 12 * std::max<int64_t>(N, 1));
+    // copy into staging buffers, validate there, and only then replace the scene (no partial
+    // writes on error)
+    DevBuf &sm = ctx->st_mean, &sc = ctx->st_chol, &so = ctx->st_opacity, &scol = ctx->st_color;
+    const size_t n1 = (size_t)std::max<int64_t>(N, 1);
+    ensure(ctx, sm, 12 * n1);
+    ensure(ctx, sc, 24 * n1);
+    ensure(ctx, so, 4 * n1);
+    ensure(ctx, scol, 12 * n1);
+    ensure(ctx, ctx->counters, sizeof(unsigned long long) * C_NCOUNTERS);
     const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (N > 0) {
-      CK(cudaMemcpyAsync(ctx->mean.p, mean, 12 * N, kind, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->chol.p, chol, 24 * N, kind, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->opacity.p, opacity, 4 * N, kind, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->color.p, color, 12 * N, kind, ctx->stream));
+    unsigned long long bad = ~0ull;
+    try {
+      if (N > 0) {
+        CK(cudaMemcpyAsync(sm.p, mean, 12 * N, kind, st));
+        CK(cudaMemcpyAsync(sc.p, chol, 24 * N, kind, st));
+        CK(cudaMemcpyAsync(so.p, opacity, 4 * N, kind, st));
+        CK(cudaMemcpyAsync(scol.p, color, 12 * N, kind, st));
+        unsigned long long* dbad = P<unsigned long long>(ctx->counters) + C_SCENE;
+        CK(cudaMemcpyAsync(dbad, &bad, sizeof bad, cudaMemcpyHostToDevice, st));
+        k_validate<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, P<float>(sm), P<float>(sc),
+                                                                 P<float>(so), P<float>(scol), dbad);
+        LAUNCHED(ctx, 1);
+        CK(cudaMemcpyAsync(&bad, dbad, sizeof bad, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+    } catch (const Err&) {
+      throw;
     }
+    if (bad != ~0ull) {
+      const long long gi = (long long)(bad >> 3);
+      switch ((int)(bad & 7)) {
+        case 1: set_err(ctx, "Gaussian %lld: mean/colour not finite or colour outside [0,1]", gi); break;
+        case 2: set_err(ctx, "Gaussian %lld: chol not finite", gi); break;
+        case 3: set_err(ctx, "Gaussian %lld: chol diagonal must be > 0", gi); break;
+        default: set_err(ctx, "Gaussian %lld: opacity outside [0,1]", gi); break;
+      }
+      return AS_E_SCENE;
+    }
+    std::swap(ctx->mean, sm);  // the previous scene becomes the next staging area
+    std::swap(ctx->chol, sc);
+    std::swap(ctx->opacity, so);
+    std::swap(ctx->color, scol);
     ctx->N = N;
     ctx->n_groups = 0;
     ctx->has_group = ctx->has_col = ctx->has_op = false;

@@ -262,3 +262,22 @@ def test_adaptive_taylor_order_parity(ctx, oracle):
     assert err <= TOL, err
     assert st["fails"] == ost["fails"]
     ctx.as_set_matrixinv(0.0)
+
+
+def test_invalid_scene_is_rejected_atomically(ctx):
+    """as_load_scene validates on the device; an invalid scene is rejected with AS_E_SCENE and
+    the previously loaded scene is kept."""
+    import torch
+    from paper_2503_00308_b200 import AbsplatError
+    w = make_config("C1")
+    ctx.load_workload(w)
+    lo0, hi0, _ = ctx.as_render_bounds(16, 16)
+    for field, idx, val in (("mean", (3, 1), np.nan), ("chol", (5, 2), -1.0),
+                            ("opacity", (7,), 1.5), ("color", (2, 0), -0.1)):
+        bad = {k: getattr(w, k).copy() for k in ("mean", "chol", "opacity", "color")}
+        bad[field][idx] = val
+        with pytest.raises(AbsplatError) as ei:
+            ctx.as_load_scene(bad["mean"], bad["chol"], bad["opacity"], bad["color"])
+        assert ei.value.status == 2 and f"Gaussian {idx[0]}" in str(ei.value)
+    lo, hi, _ = ctx.as_render_bounds(16, 16)
+    assert torch.equal(lo, lo0) and torch.equal(hi, hi0)
