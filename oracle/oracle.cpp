@@ -207,7 +207,8 @@ struct VarDef {
   double c, r;    // parameter = c + r * xi
 };
 struct SubBox {
-  int n;
+  int n;   // form variables: the shared ones (v[0..ns)) then the private mean offsets
+  int ns;  // shared variables (pose axes and group shifts)
   VarDef v[NV];
   double fixed[9];  // parameter value on every axis when xi = 0 (centre or fixed value)
 };
@@ -221,6 +222,8 @@ struct Problem {
   const int32_t* group_of;
   double dir[3][3];
   const float *col_lo, *col_hi, *op_lo, *op_hi;
+  const float *priv_lo, *priv_hi;  // per-Gaussian private mean offsets (NEXT-2)
+  int n_priv;                      // 3 when present, else 0
   Axis axes[9];
   int n_sub;
 };
@@ -245,6 +248,14 @@ int setup_problem(Problem& P, int64_t N, const float* mean, const float* chol, c
   P.col_hi = sbox ? sbox->col_hi : nullptr;
   P.op_lo = sbox ? sbox->op_lo : nullptr;
   P.op_hi = sbox ? sbox->op_hi : nullptr;
+  P.priv_lo = sbox ? sbox->priv_lo : nullptr;
+  P.priv_hi = sbox ? sbox->priv_hi : nullptr;
+  if ((P.priv_lo == nullptr) != (P.priv_hi == nullptr)) return -1;
+  P.n_priv = P.priv_lo ? 3 : 0;
+  for (int64_t i = 0; P.priv_lo && i < 3 * N; ++i)
+    if (!(P.priv_lo[i] <= P.priv_hi[i]) || !std::isfinite(P.priv_lo[i]) ||
+        !std::isfinite(P.priv_hi[i]))
+      return -1;
   if ((P.col_lo == nullptr) != (P.col_hi == nullptr)) return -1;
   if ((P.op_lo == nullptr) != (P.op_hi == nullptr)) return -1;
   for (int a = 0; a < 3; ++a) {
@@ -284,13 +295,20 @@ int setup_problem(Problem& P, int64_t N, const float* mean, const float* chol, c
       }
     P.n_sub = box->n_explicit;
   }
-  if (nvar > NV) return -1;
+  if (nvar + P.n_priv > NV) return -1;
   if (cam->W <= 0 || cam->H <= 0) return -1;
   return 0;
 }
 
 // sub-box s: multi-index over axes (axis 0 fastest), uniform split (G18)
+SubBox make_subbox_shared(const Problem& P, int s);
 SubBox make_subbox(const Problem& P, int s) {
+  SubBox B = make_subbox_shared(P, s);
+  B.ns = B.n;
+  B.n += P.n_priv;
+  return B;
+}
+SubBox make_subbox_shared(const Problem& P, int s) {
   SubBox B;
   B.n = 0;
   if (P.box.n_explicit > 0) {  // explicit partition: centre / half-width of each axis
@@ -332,7 +350,7 @@ struct Pose {
 
 Pose pose_forms(const Problem& P, const SubBox& B) {
   Pose pose;
-  const int n = B.n;
+  const int n = B.ns;  // the pose depends on the shared variables only
   // Euler centre of this sub-box
   double ec[3];
   for (int k = 0; k < 3; ++k) ec[k] = P.cam.euler[k] + B.fixed[3 + k];
@@ -530,6 +548,12 @@ GRec gaussian_setup(const Problem& P, const SubBox& B, const Pose& pose, int64_t
   for (int b = 0; b < 3; ++b) {
     Form w = constant(uw[b]);
     if (grp >= 0 && grp < P.n_groups) w = add(w, scale(pose.g[grp], P.dir[grp][b]));
+    if (P.n_priv) {  // private offset: centre + radius * eta_b, eta_b = variable ns + b
+      const double lo = P.priv_lo[3 * i + b], hi = P.priv_hi[3 * i + b];
+      w = add_const(w, 0.5 * (lo + hi));
+      w.lo.A[B.ns + b] += 0.5 * (hi - lo);
+      w.hi.A[B.ns + b] += 0.5 * (hi - lo);
+    }
     v[b] = add(w, scale(pose.t[b], -1.0));
   }
   for (int a = 0; a < 3; ++a) {
@@ -649,12 +673,18 @@ bool culled(const GRec& G, double x0, double x1, double y0, double y1) {
 
 // step 13: three-valued Ind(d_i - d_j) with the index tie-break (G6).
 // returns 1 (j certainly in front of i), 0 (certainly not), -1 ('?')
-int ind_class(const GRec& Gi, int64_t i, const GRec& Gj, int64_t j, int n) {
+// Variables k >= ns are private to each Gaussian (NEXT-2): independent in d_i and d_j, so
+// their slopes add in absolute value instead of cancelling.
+int ind_class(const GRec& Gi, int64_t i, const GRec& Gj, int64_t j, int n, int ns) {
   double dl = Gi.d.lo.b - Gj.d.hi.b, du = Gi.d.hi.b - Gj.d.lo.b;
   double s1 = 0, s2 = 0;
-  for (int k = 0; k < n; ++k) {
+  for (int k = 0; k < ns; ++k) {
     s1 += std::fabs(Gi.d.lo.A[k] - Gj.d.hi.A[k]);
     s2 += std::fabs(Gi.d.hi.A[k] - Gj.d.lo.A[k]);
+  }
+  for (int k = ns; k < n; ++k) {
+    s1 += std::fabs(Gi.d.lo.A[k]) + std::fabs(Gj.d.hi.A[k]);
+    s2 += std::fabs(Gi.d.hi.A[k]) + std::fabs(Gj.d.lo.A[k]);
   }
   dl -= s1;  // lower bound of d_i - d_j over the box
   du += s2;  // upper bound
@@ -755,7 +785,7 @@ void build_tile_list(const Problem& P, const SubData& S, int ts, int tile, bool 
   for (int p = 0; p < K; ++p)
     for (int q = 0; q < K; ++q) {
       if (q == p) continue;
-      int c = ind_class(S.G[T.L[p]], T.L[p], S.G[T.L[q]], T.L[q], n);
+      int c = ind_class(S.G[T.L[p]], T.L[p], S.G[T.L[q]], T.L[q], n, S.B.ns);
       if (c == -1) {
         if (q < p)
           T.EF[p].push_back(q);
@@ -817,7 +847,7 @@ void blend_direct(const SubData& S, const std::vector<int64_t>& L, const double*
     double Tb = 1.0, Tl = 1.0;  // T_hi over F(i), T_lo over G(i)
     for (int q = 0; q < K; ++q) {
       if (q == p) continue;  // Ind(d_i - d_i) = 0
-      int c = ind_class(S.G[L[p]], L[p], S.G[L[q]], L[q], n);
+      int c = ind_class(S.G[L[p]], L[p], S.G[L[q]], L[q], n, S.B.ns);
       if (c == 1) {
         Tb *= 1.0 - alo[q];
         Tl *= 1.0 - ahi[q];
@@ -1148,7 +1178,7 @@ int32_t or_pose_forms(const or_camera* cam, const or_pose_box* box, const or_sce
   if (sub < 0 || sub >= P.n_sub) return -1;
   SubBox B = make_subbox(P, sub);
   Pose pose = pose_forms(P, B);
-  const int n = B.n;
+  const int n = B.ns;
   for (int e = 0; e < 9; ++e) form_to(pose.R[e], n, R + e * 2 * (n + 1));
   for (int e = 0; e < 3; ++e) form_to(pose.t[e], n, t + e * 2 * (n + 1));
   *nvars = n;

@@ -58,6 +58,11 @@ typedef struct {
   const float* col_hi;
   const float* op_lo;         /* [N] or NULL (opacity interval) */
   const float* op_hi;
+  /* [N][3] or NULL: per-Gaussian private mean offsets (world axes, metres), independent of
+   * every other Gaussian.  They enter each Gaussian's forms as three
+   * private variables after the shared ones; depth comparisons treat them as independent. */
+  const float* priv_lo;
+  const float* priv_hi;
 } or_scene_box;
 
 typedef struct {

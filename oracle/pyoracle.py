@@ -47,7 +47,7 @@ class SceneBox(C.Structure):
     _fields_ = [("n_groups", C.c_int32), ("group_of", C.c_void_p), ("dir", C.c_void_p),
                 ("shift_lo", C.c_void_p), ("shift_hi", C.c_void_p), ("parts", C.c_int32 * 3),
                 ("col_lo", C.c_void_p), ("col_hi", C.c_void_p), ("op_lo", C.c_void_p),
-                ("op_hi", C.c_void_p)]
+                ("op_hi", C.c_void_p), ("priv_lo", C.c_void_p), ("priv_hi", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -166,6 +166,8 @@ class _SceneBoxHolder:
         s.col_hi = _ptr(arr(sbox.get("col_hi"), np.float32))
         s.op_lo = _ptr(arr(sbox.get("op_lo"), np.float32))
         s.op_hi = _ptr(arr(sbox.get("op_hi"), np.float32))
+        s.priv_lo = _ptr(arr(sbox.get("priv_lo"), np.float32))
+        s.priv_hi = _ptr(arr(sbox.get("priv_hi"), np.float32))
         self.s = s
 
     def ref(self):
