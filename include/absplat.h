@@ -82,6 +82,12 @@ typedef struct {
   const float* col_hi;
   const float* op_lo;
   const float* op_hi;
+  /* [N][3] or NULL (NEXT-2): per-Gaussian private mean offsets in world units, independent
+   * across Gaussians: Gaussian i's mean is mean[i] + delta with delta_b in
+   * [priv_lo[i][b], priv_hi[i][b]].  They add three private variables to every Gaussian's
+   * forms (n = shared + 3 <= 9); depth comparisons treat them as independent. */
+  const float* priv_lo;
+  const float* priv_hi;
 } as_scene_box;
 
 /* Counters and per-phase device times of the last render (times in ms, CUDA events). */

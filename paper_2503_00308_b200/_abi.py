@@ -34,7 +34,7 @@ class AsSceneBox(C.Structure):
     _fields_ = [("n_groups", C.c_int32), ("group_of", C.c_void_p), ("dir", C.c_void_p),
                 ("shift_lo", C.c_void_p), ("shift_hi", C.c_void_p), ("parts", C.c_int32 * 3),
                 ("col_lo", C.c_void_p), ("col_hi", C.c_void_p), ("op_lo", C.c_void_p),
-                ("op_hi", C.c_void_p)]
+                ("op_hi", C.c_void_p), ("priv_lo", C.c_void_p), ("priv_hi", C.c_void_p)]
 
 
 class AsStats(C.Structure):

@@ -191,6 +191,8 @@ class Context:
         s.col_hi = host(sbox.get("col_hi"), np.float32)
         s.op_lo = host(sbox.get("op_lo"), np.float32)
         s.op_hi = host(sbox.get("op_hi"), np.float32)
+        s.priv_lo = host(sbox.get("priv_lo"), np.float32)
+        s.priv_hi = host(sbox.get("priv_hi"), np.float32)
         self._check(self._L.as_set_scene_box(self._ctx, C.byref(s)))
 
     def load_workload(self, w):

@@ -45,8 +45,8 @@ struct as_ctx {
   double dir[3][3] = {};
   double shift_lo[3] = {}, shift_hi[3] = {};
   int gparts[3] = {1, 1, 1};
-  DevBuf group_of, col_lo, col_hi, op_lo, op_hi;
-  bool has_group = false, has_col = false, has_op = false;
+  DevBuf group_of, col_lo, col_hi, op_lo, op_hi, priv_lo, priv_hi;
+  bool has_group = false, has_col = false, has_op = false, has_priv = false;
   // camera / box
   as_camera cam{};
   as_pose_box box{};
@@ -166,7 +166,8 @@ bool finite_f(float v) { return std::isfinite(v); }
 struct BoxInfo {
   BoxParams bp;
   int n_sub;
-  int n_vars;
+  int n_vars;    // form variables: shared + private (3 with per-Gaussian mean offsets)
+  int n_shared;  // pose axes and group shifts
   // full-box variables (for as_render_concrete)
   int axis[NVMAX];
   double c[NVMAX], r[NVMAX];
@@ -245,7 +246,12 @@ as_status make_box(as_ctx* ctx, BoxInfo& bi) {
     bp.t0[k] = ctx->cam.t[k];
   }
   bi.n_sub = (int)nsub;
-  bi.n_vars = nv;
+  bi.n_shared = nv;
+  bi.n_vars = nv + (ctx->has_priv ? 3 : 0);
+  if (bi.n_vars > NVMAX) {
+    set_err(ctx, "too many box variables (%d shared + 3 private > %d)", nv, NVMAX);
+    return AS_E_ARG;
+  }
   return AS_OK;
 }
 
@@ -270,6 +276,9 @@ void run_setup(as_ctx* ctx, const BoxInfo& bi, int s) {
   a.col_hi = ctx->has_col ? P<float>(ctx->col_hi) : nullptr;
   a.op_lo = ctx->has_op ? P<float>(ctx->op_lo) : nullptr;
   a.op_hi = ctx->has_op ? P<float>(ctx->op_hi) : nullptr;
+  a.priv_lo = ctx->has_priv ? P<float>(ctx->priv_lo) : nullptr;
+  a.priv_hi = ctx->has_priv ? P<float>(ctx->priv_hi) : nullptr;
+  a.ns = bi.n_shared;
   a.N = ctx->N;
   a.fx = ctx->cam.fx;
   a.fy = ctx->cam.fy;
@@ -497,6 +506,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     pa.mF = P<ulonglong2>(ctx->maskF);
     pa.mG = P<ulonglong2>(ctx->maskG);
     pa.subunc = ctr + C_SUBUNC;
+    pa.ns = bi.n_shared;
     CK(cudaMemsetAsync(pa.subunc, 0, sizeof(unsigned long long), st));
     launch_pairs_prep(pa, st);
     LAUNCHED(ctx, 2);
@@ -853,7 +863,7 @@ as_status as_destroy(as_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->st_mean,
                     &ctx->st_chol, &ctx->st_opacity, &ctx->st_color, &ctx->group_of,
-                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->tile_unc, &ctx->lin_tiles, &ctx->pose, &ctx->hot,
+                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->priv_lo, &ctx->priv_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->tile_unc, &ctx->lin_tiles, &ctx->pose, &ctx->hot,
                     &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
                     &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
@@ -965,7 +975,7 @@ as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* 
     std::swap(ctx->color, scol);
     ctx->N = N;
     ctx->n_groups = 0;
-    ctx->has_group = ctx->has_col = ctx->has_op = false;
+    ctx->has_group = ctx->has_col = ctx->has_op = ctx->has_priv = false;
     return AS_OK;
   } catch (const Err& e) {
     return e.st;
@@ -1107,7 +1117,7 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
   }
   if (!sb) {
     ctx->n_groups = 0;
-    ctx->has_group = ctx->has_col = ctx->has_op = false;
+    ctx->has_group = ctx->has_col = ctx->has_op = ctx->has_priv = false;
     return AS_OK;
   }
   const int64_t N = ctx->N;
@@ -1117,7 +1127,8 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
     return AS_E_ARG;
   }
   if ((sb->col_lo == nullptr) != (sb->col_hi == nullptr) ||
-      (sb->op_lo == nullptr) != (sb->op_hi == nullptr)) {
+      (sb->op_lo == nullptr) != (sb->op_hi == nullptr) ||
+      (sb->priv_lo == nullptr) != (sb->priv_hi == nullptr)) {
     set_err(ctx, "as_set_scene_box: lo/hi must both be given");
     return AS_E_ARG;
   }
@@ -1148,6 +1159,14 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
         return AS_E_SCENE;
       }
     }
+    if (sb->priv_lo)
+      for (int k = 0; k < 3; ++k) {
+        const float l = sb->priv_lo[3 * i + k], h = sb->priv_hi[3 * i + k];
+        if (!std::isfinite(l) || !std::isfinite(h) || !(l <= h)) {
+          set_err(ctx, "private mean interval of Gaussian %lld invalid", (long long)i);
+          return AS_E_SCENE;
+        }
+      }
   }
   try {
     cudaSetDevice(ctx->device);
@@ -1176,6 +1195,13 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
       ensure(ctx, ctx->op_hi, 4 * std::max<int64_t>(N, 1));
       CK(cudaMemcpyAsync(ctx->op_lo.p, sb->op_lo, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
       CK(cudaMemcpyAsync(ctx->op_hi.p, sb->op_hi, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->has_priv = sb->priv_lo != nullptr;
+    if (ctx->has_priv) {
+      ensure(ctx, ctx->priv_lo, 12 * std::max<int64_t>(N, 1));
+      ensure(ctx, ctx->priv_hi, 12 * std::max<int64_t>(N, 1));
+      CK(cudaMemcpyAsync(ctx->priv_lo.p, sb->priv_lo, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->priv_hi.p, sb->priv_hi, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));  // host sources may be freed after return
     return AS_OK;
@@ -1554,6 +1580,10 @@ as_status as_render_concrete(as_ctx* ctx, const double* xi, float* img, int32_t 
   if ((st = make_box(ctx, bi)) != AS_OK) return st;
   if (!img || (bi.n_vars > 0 && !xi)) {
     set_err(ctx, "as_render_concrete: bad arguments");
+    return AS_E_ARG;
+  }
+  if (ctx->has_priv) {
+    set_err(ctx, "as_render_concrete: private mean offsets set (load the offset means instead)");
     return AS_E_ARG;
   }
   double param[9];

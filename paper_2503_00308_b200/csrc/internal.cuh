@@ -227,6 +227,9 @@ struct SetupArgs {
   unsigned long long* counters;  // [4]: fails, straddles, dropped, spare
   double k_tol;               // adaptive MatrixInv order (P:470 (3)): > 0 enables
   int k_max;
+  const float* priv_lo;       // [N][3] private mean offsets (NEXT-2) or nullptr
+  const float* priv_hi;
+  int ns;                     // shared variables (privates are ns .. ns+2)
 };
 
 void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st);
@@ -278,6 +281,7 @@ struct PairArgs {
   ulonglong2* mF;         // [M] E_F bits over [h, h+128) (0 for PM_OVF positions)
   ulonglong2* mG;         // [M] E_G bits over (p, p+128] (0 for PM_OVF positions)
   unsigned long long* subunc;  // uncertain (position, partner) entries of this sub-box
+  int ns;                 // shared variables; slots ns.. are per-Gaussian private (NEXT-2)
   unsigned long long* counters;  // [0] uncertain pairs, [1] order violations
 };
 void launch_pairs_prep(const PairArgs& a, cudaStream_t st);

@@ -129,31 +129,6 @@ void launch_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin, 
 }
 
 // ------------------------------------------------------------------------- pairs (a7)
-// Ind(d_i - d_j) over the box with the index tie-break (G6): 1 = j certainly in front of i,
-// 0 = certainly not, -1 = '?'.  Same expression order as the definition (no FMA).
-template <int NV>
-__device__ __forceinline__ int ind_class(const PairRec<NV>& Pi, int32_t i, const PairRec<NV>& Pj,
-                                         int32_t j) {
-  double dl = __dsub_rn(Pi.dl[NV], Pj.du[NV]);
-  double du = __dsub_rn(Pi.du[NV], Pj.dl[NV]);
-  double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    s1 = __dadd_rn(s1, fabs(__dsub_rn(Pi.dl[k], Pj.du[k])));
-    s2 = __dadd_rn(s2, fabs(__dsub_rn(Pi.du[k], Pj.dl[k])));
-  }
-  dl = __dsub_rn(dl, s1);
-  du = __dadd_rn(du, s2);
-  if (i > j) {
-    if (dl >= 0.0) return 1;
-    if (du < 0.0) return 0;
-  } else {
-    if (dl > 0.0) return 1;
-    if (du <= 0.0) return 0;
-  }
-  return -1;
-}
-
 template <int NV>
 __device__ __forceinline__ PairRec<NV> load_pair(const void* base, int32_t g) {
   return reinterpret_cast<const PairRec<NV>*>(base)[g];
@@ -175,16 +150,24 @@ __device__ __forceinline__ DForm<NV> load_posd(const double* posD, int64_t q) {
   }
   return f;
 }
+// Ind(d_i - d_j) over the box with the index tie-break (G6): 1 = j certainly in front of i,
+// 0 = certainly not, -1 = '?'.  Same expression order as the definition (no FMA).  Slots
+// k >= ns are private to each Gaussian (NEXT-2): independent, so their slopes add.
 template <int NV>
 __device__ __forceinline__ int ind_class_d(const DForm<NV>& Pi, int32_t i, const DForm<NV>& Pj,
-                                           int32_t j) {
+                                           int32_t j, int ns) {
   double dl = __dsub_rn(Pi.l[NV], Pj.u[NV]);
   double du = __dsub_rn(Pi.u[NV], Pj.l[NV]);
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    s1 = __dadd_rn(s1, fabs(__dsub_rn(Pi.l[k], Pj.u[k])));
-    s2 = __dadd_rn(s2, fabs(__dsub_rn(Pi.u[k], Pj.l[k])));
+    if (k < ns) {
+      s1 = __dadd_rn(s1, fabs(__dsub_rn(Pi.l[k], Pj.u[k])));
+      s2 = __dadd_rn(s2, fabs(__dsub_rn(Pi.u[k], Pj.l[k])));
+    } else {
+      s1 = __dadd_rn(s1, __dadd_rn(fabs(Pi.l[k]), fabs(Pj.u[k])));
+      s2 = __dadd_rn(s2, __dadd_rn(fabs(Pi.u[k]), fabs(Pj.l[k])));
+    }
   }
   dl = __dsub_rn(dl, s1);
   du = __dadd_rn(du, s2);
@@ -346,7 +329,7 @@ __global__ void k_pairs(PairArgs A) {
     const double kj = A.kapP[q];
     if (beyond(ki - kj, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj, A.ns);
     if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
       if (c == 0) ++viol;
       if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
@@ -365,7 +348,7 @@ __global__ void k_pairs(PairArgs A) {
     const double kj = A.kapP[q];
     if (beyond(kj - ki, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj, A.ns);
     if (c == -1 || c == 1) {
       if (c == 1) ++viol;
       if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);

@@ -241,6 +241,11 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
     double c = real ? -sp.t[b][kc] : 0.0;
     if (grp >= 0 && real) c += A.dir[grp][b] * sp.g[grp][kc];
     if (L.cst()) c += (double)A.mean[3 * i + b];
+    if (A.priv_lo) {  // private offset (NEXT-2): centre + radius * eta_b, eta_b = slot ns + b
+      const double lo = A.priv_lo[3 * i + b], hi = A.priv_hi[3 * i + b];
+      if (L.cst()) c += 0.5 * (lo + hi);
+      if (k == A.ns + b) c += 0.5 * (hi - lo);
+    }
     v[b] = HL{c, c};
   }
   HL uc[3];

@@ -90,3 +90,58 @@ def test_depth_flip_between_two_private_boxes(oracle):
     worst, st = _sampled_containment(oracle, w, lo, hi, 20, 5)
     assert st["uncertain_pairs"] >= 1
     assert worst <= 1e-9, worst
+
+
+# ------------------------------------------------------------------ GPU (through the C ABI)
+@pytest.fixture(scope="module")
+def gctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _gpu_vs_oracle(gctx, oracle, v):
+    gctx.load_workload(v)
+    lo, hi, st = gctx.as_render_bounds(v.tile, v.batch)
+    olo, ohi, ost = oracle.render_bounds(v)
+    err = max(np.abs(lo.cpu().numpy() - olo).max(), np.abs(hi.cpu().numpy() - ohi).max())
+    assert err <= 1e-4, err
+    assert st["n_vars"] == ost["n_vars"]
+    assert st["pairs"] == ost["pairs"] and st["uncertain_pairs"] == ost["uncertain_pairs"]
+    assert st["order_violations"] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_private_parity_c1(gctx, oracle):
+    w = make_config("C1")
+    _gpu_vs_oracle(gctx, oracle, with_private(w, np.full((w.N, 3), -0.02), np.full((w.N, 3), 0.02)))
+
+
+@pytest.mark.gpu
+def test_gpu_private_parity_c5_blade(gctx, oracle):
+    """C5 (reduced) with independent +-2 cm mean boxes on the blade Gaussians on top of the
+    shared blade shift, the colour box and the camera box (n = 2 shared + 3 private)."""
+    w = make_config("C5", N=3000, res=48)
+    blade = w.scene_box["group_of"] >= 0
+    lo = np.zeros((w.N, 3), np.float32)
+    hi = np.zeros((w.N, 3), np.float32)
+    lo[blade] = -0.02
+    hi[blade] = 0.02
+    _gpu_vs_oracle(gctx, oracle, with_private(w, lo, hi))
+
+
+@pytest.mark.gpu
+def test_gpu_private_depth_flip(gctx, oracle):
+    w = make_config("C1", N=2, res=16)
+    m = w.mean.copy()
+    m[0] = [0.0, 0.0, 5.0]
+    m[1] = [0.02, 0.0, 5.0]
+    w.mean = m
+    w.pose_box["eps_t"] = [0.0, 0.0, 0.0]
+    v = with_private(w, np.array([[0, 0, -0.05]] * 2), np.array([[0, 0, 0.05]] * 2))
+    _gpu_vs_oracle(gctx, oracle, v)
+    gctx.as_set_scene_box(None)
