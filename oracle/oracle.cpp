@@ -444,7 +444,7 @@ int adaptive_k(double nx0, double rho, int k0, double tol, int kmax) {
 // MatrixInv (Alg. 4) on forms X[4] (row-major).  Returns 0 / 1 (det<=0) / 2 (rho>=1)
 // k < 0 selects the order adaptively: k = adaptive_k(|X0|_F, rho, 8, k_tol, k_max).
 int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rho,
-               double k_tol = 0.0, int k_max = 8, int* k_used = nullptr) {
+               double k_tol = 0.0, int k_max = 8, int* k_used = nullptr, bool backward = false) {
   // (1) X0 = inverse of the centre matrix of the input set (P:470, P:550 footnote)
   double Xc[4];
   for (int e = 0; e < 4; ++e) {
@@ -485,6 +485,7 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
   std::vector<Form> Pw(4), Pn(4);
   Form Xp[4];
   for (int e = 0; e < 4; ++e) Xp[e] = constant(0.0);
+  std::vector<double> Bl((k + 1) * 4), Bh((k + 1) * 4);  // bounds of P^i entries (backward)
   for (int i = 0; i <= k; ++i) {
     if (i == 0) {
       Pw[0] = constant(1.0);
@@ -508,6 +509,7 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
         }
       Pw = Pn;
     }
+    for (int e = 0; e < 4; ++e) conc(Pw[e], n, Bl[i * 4 + e], Bh[i * 4 + e]);
     // Xa = X0 . P^i (exact), l.4 Xp = Sum(Xa)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b) {
@@ -523,6 +525,67 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
     conic[e] = Xp[e];
     conic[e].lo.b -= eps;
     conic[e].hi.b += eps;
+  }
+  if (!backward) return 0;
+  // NEXT-4 (CROWN-style back-substitution): the lower / upper affine bound of
+  // each conic entry by propagating its coefficients backwards through
+  // Xp = X0 + X0 sum_i P^i, P^i = P^{i-1} E with the same R1 planes (R2 at i = 2 on the
+  // diagonal) down to E = I - X X0, affine in the box variables, so the product relaxations
+  // are not compounded.  The planes use the forward pass's bounds of P^{i-1} and E.
+  double El[4], Eh[4];
+  for (int e = 0; e < 4; ++e) conc(E[e], n, El[e], Eh[e]);
+  // lower affine bound of  cst + sum_{i=1..top} sum_e lam[i][e] P^i_e   (P^1 = E)
+  auto backsub = [&](std::vector<double> lam, int top, double cst) -> Aff {
+    double mu[4] = {0, 0, 0, 0};
+    for (int i = top; i >= 2; --i)
+      for (int c = 0; c < 2; ++c)
+        for (int d = 0; d < 2; ++d) {
+          const double lm = lam[i * 4 + 2 * c + d];
+          if (lm == 0.0) continue;
+          for (int l = 0; l < 2; ++l) {
+            const double xl = Bl[(i - 1) * 4 + 2 * c + l], xh = Bh[(i - 1) * 4 + 2 * c + l];
+            const double yl = El[2 * l + d], yh = Eh[2 * l + d];
+            if (i == 2 && c == l && l == d) {  // E_cc * E_cc: R2 (tangent / chord)
+              if (lm >= 0) {
+                const double p = std::min(std::max(0.0, xl), xh);
+                mu[2 * c + c] += lm * 2.0 * p;
+                cst -= lm * p * p;
+              } else {
+                mu[2 * c + c] += lm * (xl + xh);
+                cst -= lm * xl * xh;
+              }
+            } else {  // R1: lower plane yl f + xl g - xl yl, upper plane yh f + xl g - xl yh
+              const double yy = lm >= 0 ? yl : yh;
+              lam[(i - 1) * 4 + 2 * c + l] += lm * yy;
+              mu[2 * l + d] += lm * xl;
+              cst -= lm * xl * yy;
+            }
+          }
+        }
+    Aff r = aff_zero();
+    r.b = cst;
+    for (int e = 0; e < 4; ++e) {
+      const double ce = mu[e] + lam[4 + e];
+      r = aff_add(r, ce >= 0 ? aff_scale(E[e].lo, ce) : aff_scale(E[e].hi, ce));
+    }
+    return r;
+  };
+  for (int out = 0; out < 4; ++out) {
+    const int oa = out / 2, ob = out % 2;
+    for (int side = 0; side < 2; ++side) {
+      const double sg = side == 0 ? 1.0 : -1.0;  // lower bound of sg * Conic_ab
+      std::vector<double> lam((k + 1) * 4, 0.0);
+      for (int i = 1; i <= k; ++i)
+        for (int m = 0; m < 2; ++m) lam[i * 4 + 2 * m + ob] = sg * X0[2 * oa + m];
+      const Aff bnd = backsub(lam, k, sg * X0[out]);  // i = 0 term: X0 . I
+      if (side == 0) {
+        conic[out].lo = bnd;
+        conic[out].lo.b -= eps;
+      } else {
+        conic[out].hi = aff_scale(bnd, -1.0);
+        conic[out].hi.b += eps;
+      }
+    }
   }
   return 0;
 }
@@ -594,9 +657,10 @@ GRec gaussian_setup(const Problem& P, const SubBox& B, const Pose& pose, int64_t
   G.X[2] = X11;
   Form Xm[4] = {X00, X01, X01, X11};
   G.k = K_TAYLOR;
+  const bool bwd = P.box.inv_backward != 0;
   int st = (P.box.k_tol > 0)
-               ? matrix_inv(Xm, n, -1, G.conic, G.eps, G.rho, P.box.k_tol, P.box.k_max, &G.k)
-               : matrix_inv(Xm, n, K_TAYLOR, G.conic, G.eps, G.rho);
+               ? matrix_inv(Xm, n, -1, G.conic, G.eps, G.rho, P.box.k_tol, P.box.k_max, &G.k, bwd)
+               : matrix_inv(Xm, n, K_TAYLOR, G.conic, G.eps, G.rho, 0.0, 8, nullptr, bwd);
   if (st != 0) G.flags |= GF_FAIL;
   // l.9 pieces: W = Mmul(Conic, Mp) (association G4), D2 = Mul(d,d), DU = Mul(d, up)
   if (!(G.flags & GF_FAIL)) {
@@ -1158,6 +1222,17 @@ int32_t or_ind_relax(double xl, double xh) {
   if (xl > 0) return 1;
   if (xh <= 0) return 0;
   return -1;
+}
+
+int32_t or_matrix_inv_bwd(int32_t n, const double* X, int32_t k, double* conic, double* eps,
+                          double* rho) {
+  if (n < 0 || n > NV || k < 1) return -1;
+  Form Xf[4], Cf[4];
+  for (int e = 0; e < 4; ++e) form_from(X + e * 2 * (n + 1), n, Xf[e]);
+  int st = matrix_inv(Xf, n, k, Cf, *eps, *rho, 0.0, 8, nullptr, true);
+  if (st == 0)
+    for (int e = 0; e < 4; ++e) form_to(Cf[e], n, conic + e * 2 * (n + 1));
+  return st;
 }
 
 int32_t or_matrix_inv(int32_t n, const double* X, int32_t k, double* conic, double* eps,

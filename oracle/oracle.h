@@ -45,6 +45,9 @@ typedef struct {
    * k_max; k_tol <= 0 keeps k = 8 (G14). */
   double k_tol;
   int32_t k_max;
+  /* NEXT-4: 1 = conic bounds by back-substitution through MatrixInv (CROWN-style, P:141,
+   * P:486) instead of the forward forms; 0 = forward (reading G3). */
+  int32_t inv_backward;
 } or_pose_box;
 
 typedef struct {
@@ -145,6 +148,9 @@ int32_t or_ind_relax(double xl, double xh);
  * Returns 0 ok, 1 FAIL(det<=0), 2 FAIL(rho>=1). */
 int32_t or_matrix_inv(int32_t n, const double* X, int32_t k, double* conic, double* eps,
                       double* rho);
+/* Same input / output as or_matrix_inv, with the conic bounds by back-substitution (NEXT-4). */
+int32_t or_matrix_inv_bwd(int32_t n, const double* X, int32_t k, double* conic, double* eps,
+                          double* rho);
 
 /* Pose forms of sub-box `sub` (step 1): R (world->camera) [9 forms] and t [3 forms],
  * plus the number of variables.  Returns number of sub-boxes, or <0 on error. */

@@ -40,7 +40,7 @@ class PoseBox(C.Structure):
     _fields_ = [("eps_t", C.c_double * 3), ("eps_R", C.c_double * 3), ("t_off", C.c_double * 3),
                 ("R_off", C.c_double * 3), ("t_frame", C.c_int32), ("parts", C.c_int32 * 6),
                 ("n_explicit", C.c_int32), ("explicit_bounds", C.c_void_p),
-                ("k_tol", C.c_double), ("k_max", C.c_int32)]
+                ("k_tol", C.c_double), ("k_max", C.c_int32), ("inv_backward", C.c_int32)]
 
 
 class SceneBox(C.Structure):
@@ -90,6 +90,8 @@ def lib():
         L.or_ind_relax.restype = C.c_int32
         L.or_matrix_inv.argtypes = [C.c_int32, P, C.c_int32, P, P, P]
         L.or_matrix_inv.restype = C.c_int32
+        L.or_matrix_inv_bwd.argtypes = [C.c_int32, P, C.c_int32, P, P, P]
+        L.or_matrix_inv_bwd.restype = C.c_int32
         L.or_pose_forms.argtypes = [P, P, P, C.c_int32, P, P, P]
         L.or_pose_forms.restype = C.c_int32
         L.or_gaussian_forms.argtypes = [C.c_int64, P, P, P, P, P, P, P, C.c_int32, P, P]
@@ -125,6 +127,7 @@ def pose_box_struct(box: dict) -> PoseBox:
         b.parts[k] = int(box["parts"][k])
     b.k_tol = float(box.get("k_tol", 0.0))
     b.k_max = int(box.get("k_max", 8))
+    b.inv_backward = int(box.get("inv_backward", 0))
     sub = box.get("subboxes")
     if sub is not None and len(sub) > 0:
         arr = np.ascontiguousarray(sub, np.float64).reshape(-1, 9, 2)
@@ -352,13 +355,15 @@ def ind_relax(xl, xh):
     return int(lib().or_ind_relax(xl, xh))
 
 
-def matrix_inv(X, n, k=8):
-    """X: [4, 2(n+1)] forms.  Returns (status, conic [4,2(n+1)], eps, rho)."""
+def matrix_inv(X, n, k=8, backward=False):
+    """X: [4, 2(n+1)] forms.  Returns (status, conic [4,2(n+1)], eps, rho); backward=True
+    bounds the conic by back-substitution (NEXT-4)."""
     X = np.ascontiguousarray(X, np.float64).reshape(-1)
     out = np.zeros(4 * 2 * (n + 1))
     eps = C.c_double()
     rho = C.c_double()
-    st = lib().or_matrix_inv(n, _ptr(X), k, _ptr(out), C.addressof(eps), C.addressof(rho))
+    fn = lib().or_matrix_inv_bwd if backward else lib().or_matrix_inv
+    st = fn(n, _ptr(X), k, _ptr(out), C.addressof(eps), C.addressof(rho))
     return st, out.reshape(4, 2 * (n + 1)), eps.value, rho.value
 
 
