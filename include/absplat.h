@@ -175,6 +175,12 @@ as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds);
  * Eps = |X0|_F rho^(k+1) / (1 - rho) is <= k_tol, at most k_max (8..64); k_tol <= 0 restores the
  * fixed k = 8.  Applies to subsequent renders. */
 as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max);
+/* MatrixInv conic bounds: backward = 0 (default) concretises the
+ * forward forms of Xp = X0 + X0 sum_i P^i (reading G3); backward = 1 bounds each conic entry
+ * by back-substitution (CROWN-style) through P^i = P^{i-1} E with the same
+ * McCormick planes down to E = I - X X0 (reading O17); tighter (Example 1: 0.7588 -> 0.7371).
+ * With back-substitution the adaptive order is limited to k_max <= 32. */
+as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward);
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
 
 /* ---- blend mode ----

@@ -201,7 +201,9 @@ class Context:
         self.as_set_camera(w.camera)
         self.as_set_pose_box(w.pose_box)
         self.as_set_scene_box(w.scene_box)
+        self.as_set_inverse_mode(0)
         self.as_set_matrixinv(w.pose_box.get("k_tol", 0.0), w.pose_box.get("k_max", 8))
+        self.as_set_inverse_mode(w.pose_box.get("inv_backward", 0))
         if w.pose_box.get("subboxes") is not None:
             self.as_set_subboxes(w.pose_box["subboxes"])
 
@@ -257,6 +259,10 @@ class Context:
     def as_set_blend(self, mode: int = 0):
         """0: interval blend; 1: + linear-relation blend on exception-free tiles (n <= 3)."""
         self._check(self._L.as_set_blend(self._ctx, int(mode)))
+
+    def as_set_inverse_mode(self, backward: int = 0):
+        """MatrixInv conic bounds: 0 forward forms, 1 back-substitution (NEXT-4)."""
+        self._check(self._L.as_set_inverse_mode(self._ctx, int(backward)))
 
     def as_subbox_fails(self):
         """MatrixInv FAIL count per sub-box of the current partition (setup only)."""

@@ -69,6 +69,7 @@ struct as_ctx {
   DevBuf subs;
   double k_tol = 0.0;  // as_set_matrixinv (adaptive Taylor order)
   int k_max = 8;
+  int inv_backward = 0;  // as_set_inverse_mode (NEXT-4 back-substitution)
   int blend_mode = 0;  // as_set_blend: 0 interval, 1 + linear on exception-free tiles
   bool last_has_exc = false;
   int64_t last_M = 0;
@@ -293,6 +294,7 @@ void run_setup(as_ctx* ctx, const BoxInfo& bi, int s) {
   a.kval = P<int32_t>(ctx->kval);
   a.k_tol = ctx->k_tol;
   a.k_max = ctx->k_max;
+  a.inv_backward = ctx->inv_backward;
   a.wsmax = P<unsigned long long>(ctx->counters) + 4;
   a.counters = P<unsigned long long>(ctx->counters);
   launch_setup(bi.n_vars, a, ctx->stream);
@@ -1041,10 +1043,28 @@ as_status as_set_blend(as_ctx* ctx, int32_t mode) {
   return AS_OK;
 }
 
+as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward) {
+  if (!ctx) return AS_E_ARG;
+  if (backward != 0 && backward != 1) {
+    set_err(ctx, "as_set_inverse_mode: 0 (forward) or 1 (back-substitution)");
+    return AS_E_ARG;
+  }
+  if (backward && ctx->k_tol > 0 && ctx->k_max > 32) {
+    set_err(ctx, "as_set_inverse_mode: back-substitution supports k_max <= 32");
+    return AS_E_ARG;
+  }
+  ctx->inv_backward = backward;
+  return AS_OK;
+}
+
 as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max) {
   if (!ctx) return AS_E_ARG;
   if (!std::isfinite(k_tol) || (k_tol > 0 && (k_max < 8 || k_max > 64))) {
     set_err(ctx, "as_set_matrixinv: k_tol finite, k_max in [8, 64] (got %g, %d)", k_tol, k_max);
+    return AS_E_ARG;
+  }
+  if (ctx->inv_backward && k_tol > 0 && k_max > 32) {
+    set_err(ctx, "as_set_matrixinv: back-substitution mode supports k_max <= 32");
     return AS_E_ARG;
   }
   ctx->k_tol = k_tol > 0 ? k_tol : 0.0;

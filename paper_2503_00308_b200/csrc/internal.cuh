@@ -230,6 +230,7 @@ struct SetupArgs {
   const float* priv_lo;       // [N][3] private mean offsets (NEXT-2) or nullptr
   const float* priv_hi;
   int ns;                     // shared variables (privates are ns .. ns+2)
+  int inv_backward;           // NEXT-4: conic bounds by back-substitution
 };
 
 void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st);

@@ -350,6 +350,14 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
     P[e] = E[e];
     S[e] = E[e];
   }
+  // NEXT-4 back-substitution needs the forward bounds of every P^i entry (level 1 = E)
+  constexpr int KB = 33;
+  double Bl[KB][4], Bh[KB][4];
+  const bool bwd = A.inv_backward != 0;
+  if (bwd) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) L.conc(E[e], Bl[1][e], Bh[1][e]);
+  }
 #pragma unroll 1
   for (int it = 2; it <= k_warp; ++it) {
     const bool acc = it <= k_own;  // beyond this Gaussian's order: computed, not summed
@@ -377,6 +385,17 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
         S[2 * a + 1].u += q1.u;
       }
     }
+    if (bwd) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        double lo, hi;
+        L.conc(P[e], lo, hi);
+        if (it < KB) {
+          Bl[it][e] = lo;
+          Bh[it][e] = hi;
+        }
+      }
+    }
   }
   const double nx0 = sqrt(X0[0] * X0[0] + X0[1] * X0[1] + X0[2] * X0[2] + X0[3] * X0[3]);
   const double rs = ok ? rho : 0.0;
@@ -392,6 +411,72 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
       L.add_const(xp, -eps, eps);      // l.6-7, union
       conic[2 * a + b] = xp;
     }
+  if (bwd && ok) {
+    // NEXT-4 (reading O17): each conic entry's lower / upper affine bound by propagating its
+    // coefficients backwards through Xp = X0 + X0 sum_i P^i, P^i = P^{i-1} E (R1 planes, R2 at
+    // i = 2 on the diagonal, forward bounds of the operands) down to E, affine in xi.  The
+    // recursion is on scalars (uniform over the lanes); the final substitution per lane.
+#pragma unroll 1
+    for (int out = 0; out < 4; ++out) {
+      const int oa = out >> 1, ob = out & 1;
+#pragma unroll 1
+      for (int side = 0; side < 2; ++side) {
+        const double sg = side == 0 ? 1.0 : -1.0;  // lower bound of sg * Conic_ab
+        double init[4] = {0.0, 0.0, 0.0, 0.0};
+        init[0 + ob] = sg * X0[2 * oa];      // coefficient on P^i_{0 ob}
+        init[2 + ob] = sg * X0[2 * oa + 1];  // on P^i_{1 ob}
+        double lam[4], mu[4] = {0.0, 0.0, 0.0, 0.0};
+        double cst = sg * X0[out];  // i = 0: X0 . I
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lam[e] = init[e];
+#pragma unroll 1
+        for (int it = k_own; it >= 2; --it) {
+          double nxt[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) nxt[e] = init[e];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int dd = 0; dd < 2; ++dd) {
+              const double lm = lam[2 * c + dd];
+              if (lm == 0.0) continue;
+#pragma unroll
+              for (int l = 0; l < 2; ++l) {
+                const double xl = Bl[it - 1][2 * c + l], xh = Bh[it - 1][2 * c + l];
+                const double yl = Bl[1][2 * l + dd], yh = Bh[1][2 * l + dd];
+                if (it == 2 && c == l && l == dd) {  // E_cc * E_cc: R2
+                  if (lm >= 0) {
+                    const double pp = fmin(fmax(0.0, xl), xh);
+                    mu[2 * c + c] += lm * 2.0 * pp;
+                    cst -= lm * pp * pp;
+                  } else {
+                    mu[2 * c + c] += lm * (xl + xh);
+                    cst -= lm * xl * xh;
+                  }
+                } else {  // R1 planes
+                  const double yy = lm >= 0 ? yl : yh;
+                  nxt[2 * c + l] += lm * yy;
+                  mu[2 * l + dd] += lm * xl;
+                  cst -= lm * xl * yy;
+                }
+              }
+            }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) lam[e] = nxt[e];
+        }
+        double rl = L.cst() ? cst : 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double ce = mu[e] + lam[e];  // P^1 = E
+          rl += ce * (ce >= 0 ? E[e].l : E[e].u);
+        }
+        if (side == 0)
+          conic[out].l = rl - (L.cst() ? eps : 0.0);
+        else
+          conic[out].u = -rl + (L.cst() ? eps : 0.0);
+      }
+    }
+  }
   // ---- l.9 pieces: W = Mmul(Conic, Mp) (G4), D2 = Mul(d,d), DU = Mul(d, up)
   HotRec<NV>* H = reinterpret_cast<HotRec<NV>*>(A.hot) + i;
   float wv[6][2];

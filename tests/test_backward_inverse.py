@@ -106,3 +106,26 @@ def test_pipeline_backward_sound_and_tighter(oracle):
         e, t, sh = H.pose_of(w, p)
         img = oracle.render_concrete(w, euler=e, t=t, shifts=sh)
         assert np.all(lo <= img + 1e-9) and np.all(img <= hi + 1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,kw", [("C4", dict(N=6000, res=72)), ("C3", dict(N=5000, res=56)),
+                                     ("C1", {})])
+def test_gpu_backward_parity(oracle, name, kw):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    w = make_config(name, **kw)
+    w.pose_box = dict(w.pose_box, inv_backward=1)
+    with Context(0) as ctx:
+        ctx.load_workload(w)
+        lo, hi, st = ctx.as_render_bounds(w.tile, w.batch)
+        olo, ohi, ost = oracle.render_bounds(w)
+        err = max(np.abs(lo.cpu().numpy() - olo).max(), np.abs(hi.cpu().numpy() - ohi).max())
+        assert err <= 1e-4, err
+        assert st["fails"] == ost["fails"] and st["pairs"] == ost["pairs"]
+        # tighter than the forward conic on the same context
+        ctx.as_set_inverse_mode(0)
+        flo, fhi, _ = ctx.as_render_bounds(w.tile, w.batch)
+        assert H.mpg(lo.cpu().numpy(), hi.cpu().numpy()) <= H.mpg(flo.cpu().numpy(), fhi.cpu().numpy()) + 1e-9
