@@ -400,6 +400,7 @@ def run_ours(args):
                            "gpu_sample_mpg": float(gap[m].mean()),
                            "max_abs_diff_vs_oracle_sample": float(d.max())})
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "image_px_per_s": W * H / (ms / 1000.0),  # final-image pixels (P sub-boxes each)
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "f32", "data": "synthetic",
