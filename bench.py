@@ -205,7 +205,8 @@ def count_launches(step):
             # the library's kernels (its own and the CUB sorts / scans it launches); not NCCL's
             # collectives or torch's
             if (dt is not None and "CUDA" in str(dt) and not e.name.startswith(("Memcpy", "Memset"))
-                    and "nccl" not in e.name.lower() and "at::" not in e.name):
+                    and "nccl" not in e.name.lower()
+                    and not e.name.startswith(("void at::", "at::")) and "at::native" not in e.name):
                 n += 1
                 names[e.name] = names.get(e.name, 0) + 1
         return n, names
