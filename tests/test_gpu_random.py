@@ -1,0 +1,58 @@
+"""Randomised GPU parity sweep: reduced workloads of every config with random pose boxes
+(translation / rotation widths, partitions), tile sizes, batches and sizes that are not multiples
+of the tile, against the fp64 oracle at 1e-4 with equal integer statistics."""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    name = ["C1", "C2", "C3", "C4", "C5"][seed % 5]
+    res = int(rng.integers(20, 70))
+    N = int(rng.integers(200, 3000)) if name != "C1" else int(rng.integers(4, 40))
+    w = make_config(name, N=N, res=res)
+    pb = dict(w.pose_box)
+    pb["eps_t"] = [float(rng.choice([0.0, rng.uniform(0, 0.03)])) for _ in range(3)]
+    pb["eps_R"] = [float(rng.choice([0.0, math.radians(rng.uniform(0, 0.3))])) for _ in range(3)]
+    if not any(pb["eps_t"]) and not any(pb["eps_R"]):
+        pb["eps_t"][0] = 0.01
+    parts = [1] * 6
+    var = [a for a in range(6) if (pb["eps_t"] + pb["eps_R"])[a] > 0]
+    if rng.uniform() < 0.4:
+        parts[int(rng.choice(var))] = int(rng.integers(2, 4))
+    pb["parts"] = parts
+    w.pose_box = pb
+    tile = int(rng.choice([8, 16, 32]))
+    batch = int(rng.choice([1, 5, 16, 24, 64]))
+    return w, tile, batch
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_parity(ctx, oracle, seed):
+    w, tile, batch = _case(seed)
+    ctx.load_workload(w)
+    lo, hi, st = ctx.as_render_bounds(tile, batch)
+    olo, ohi, ost = oracle.render_bounds(w, tile=tile)
+    lo, hi = lo.cpu().numpy(), hi.cpu().numpy()
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= 1e-4, (seed, w.name, tile, batch, err)
+    for k in ("pairs", "active_pairs", "uncertain_pairs", "fails", "dropped"):
+        assert st[k] == ost[k], (seed, k, st[k], ost[k])
+    assert st["order_violations"] == 0
