@@ -50,7 +50,7 @@ __host__ __device__ __forceinline__ int pix_of(int x, int y, int bx) {
   return bx == 16 ? ((y >> 2) * 2 + (x >> 3)) * 32 + (y & 3) * 8 + (x & 7) : y * 8 + x;
 }
 constexpr int FB = 48;           // finalisation records staged in shared memory per batch
-constexpr int EG8 = 28;          // E_G operands precomputed per staged finalisation record
+constexpr int EG8 = 60;          // E_G operands precomputed per staged finalisation record
 constexpr int TL8 = 32;          // T_hi window operands precomputed per position
 
 template <int NV>
