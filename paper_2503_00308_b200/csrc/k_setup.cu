@@ -130,9 +130,10 @@ void launch_pose(const BoxParams& bp, PoseDev* out, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------------- k_setup
-// Layout: 8 lanes (n <= 7) or 16 lanes per Gaussian, lane k holding coefficient k of the
-// lower and the upper affine function of every form (k < NV: slope of xi_k, k == NV:
-// constant, k > NV: zero padding).  Concretisation is a shuffle reduction over the group.  This keeps the
+// Layout: 4 lanes (n <= 3), 8 lanes (n <= 7) or 16 lanes per Gaussian, lane k holding
+// coefficient k of the lower and the upper affine function of every form (k < NV: slope of
+// xi_k, k == NV: constant, k > NV: zero padding).  Concretisation is a shuffle reduction over
+// the group.  This keeps the
 // ~40 live forms of Alg. 1 + MatrixInv in registers (2 doubles per form per lane) instead
 // of spilling ~10 KB per thread.  All control flow is uniform across the Gaussians of a
 // warp (selects, no data-dependent branches) so the shuffles stay converged.
@@ -143,10 +144,10 @@ struct HL {  // this lane's coefficient of a form: lower, upper
   double l, u;
 };
 
-// lanes per Gaussian: 8 when the n + 1 coefficients fit (n <= 7), else 16
+// lanes per Gaussian: 4 when the n + 1 coefficients fit (n <= 3), 8 (n <= 7), else 16
 template <int NV>
 constexpr int lanes_for() {
-  return (NV + 1 <= 8) ? 8 : 16;
+  return (NV + 1 <= 4) ? 4 : ((NV + 1 <= 8) ? 8 : 16);
 }
 
 template <int W>
@@ -588,8 +589,8 @@ __global__ void __launch_bounds__(128) k_setup(SetupArgs A) {
 }
 
 void launch_setup(int nv, const SetupArgs& a, cudaStream_t st) {
-  const int threads = 128;  // 16 (n <= 7) or 8 Gaussians per block
-  const int64_t total = a.N * (nv + 1 <= 8 ? 8 : 16);
+  const int threads = 128;  // 32 (n <= 3), 16 (n <= 7) or 8 Gaussians per block
+  const int64_t total = a.N * (nv + 1 <= 4 ? 4 : (nv + 1 <= 8 ? 8 : 16));
   const unsigned blocks = (unsigned)((total + threads - 1) / threads);
   if (a.N <= 0) return;
   switch (nv) {
