@@ -271,7 +271,7 @@ struct PairArgs {
   unsigned long long* tilemax;  // [ntiles] max over the tile's list of w + S' (ordered bits)
   double* wsP;            // [M] w + S' of the Gaussian at each position
   double* kapP;           // [M] kappa at each position
-  double* posD;           // [M][2(NV+1)] depth form at each position
+  double* posD;           // [2(NV+1)][M] depth form at each position (coefficient-major)
   int32_t* nF;            // [M]
   int32_t* nG;            // [M]
   int64_t* ntot;          // [M+1] nF + nG (scanned into off)

@@ -139,14 +139,15 @@ template <int NV>
 struct DForm {
   double l[NV + 1], u[NV + 1];
 };
+// posD is coefficient-major ([2(NV+1)][M]): the window scans of neighbouring positions read
+// neighbouring entries, so a warp's load of one coefficient is contiguous
 template <int NV>
-__device__ __forceinline__ DForm<NV> load_posd(const double* posD, int64_t q) {
+__device__ __forceinline__ DForm<NV> load_posd(const double* posD, int64_t M, int64_t q) {
   DForm<NV> f;
-  const double* D = posD + (size_t)q * 2 * (NV + 1);
 #pragma unroll
   for (int k = 0; k <= NV; ++k) {
-    f.l[k] = D[k];
-    f.u[k] = D[NV + 1 + k];
+    f.l[k] = posD[(size_t)k * M + q];
+    f.u[k] = posD[(size_t)(NV + 1 + k) * M + q];
   }
   return f;
 }
@@ -249,11 +250,10 @@ __global__ void k_pairs_prep(PairArgs A) {
     A.kapP[p] = Pi.kappa;
     // position-ordered copy of the depth form: the window scans then read neighbours
     // contiguously instead of gathering PairRec by Gaussian id
-    double* D = A.posD + (size_t)p * 2 * (NV + 1);
 #pragma unroll
     for (int k = 0; k <= NV; ++k) {
-      D[k] = Pi.dl[k];
-      D[NV + 1 + k] = Pi.du[k];
+      A.posD[(size_t)k * A.M + p] = Pi.dl[k];
+      A.posD[(size_t)(NV + 1 + k) * A.M + p] = Pi.du[k];
     }
   }
   // tile max of ws (ws >= 0, so its bit pattern orders like the value): positions are
@@ -315,7 +315,7 @@ __global__ void k_pairs(PairArgs A) {
   const uint32_t t = A.keys[p];
   const int64_t b = A.tbegin[t], e = A.tend[t];
   const int32_t gi = A.vals[p];
-  const DForm<NV> Pi = load_posd<NV>(A.posD, p);
+  const DForm<NV> Pi = load_posd<NV>(A.posD, A.M, p);
   const double ki = A.kapP[p];
   const double M = __longlong_as_double((long long)A.tilemax[t]);
   const double factor = A.tileh[(size_t)t * (NVMAX + 1) + NVMAX];
@@ -329,7 +329,7 @@ __global__ void k_pairs(PairArgs A) {
     const double kj = A.kapP[q];
     if (beyond(ki - kj, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj, A.ns);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, A.M, q), gj, A.ns);
     if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
       if (c == 0) ++viol;
       if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
@@ -348,7 +348,7 @@ __global__ void k_pairs(PairArgs A) {
     const double kj = A.kapP[q];
     if (beyond(kj - ki, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
-    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, q), gj, A.ns);
+    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, A.M, q), gj, A.ns);
     if (c == -1 || c == 1) {
       if (c == 1) ++viol;
       if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);
