@@ -529,30 +529,30 @@ __global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4*
     const int s = k * target, e = min(K, s + target);
     int A = s, L = e, wmax = 0;
     bool exc = false;
-    if (pm)
-      for (int base = s; base < e; base += 32) {
-        const int i = base + lane;
-        int a = s, l = e, wl = 0;
-        bool ex = false;
-        if (i < e) {
-          const int4 m = pm[b + i];
-          if (m.x != 0) {
-            ex = true;
-            if (m.x & PM_EF) a = min(a, m.y);
-            if (m.x & PM_EG) l = max(l, m.z + 1);
-            wl = max(i - m.y, m.z - i);
-          }
+    if (pm) {
+      // each lane folds a strided share of the chunk (loads pipelined), one reduction per chunk
+      int a = s, l = e, wl = 0;
+      bool ex = false;
+#pragma unroll 4
+      for (int i = s + lane; i < e; i += 32) {
+        const int4 m = pm[b + i];
+        if (m.x != 0) {
+          ex = true;
+          if (m.x & PM_EF) a = min(a, m.y);
+          if (m.x & PM_EG) l = max(l, m.z + 1);
+          wl = max(wl, max(i - m.y, m.z - i));
         }
-        for (int sh = 16; sh > 0; sh >>= 1) {
-          a = min(a, __shfl_xor_sync(0xffffffffu, a, sh));
-          l = max(l, __shfl_xor_sync(0xffffffffu, l, sh));
-          wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, sh));
-        }
-        A = min(A, a);
-        L = max(L, l);
-        wmax = max(wmax, wl);
-        exc |= __any_sync(0xffffffffu, ex);
       }
+      for (int sh = 16; sh > 0; sh >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, sh));
+        l = max(l, __shfl_xor_sync(0xffffffffu, l, sh));
+        wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, sh));
+      }
+      A = min(A, a);
+      L = max(L, l);
+      wmax = max(wmax, wl);
+      exc = __any_sync(0xffffffffu, ex);
+    }
     int lr = 0;
     while ((1 << lr) <= wmax) ++lr;
     const int Anext = (k == n - 1) ? e : prevA;
