@@ -66,9 +66,10 @@ struct alignas(16) SRec {
   //   q_hi,k = phi + du0 q0hi + du1 q1hi + x0 wm0 + |x0| wr0 + x1 wm1 + |x1| wr1
   // stored as mid / radius:  q_lo,k = m - r,  q_hi,k = m + r  with
   //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
-  float pm[3][CP], pr[3][CP], q0m[3][CP], q0r[3][CP], q1m[3][CP], q1r[3][CP];
-  float wm0[3][CP], wr0[3][CP], wm1[3][CP], wr1[3][CP];
-  float wcm[6], wcd[6];     // concretised W, [a*3+c]: (lo + hi) / 2, (lo - hi) / 2
+  // kept as (mid, radius) pairs so both evaluate with one packed FFMA2 per term:
+  //   P = (pm, pr), Q0 = (q0m, q0r), Q1 = (q1m, q1r), W0 = (wm0, wr0), W1 = (wm1, wr1)
+  float2 P[3][CP], Q0[3][CP], Q1[3][CP], W0[3][CP], W1[3][CP];
+  float2 WC[6];             // concretised W, [a*3+c]: ((lo + hi) / 2, (lo - hi) / 2)
   float o[2];
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
@@ -115,8 +116,7 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
   if (part == NPART - 1) {
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
-      S.wcm[e] = (float)(0.5 * (wl[e] + wh[e]));
-      S.wcd[e] = (float)(0.5 * (wl[e] - wh[e]));
+      S.WC[e] = make_float2((float)(0.5 * (wl[e] + wh[e])), (float)(0.5 * (wl[e] - wh[e])));
     }
   }
 #pragma unroll 1
@@ -147,25 +147,22 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
       const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
       const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q1lo = w1l * (w1l >= 0 ? d2l : d2h);
       const double q0hi = w0h * (w0h >= 0 ? d2h : d2l), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
-      S.pm[c][k] = (float)(0.5 * (plo + phi));
-      S.pr[c][k] = (float)(0.5 * (phi - plo));
-      S.q0m[c][k] = (float)(0.5 * (q0lo + q0hi));
-      S.q0r[c][k] = (float)(0.5 * (q0hi - q0lo));
-      S.q1m[c][k] = (float)(0.5 * (q1lo + q1hi));
-      S.q1r[c][k] = (float)(0.5 * (q1hi - q1lo));
+      S.P[c][k] = make_float2((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)));
+      S.Q0[c][k] = make_float2((float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+      S.Q1[c][k] = make_float2((float)(0.5 * (q1lo + q1hi)), (float)(0.5 * (q1hi - q1lo)));
       const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
-      S.wm0[c][k] = (float)(0.5 * (a0 + b0));
-      S.wr0[c][k] = (float)(0.5 * (b0 - a0));
-      S.wm1[c][k] = (float)(0.5 * (a1 + b1));
-      S.wr1[c][k] = (float)(0.5 * (b1 - a1));
+      S.W0[c][k] = make_float2((float)(0.5 * (a0 + b0)), (float)(0.5 * (b0 - a0)));
+      S.W1[c][k] = make_float2((float)(0.5 * (a1 + b1)), (float)(0.5 * (b1 - a1)));
     }
   }
 }
 
-// steps 14-17 for one pixel at offset (du0, du1) from the block centre: (a_lo, a_hi)
+// steps 14-16 for one pixel at offset (du0, du1) from the block centre: the lower / upper
+// forms of s as pairs S[k] = (s_lo,k, s_hi,k).  (m, r) pairs and the (s_lo, s_hi) pairs each
+// take one packed FFMA2 per term, in the same order as the scalar formulas.
 template <int NV>
-__device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1, float& alo,
-                                        float& ahi) {
+__device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
+                                        float2 (&S)[NV + 1]) {
   constexpr int C = NV + 1;
   // 14: concretised lower bound of x_a = Add(Mul(d,d,u_a), -Mul(d, up_a))
   float x0 = fmaf(du0, R.d2lo[NV], R.xb[0][NV]);
@@ -175,32 +172,28 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
     x0 -= fabsf(fmaf(du0, R.d2lo[k], R.xb[0][k]));
     x1 -= fabsf(fmaf(du1, R.d2lo[k], R.xb[1][k]));
   }
-  const float ax0 = fabsf(x0), ax1 = fabsf(x1);
+  const float2 D0 = make_float2(du0, du0), D1 = make_float2(du1, du1);
+  const float2 X0 = make_float2(x0, fabsf(x0)), X1 = make_float2(x1, fabsf(x1));
+  const float2 Y0 = make_float2(-x0, x0), Y1 = make_float2(-x1, x1);
   // 15-16: q_c = mul(x0, W_0c) + mul(x1, W_1c) (R1); s = sum_c sq(q_c) (R2)
-  float sl[C], sh[C];
 #pragma unroll
-  for (int k = 0; k < C; ++k) sl[k] = sh[k] = 0.f;
+  for (int k = 0; k < C; ++k) S[k] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     float ql[C], qh[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      float m = fmaf(du0, R.q0m[c][k], R.pm[c][k]);
-      m = fmaf(du1, R.q1m[c][k], m);
-      m = fmaf(x0, R.wm0[c][k], m);
-      m = fmaf(x1, R.wm1[c][k], m);
-      float r = fmaf(du0, R.q0r[c][k], R.pr[c][k]);
-      r = fmaf(du1, R.q1r[c][k], r);
-      r = fmaf(ax0, R.wr0[c][k], r);
-      r = fmaf(ax1, R.wr1[c][k], r);
+      // m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
+      float2 mr = __ffma2_rn(D0, R.Q0[c][k], R.P[c][k]);
+      mr = __ffma2_rn(D1, R.Q1[c][k], mr);
+      mr = __ffma2_rn(X0, R.W0[c][k], mr);
+      mr = __ffma2_rn(X1, R.W1[c][k], mr);
       if (k == NV) {  // constant: q_lo -= x0 W_lo,0c + x1 W_lo,1c, q_hi -= x0 W_hi,0c + x1 W_hi,1c
-        m = fmaf(-x0, R.wcm[c], m);
-        m = fmaf(-x1, R.wcm[3 + c], m);
-        r = fmaf(x0, R.wcd[c], r);
-        r = fmaf(x1, R.wcd[3 + c], r);
+        mr = __ffma2_rn(Y0, R.WC[c], mr);
+        mr = __ffma2_rn(Y1, R.WC[3 + c], mr);
       }
-      ql[k] = m - r;
-      qh[k] = m + r;
+      ql[k] = mr.x - mr.y;
+      qh[k] = mr.x + mr.y;
     }
     float qmin = ql[NV], qmax = qh[NV];
 #pragma unroll
@@ -211,19 +204,25 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
     const float p = fminf(fmaxf(0.f, qmin), qmax);
     const float tp = 2.f * p, sm = qmin + qmax;
     const bool pa = tp >= 0.f, pb = sm >= 0.f;
+    const float2 T = make_float2(tp, sm);
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      sl[k] = fmaf(tp, pa ? ql[k] : qh[k], sl[k]);
-      sh[k] = fmaf(sm, pb ? qh[k] : ql[k], sh[k]);
-    }
-    sl[NV] -= p * p;
-    sh[NV] -= qmin * qmax;
+    for (int k = 0; k < C; ++k)
+      S[k] = __ffma2_rn(T, make_float2(pa ? ql[k] : qh[k], pb ? qh[k] : ql[k]), S[k]);
+    S[NV] = __ffma2_rn(make_float2(-p, -qmin), make_float2(p, qmax), S[NV]);
   }
-  float smin = sl[NV], smax = sh[NV];
+}
+
+// steps 14-17 for one pixel at offset (du0, du1) from the block centre: (a_lo, a_hi)
+template <int NV>
+__device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1, float& alo,
+                                        float& ahi) {
+  float2 S[NV + 1];
+  s_forms<NV>(R, du0, du1, S);
+  float smin = S[NV].x, smax = S[NV].y;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    smin -= fabsf(sl[k]);
-    smax += fabsf(sh[k]);
+    smin -= fabsf(S[k].x);
+    smax += fabsf(S[k].y);
   }
   smin = fmaxf(smin, 0.f);
   // 17: a = o * Exp(-s/2) concretised (O11)
@@ -235,55 +234,12 @@ __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1,
 template <int NV>
 __device__ __forceinline__ void opacity_sforms(const SRec<NV>& R, float du0, float du1,
                                                float (&sl)[NV + 1], float (&sh)[NV + 1]) {
-  constexpr int C = NV + 1;
-  float x0 = fmaf(du0, R.d2lo[NV], R.xb[0][NV]);
-  float x1 = fmaf(du1, R.d2lo[NV], R.xb[1][NV]);
+  float2 S[NV + 1];
+  s_forms<NV>(R, du0, du1, S);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    x0 -= fabsf(fmaf(du0, R.d2lo[k], R.xb[0][k]));
-    x1 -= fabsf(fmaf(du1, R.d2lo[k], R.xb[1][k]));
-  }
-  const float ax0 = fabsf(x0), ax1 = fabsf(x1);
-#pragma unroll
-  for (int k = 0; k < C; ++k) sl[k] = sh[k] = 0.f;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    float ql[C], qh[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      float m = fmaf(du0, R.q0m[c][k], R.pm[c][k]);
-      m = fmaf(du1, R.q1m[c][k], m);
-      m = fmaf(x0, R.wm0[c][k], m);
-      m = fmaf(x1, R.wm1[c][k], m);
-      float r = fmaf(du0, R.q0r[c][k], R.pr[c][k]);
-      r = fmaf(du1, R.q1r[c][k], r);
-      r = fmaf(ax0, R.wr0[c][k], r);
-      r = fmaf(ax1, R.wr1[c][k], r);
-      if (k == NV) {
-        m = fmaf(-x0, R.wcm[c], m);
-        m = fmaf(-x1, R.wcm[3 + c], m);
-        r = fmaf(x0, R.wcd[c], r);
-        r = fmaf(x1, R.wcd[3 + c], r);
-      }
-      ql[k] = m - r;
-      qh[k] = m + r;
-    }
-    float qmin = ql[NV], qmax = qh[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      qmin -= fabsf(ql[k]);
-      qmax += fabsf(qh[k]);
-    }
-    const float p = fminf(fmaxf(0.f, qmin), qmax);
-    const float tp = 2.f * p, sm = qmin + qmax;
-    const bool pa = tp >= 0.f, pb = sm >= 0.f;
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      sl[k] = fmaf(tp, pa ? ql[k] : qh[k], sl[k]);
-      sh[k] = fmaf(sm, pb ? qh[k] : ql[k], sh[k]);
-    }
-    sl[NV] -= p * p;
-    sh[NV] -= qmin * qmax;
+  for (int k = 0; k <= NV; ++k) {
+    sl[k] = S[k].x;
+    sh[k] = S[k].y;
   }
 }
 
