@@ -58,7 +58,7 @@ struct alignas(16) SRec {
   static constexpr int C = NV + 1;
   static constexpr int CP = (C + 3) & ~3;  // padded for 16-byte vector loads
   // x_a lower forms (for the concretised x_lo_a only): B_a + du_a * D2_lo
-  float xb[2][CP];
+  float2 XB[CP];            // (B_lo,0, B_lo,1) per coefficient
   float d2lo[CP];
   // q_c = mul(x0, W_0c) + mul(x1, W_1c) with the x-side McCormick terms folded into affine
   // functions of the pixel offset du, and the W-side terms in mid / radius form:
@@ -137,8 +137,7 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
       wb[e] = H->w[e][1][k];
     }
     // x lower forms
-    S.xb[0][k] = (float)blo[0];
-    S.xb[1][k] = (float)blo[1];
+    S.XB[k] = make_float2((float)blo[0], (float)blo[1]);
     S.d2lo[k] = (float)d2l;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -165,12 +164,14 @@ __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
                                         float2 (&S)[NV + 1]) {
   constexpr int C = NV + 1;
   // 14: concretised lower bound of x_a = Add(Mul(d,d,u_a), -Mul(d, up_a))
-  float x0 = fmaf(du0, R.d2lo[NV], R.xb[0][NV]);
-  float x1 = fmaf(du1, R.d2lo[NV], R.xb[1][NV]);
+  const float2 DU = make_float2(du0, du1);
+  const float2 xc = __ffma2_rn(DU, make_float2(R.d2lo[NV], R.d2lo[NV]), R.XB[NV]);
+  float x0 = xc.x, x1 = xc.y;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    x0 -= fabsf(fmaf(du0, R.d2lo[k], R.xb[0][k]));
-    x1 -= fabsf(fmaf(du1, R.d2lo[k], R.xb[1][k]));
+    const float2 v = __ffma2_rn(DU, make_float2(R.d2lo[k], R.d2lo[k]), R.XB[k]);
+    x0 -= fabsf(v.x);
+    x1 -= fabsf(v.y);
   }
   const float2 D0 = make_float2(du0, du0), D1 = make_float2(du1, du1);
   const float2 X0 = make_float2(x0, fabsf(x0)), X1 = make_float2(x1, fabsf(x1));
@@ -181,6 +182,7 @@ __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     float ql[C], qh[C];
+    float2 MR[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       // m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
@@ -192,6 +194,7 @@ __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
         mr = __ffma2_rn(Y0, R.WC[c], mr);
         mr = __ffma2_rn(Y1, R.WC[3 + c], mr);
       }
+      MR[k] = mr;
       ql[k] = mr.x - mr.y;
       qh[k] = mr.x + mr.y;
     }
@@ -203,11 +206,13 @@ __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
     }
     const float p = fminf(fmaxf(0.f, qmin), qmax);
     const float tp = 2.f * p, sm = qmin + qmax;
-    const bool pa = tp >= 0.f, pb = sm >= 0.f;
-    const float2 T = make_float2(tp, sm);
+    // tp sel(ql, qh) = tp m - |tp| r and sm sel(qh, ql) = sm m + |sm| r
+    const float2 T = make_float2(tp, sm), TA = make_float2(-fabsf(tp), fabsf(sm));
 #pragma unroll
-    for (int k = 0; k < C; ++k)
-      S[k] = __ffma2_rn(T, make_float2(pa ? ql[k] : qh[k], pb ? qh[k] : ql[k]), S[k]);
+    for (int k = 0; k < C; ++k) {
+      S[k] = __ffma2_rn(T, make_float2(MR[k].x, MR[k].x), S[k]);
+      S[k] = __ffma2_rn(TA, make_float2(MR[k].y, MR[k].y), S[k]);
+    }
     S[NV] = __ffma2_rn(make_float2(-p, -qmin), make_float2(p, qmax), S[NV]);
   }
 }
