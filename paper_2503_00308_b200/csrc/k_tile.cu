@@ -74,7 +74,8 @@ struct alignas(16) SRec {
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
   int pmf, ph, pg, pnF, pnG;  // position metadata (PM_*, h, g, |E_F|, |E_G|)
-  int pfb, pfe;             // finalisation records [pfb, pfe) relative to the batch's first
+  int pfb, pfe;             // finalisation records [pfb, pfe) (absolute: F0 is subtracted in
+                            // the walk, so phase A does not wait for the batch's F0 load)
   long long peoff;          // offset of E_F(p) then E_G(p) in exc[]
   unsigned long long mf0, mf1;  // E_F(p) bits over [h, h+128)
   // precomputed ring operands of the T_hi window: positions h + tlo[t]
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
   __shared__ unsigned s_skip[8];
+  __shared__ int s_F[2];
   const int ts = A.ts;
   const int nsbx = ts / SBX;        // blocks per tile row
   const int nsub = nsbx * (ts / SBY);
@@ -424,9 +426,14 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
 
     for (int b0 = scan0; b0 < scan1; b0 += BS) {
       const int nb = min(BS, scan1 - b0);
-      // finalisation records of the batch: fin_rec[F0, F1) (sorted by finalising position)
-      const int F0 = iexc ? A.finstart[tb + b0] : 0;
-      const int F1 = iexc ? A.finstart[tb + b0 + nb] : 0;
+      // finalisation records of the batch: fin_rec[F0, F1) (sorted by finalising position);
+      // thread 0 loads the bounds now and publishes them through shared memory after its
+      // phase A work, so no thread waits on (or spills) them
+      int f0l = 0, f1l = 0;
+      if (threadIdx.x == 0 && iexc) {
+        f0l = A.finstart[tb + b0];
+        f1l = A.finstart[tb + b0 + nb];
+      }
       __syncthreads();
       // ---- phase A: fp64 record -> block-centred fp32 forms, whole-block cull (same exact
       //      test as the per-pixel one, on the block rectangle) into the skip ring, cull
@@ -461,8 +468,8 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
             S.pnF = m.w;
             S.pnG = A.nG[gp];
             S.peoff = A.eoff[gp];
-            S.pfb = A.finstart[gp] - F0;
-            S.pfe = A.finstart[gp + 1] - F0;
+            S.pfb = A.finstart[gp];
+            S.pfe = A.finstart[gp + 1];
             const ulonglong2 mf = A.mF[gp];
             S.mf0 = mf.x;
             S.mf1 = mf.y;
@@ -498,6 +505,10 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
           }
         }
         if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+      }
+      if (threadIdx.x == 0) {
+        s_F[0] = f0l;
+        s_F[1] = f1l;
       }
       __syncthreads();
       // ---- phase B (needs the batch's skip bits): T_hi window operands per position and
@@ -537,7 +548,8 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         }
       }
       // finalisation records of the batch with their ring operands (skip-filtered)
-      for (int t = (int)threadIdx.x - 32; t < min(F1 - F0, FB); t += SBP - 32) {
+      const int F0 = s_F[0];
+      for (int t = (int)threadIdx.x - 32; t < min(s_F[1] - F0, FB); t += SBP - 32) {
         if (t < 0) break;
         const FinRec fr = A.fin_rec[F0 + t];
         FinS& F = fins[t];
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         Tl = fmaf(-Tl, ahi, Tl);
         // finalise deferred lower contributions of earlier partners whose last later
         // partner is q:  T_lo(q') = T_lo,before(q') prod_{r in E_G(q')} (1 - a_hi,r)
-        for (int f = R.pfb; f < R.pfe; ++f) {
+        for (int f = R.pfb - F0; f < R.pfe - F0; ++f) {
           float tl;
           const float* clo;
           if (f < FB) {
