@@ -193,6 +193,14 @@ as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
  * as_render_subboxes); AS_E_ARG otherwise. */
 as_status as_set_blend(as_ctx* ctx, int32_t mode);
 
+/* ---- work split (performance knob, like tile and batch) ----
+ * A tile's sorted Gaussian list is cut into chunks of `target` positions that the tile kernel
+ * processes independently and composes front to back; target = 0 (default)
+ * picks it from the list lengths and the grid (about six chunks per CTA), any other value
+ * >= 1 fixes it (clamped to at least the batch size).  The bounds do not depend on it beyond
+ * fp32 rounding of the composition. */
+as_status as_set_chunk_target(as_ctx* ctx, int32_t target);
+
 /* ---- tile sharding over ranks (PAPER.md:602-603 tiles; north_star: tiles across GPUs) ----
  * Every rank holds the full scene and runs the per-Gaussian setup; image tiles are
  * assigned to ranks by a deterministic longest-processing-time rule over per-tile Gaussian

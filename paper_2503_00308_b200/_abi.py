@@ -98,6 +98,7 @@ def lib():
         "as_set_subboxes": (i32, [P, i32, P]),
         "as_subbox_fails": (i32, [P, i32, P]),
         "as_set_matrixinv": (i32, [P, C.c_double, i32]),
+        "as_set_chunk_target": (i32, [P, i32]),
         "as_set_blend": (i32, [P, i32]),
         "as_set_inverse_mode": (i32, [P, i32]),
     }

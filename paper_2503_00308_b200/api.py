@@ -256,6 +256,10 @@ class Context:
         """Adaptive MatrixInv order: smallest k >= 8 with Eps <= k_tol (<= k_max); 0 = fixed 8."""
         self._check(self._L.as_set_matrixinv(self._ctx, float(k_tol), int(k_max)))
 
+    def as_set_chunk_target(self, target: int = 0):
+        """Positions per (tile, chunk) work item; 0 = automatic (performance knob only)."""
+        self._check(self._L.as_set_chunk_target(self._ctx, int(target)))
+
     def as_set_blend(self, mode: int = 0):
         """0: interval blend; 1: + linear-relation blend on exception-free tiles (n <= 3)."""
         self._check(self._L.as_set_blend(self._ctx, int(mode)))

@@ -67,6 +67,7 @@ struct as_ctx {
   // explicit partition (as_set_subboxes): host copy [n][9][2] and its device mirror
   std::vector<double> sub_host;
   DevBuf subs;
+  int chunk_target = 0;  // as_set_chunk_target (0 = automatic)
   double k_tol = 0.0;  // as_set_matrixinv (adaptive Taylor order)
   int k_max = 8;
   int inv_backward = 0;  // as_set_inverse_mode (NEXT-4 back-substitution)
@@ -585,9 +586,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
     ensure(ctx, ctx->scratch, (size_t)grid * per);
   }
-  const int target = (int)std::max<int64_t>(
-      std::max<int64_t>(2 * bs, 2 * (int64_t)ctx->last_wmax + 2),
-      M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1);
+  const int target =
+      ctx->chunk_target > 0
+          ? std::max(ctx->chunk_target, bs)
+          : (int)std::max<int64_t>(2 * bs, M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1);
   int64_t* caps = P<int64_t>(ctx->ntot);  // reuse: int64 [ntiles+1]
   ensure(ctx, ctx->ntot, sizeof(int64_t) * (std::max<int64_t>(M, G.ntiles) + 1));
   caps = P<int64_t>(ctx->ntot);
@@ -1040,6 +1042,16 @@ as_status as_set_blend(as_ctx* ctx, int32_t mode) {
     return AS_E_ARG;
   }
   ctx->blend_mode = mode;
+  return AS_OK;
+}
+
+as_status as_set_chunk_target(as_ctx* ctx, int32_t target) {
+  if (!ctx) return AS_E_ARG;
+  if (target < 0) {
+    set_err(ctx, "as_set_chunk_target: target >= 0 (0 = automatic), got %d", target);
+    return AS_E_ARG;
+  }
+  ctx->chunk_target = target;
   return AS_OK;
 }
 

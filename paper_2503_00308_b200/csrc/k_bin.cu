@@ -508,7 +508,8 @@ void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t 
 // only feed the chunk's transmittance and exception factors.  Chunks then compose front
 // to back with multiplications only:  pc = sum_k P(<A_k) S_k,  P(<A_{k+1}) = P(<A_k) Rk,
 // where S_k is the chunk's sum relative to A_k and Rk its running product at A_{k+1}
-// (target > 2 * max window keeps A_{k+1} inside chunk k's scan).  One warp per tile.
+// (A is made non-decreasing, A_k <= A_{k+1}, so A_{k+1} lies inside chunk k's scan
+// [A_k, L_k) for any chunk length).  One warp per tile.
 //   items[i]  = {tile, s, e, flags | log2(ring length) << 8}
 //   items2[i] = {A, L, A_next, 0}
 __global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
@@ -556,6 +557,9 @@ __global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4*
     int lr = 0;
     while ((1 << lr) <= wmax) ++lr;
     const int Anext = (k == n - 1) ? e : prevA;
+    // scan starts must not decrease (chunk k records its running product at A_{k+1} inside
+    // its own scan): extend the lookback to the next chunk's start when that reaches further
+    if (k < n - 1) A = min(A, prevA);
     if (lane == 0) {
       int fl = (exc ? IT_EXC : 0) | (n == 1 ? IT_SINGLE : 0) | (lr << 8);
       items[o + k] = make_int4(t, s, e, fl);

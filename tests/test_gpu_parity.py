@@ -61,6 +61,28 @@ def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
         assert np.abs(lo - base_lo).max() <= TOL and np.abs(hi - base_hi).max() <= TOL
 
 
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_chunk_target_is_a_performance_knob(ctx, oracle, name):
+    """Cutting tile lists into short chunks (down to one batch, so lookback / lookahead margins
+    of uncertain windows span several chunks and the scan starts are extended) composes to the
+    same bounds, and to the oracle's."""
+    w = make_config(name, **SMALL[name])
+    olo, ohi, _ = oracle.render_bounds(w)
+    base_lo, base_hi, _ = gpu_render(ctx, w)
+    try:
+        for target in (1, 5, 24, 100):
+            ctx.as_set_chunk_target(target)
+            lo, hi, st = gpu_render(ctx, w)
+            assert st["n_items"] > 0
+            assert max(np.abs(lo - base_lo).max(), np.abs(hi - base_hi).max()) <= 1e-5, target
+            assert max(np.abs(lo - olo).max(), np.abs(hi - ohi).max()) <= TOL, target
+    finally:
+        ctx.as_set_chunk_target(0)
+    from paper_2503_00308_b200.api import AbsplatError
+    with pytest.raises(AbsplatError):
+        ctx.as_set_chunk_target(-1)
+
+
 def test_parity_full_c2(ctx, oracle):
     """Full-size C2 (100k Gaussians, 200x200) against the oracle's full image."""
     w = make_config("C2")
