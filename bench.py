@@ -241,6 +241,8 @@ def run_ours(args):
     ctx.load_workload(w)
     if args.blend == "linear":
         ctx.as_set_blend(1)
+    if args.chunk_target:
+        ctx.as_set_chunk_target(args.chunk_target)
     lo = torch.empty((H, W, 3), dtype=torch.float32, device=f"cuda:{dev}")
     hi = torch.empty_like(lo)
     shard = args.shard
@@ -409,7 +411,8 @@ def run_ours(args):
                           "res": f"{W}x{H}", "n_vars": n, "sub_boxes": P, "tile": tile,
                           "batch": batch, "setup_dtype": "f64",
                           "l2": "flushed before every timed step (512 MiB write)",
-                          "parallelism": parallelism, "blend": args.blend},
+                          "parallelism": parallelism, "blend": args.blend,
+                          "chunk_target": args.chunk_target or "auto"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": gpu_launches, "launch_kernels": names, "clocks": clocks,
                "bound_width": widths,
@@ -439,6 +442,8 @@ def main():
                     help="multi-GPU axis: image tiles (all-gather) or sub-box ranges "
                          "(all-reduce min/max); auto = sub-boxes when P >= world")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--chunk-target", type=int, default=0,
+                    help="positions per (tile, chunk) work item (0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -586,10 +586,13 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
     ensure(ctx, ctx->scratch, (size_t)grid * per);
   }
-  const int target =
-      ctx->chunk_target > 0
-          ? std::max(ctx->chunk_target, bs)
-          : (int)std::max<int64_t>(2 * bs, M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1);
+  // automatic: about six chunks per CTA; with windows beyond the 128-position masks (long
+  // exception lists, per-position cost growing with the window) six times more, so the few
+  // expensive tiles split finely enough to balance (C5: 14.4 -> 5.3 ms)
+  int64_t auto_target = M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1;
+  auto_target = has_exc && ctx->last_wmax > 128 ? std::max<int64_t>(bs, auto_target / 6)
+                                                 : std::max<int64_t>(2 * bs, auto_target);
+  const int target = ctx->chunk_target > 0 ? std::max(ctx->chunk_target, bs) : (int)auto_target;
   int64_t* caps = P<int64_t>(ctx->ntot);  // reuse: int64 [ntiles+1]
   ensure(ctx, ctx->ntot, sizeof(int64_t) * (std::max<int64_t>(M, G.ntiles) + 1));
   caps = P<int64_t>(ctx->ntot);
