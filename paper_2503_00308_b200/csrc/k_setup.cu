@@ -211,7 +211,7 @@ struct Lane {
 }  // namespace
 
 template <int NV>
-__global__ void __launch_bounds__(128, 3) k_setup(SetupArgs A) {
+__global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
   __shared__ PoseDev sp;
   __shared__ unsigned long long s_wsmax;
   if (threadIdx.x == 0) s_wsmax = 0ull;
