@@ -437,10 +437,11 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
       __syncthreads();
       // ---- phase A: fp64 record -> block-centred fp32 forms, whole-block cull (same exact
       //      test as the per-pixel one, on the block rectangle) into the skip ring, cull
-      //      tables and position metadata.  Four threads per Gaussian (stage_forms splits
-      //      the coefficients); each evaluates the cull, part 3 records it.
-      for (int jj = threadIdx.x; jj < NPART * nb; jj += SBP) {
-        const int j = jj / NPART, part = jj % NPART;
+      //      tables and position metadata.  Metadata and cull tables: one thread per
+      //      Gaussian, taken from the highest thread ids (idle in the staging loop when
+      //      NPART * nb < SBP); staging: four threads per Gaussian (stage_forms splits the
+      //      coefficients).  Every thread evaluates the cull itself.
+      for (int j = SBP - 1 - (int)threadIdx.x; j < nb; j += SBP) {
         const int64_t gp = tb + b0 + j;
         const int32_t g = A.vals[gp];
         const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
@@ -453,58 +454,66 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
           const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
           skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
         }
-        if (part == NPART - 1) {
-          const int bit = (b0 + j) & 255;
-          if (skip)
-            atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
-          else
-            atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
-          int pmf = 0;
-          if (iexc) {
-            const int4 m = A.pm[gp];
-            pmf = m.x;
-            S.ph = m.y;
-            S.pg = m.z;
-            S.pnF = m.w;
-            S.pnG = A.nG[gp];
-            S.peoff = A.eoff[gp];
-            S.pfb = A.finstart[gp];
-            S.pfe = A.finstart[gp + 1];
-            const ulonglong2 mf = A.mF[gp];
-            S.mf0 = mf.x;
-            S.mf1 = mf.y;
-          } else {
-            S.pfb = S.pfe = 0;
+        const int bit = (b0 + j) & 255;
+        if (skip)
+          atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
+        else
+          atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
+        int pmf = 0;
+        if (iexc) {
+          const int4 m = A.pm[gp];
+          pmf = m.x;
+          S.ph = m.y;
+          S.pg = m.z;
+          S.pnF = m.w;
+          S.pnG = A.nG[gp];
+          S.peoff = A.eoff[gp];
+          S.pfb = A.finstart[gp];
+          S.pfe = A.finstart[gp + 1];
+          const ulonglong2 mf = A.mF[gp];
+          S.mf0 = mf.x;
+          S.mf1 = mf.y;
+        } else {
+          S.pfb = S.pfe = 0;
+        }
+        S.tmode = 0;
+        S.nT = 0;
+        S.pmf = pmf;
+        S.flags = H->flags | (skip ? F_SKIP : 0);
+        S.r2 = r2;
+        // colours / opacity are read by the blend even for skipped (a = 0) entries
+        S.o[0] = H->o[0];
+        S.o[1] = H->o[1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          S.clo[c] = H->clo[c];
+          S.chi[c] = H->chi[c];
+        }
+        if (!skip) {
+#pragma unroll
+          for (int l = 0; l < SBX; ++l) {
+            const double x = ox + l + 0.5;
+            const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+            cx2[j * SBX + l] = __dmul_rn(dx, dx);
           }
-          S.tmode = 0;
-          S.nT = 0;
-          S.pmf = pmf;
-          S.flags = H->flags | (skip ? F_SKIP : 0);
-          S.r2 = r2;
-          // colours / opacity are read by the blend even for skipped (a = 0) entries
-          S.o[0] = H->o[0];
-          S.o[1] = H->o[1];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            S.clo[c] = H->clo[c];
-            S.chi[c] = H->chi[c];
-          }
-          if (!skip) {
-#pragma unroll
-            for (int l = 0; l < SBX; ++l) {
-              const double x = ox + l + 0.5;
-              const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
-              cx2[j * SBX + l] = __dmul_rn(dx, dx);
-            }
-#pragma unroll
-            for (int l = 0; l < SBY; ++l) {
-              const double y = oy + l + 0.5;
-              const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-              cy2[j * SBY + l] = __dmul_rn(dy, dy);
-            }
+          for (int l = 0; l < SBY; ++l) {
+            const double y = oy + l + 0.5;
+            const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+            cy2[j * SBY + l] = __dmul_rn(dy, dy);
           }
         }
-        if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+      }
+      for (int jj = threadIdx.x; jj < NPART * nb; jj += SBP) {
+        const int j = jj / NPART, part = jj % NPART;
+        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
+        bool skip;
+        {
+          const double dx = fmax(0.0, fmax(__dsub_rn(H->mu[0], bx1), __dsub_rn(bx0, H->mu[2])));
+          const double dy = fmax(0.0, fmax(__dsub_rn(H->mu[1], by1), __dsub_rn(by0, H->mu[3])));
+          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
+        }
+        if (!skip) stage_forms<NV>(srec[j], H, ucx, ucy, part);
       }
       if (threadIdx.x == 0) {
         s_F[0] = f0l;
