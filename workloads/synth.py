@@ -299,7 +299,7 @@ def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -
                     shift_lo=np.array([0.0]), shift_hi=np.array([0.05]), parts=[1, 1, 1],
                     col_lo=col_lo, col_hi=col_hi, op_lo=None, op_hi=None)
         box = _pose_box(eps_t=(0.01, 0, 0), t_frame=1)
-        return _pack("C5", mean, chol, o, c, cam, box, scene_box=sbox, tile=8, batch=64,
+        return _pack("C5", mean, chol, o, c, cam, box, scene_box=sbox, tile=8, batch=32,
                      description="C2 scene + blade mean/colour box + camera-x +-1 cm")
     if name == "C3":
         n = 300_000 if N is None else N
