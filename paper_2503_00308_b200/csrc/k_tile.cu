@@ -641,7 +641,8 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         // E_F factors when that is numerically safe (both products far from underflow),
         // else fall back to the window product (H3).
         float tbv = Tb;
-        if (main && (pmf & PM_EF) && !(flags & F_SKIP)) {
+        // (a_hi = 0 on this pixel: its upper contribution is exactly 0, no T_hi needed)
+        if (main && (pmf & PM_EF) && !(flags & F_SKIP) && ahi > 0.f) {
           const int wlen = qpos - R.ph;
           if (!(pmf & PM_OVF)) {
             bool done = false;
