@@ -702,6 +702,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
             if (F.qq < 0) continue;  // another chunk's position, or culled in this block
             clo = F.clo;
             tl = rf[RS<SBP>(F.qq, 3, rmask)];
+            if (tl == 0.f) continue;  // q' missed this pixel (a_lo = 0): the term is exactly 0
             if (F.n >= 0) {
               tl *= 1.f - ahi;  // g itself
 #pragma unroll 4
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
             if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
             clo = fr.clo;
             tl = rf[RS<SBP>(fr.qq, 3, rmask)];
+            if (tl == 0.f) continue;
             if (!(fr.flags & PM_OVF)) {
               tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
             } else {
