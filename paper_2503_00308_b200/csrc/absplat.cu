@@ -529,15 +529,16 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
         launch_pairs_fill(pa, st);
         LAUNCHED(ctx, 1);
       }
-      ensure(ctx, ctx->diff, sizeof(int32_t) * 2 * (M + 1));
+      ensure(ctx, ctx->diff, sizeof(int32_t) * 3 * (M + 1));
       ensure(ctx, ctx->cover, sizeof(int32_t) * 2 * (M + 1));
       ensure(ctx, ctx->pflag, sizeof(int4) * M);
       int32_t* dstore = P<int32_t>(ctx->diff);
       int32_t* dcut = dstore + (M + 1);
+      int32_t* hstart = dcut + (M + 1);
       int32_t* cstore = P<int32_t>(ctx->cover);
       int32_t* ccut = cstore + (M + 1);
-      CK(cudaMemsetAsync(dstore, 0, sizeof(int32_t) * 2 * (M + 1), st));
-      launch_mark(pa, dstore, dcut, st);
+      CK(cudaMemsetAsync(dstore, 0, sizeof(int32_t) * 3 * (M + 1), st));
+      launch_mark(pa, dstore, dcut, hstart, st);
       LAUNCHED(ctx, 1);
       cub_inclusive_sum(ctx, dstore, cstore, M + 1);
       cub_inclusive_sum(ctx, dcut, ccut, M + 1);
@@ -549,7 +550,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ensure(ctx, ctx->finval2, sizeof(int32_t) * M);
       ensure(ctx, ctx->finstart, sizeof(int32_t) * (M + 1));
       ensure(ctx, ctx->finrec, sizeof(FinRec) * M);
-      launch_meta(pa, cstore, ccut, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
+      launch_meta(pa, cstore, ccut, hstart, P<int4>(ctx->pflag), wmax, P<uint32_t>(ctx->finkey),
                   P<int32_t>(ctx->finval), st);
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),

@@ -23,7 +23,7 @@ constexpr double WCAP = 1e12;   // |W| guard -> FAIL (reading O3)
 
 enum : int { F_DROP = 1, F_STRADDLE = 2, F_FAIL = 4, F_SKIP = 8 };  // F_SKIP: staging-only
 // per list-position flags (exceptions, a9) and work-item flags
-enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8, PM_OVF = 16 };
+enum : int { PM_EF = 1, PM_EG = 2, PM_STORE = 4, PM_NOCUT = 8, PM_OVF = 16, PM_HSTART = 32 };
 enum : int { IT_EXC = 1, IT_SINGLE = 2 };
 
 // ------------------------------------------------------------------------- pose / box
@@ -288,7 +288,8 @@ struct PairArgs {
 void launch_pairs_prep(const PairArgs& a, cudaStream_t st);
 void launch_pairs_count(const PairArgs& a, cudaStream_t st);
 void launch_pairs_fill(const PairArgs& a, cudaStream_t st);
-void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t st);
+void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, int32_t* hstart,
+                 cudaStream_t st);
 // finalisation record of a position q' with later uncertain partners (sorted by max E_G)
 struct alignas(16) FinRec {
   int qq, nF, nG, flags;   // tile-local position, |E_F|, |E_G|, PM_* flags
@@ -297,8 +298,9 @@ struct alignas(16) FinRec {
   ulonglong2 mg;           // E_G(q') as bits over (q', q'+128]
   float clo[3], pad;       // lower colour of q'
 };
-void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st);
+void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut,
+                 const int32_t* hstart, int4* pm, unsigned int* wmax, uint32_t* finkey,
+                 int32_t* finval, cudaStream_t st);
 void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
                    const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
 void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st);

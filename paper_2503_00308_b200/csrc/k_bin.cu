@@ -403,8 +403,10 @@ void launch_pairs_fill(const PairArgs& a, cudaStream_t st) {
 //   * its T_hi window [h_p, p] (h_p = min E_F(p), or p) must be kept in the ring: every
 //     position inside some window is flagged PM_STORE (difference array `dstore`);
 //   * a chunk boundary between b-1 and b must not separate an uncertain pair (q < b <= p):
-//     positions b in (h_p, p] are flagged PM_NOCUT (difference array `dcut`).
-__global__ void k_mark(PairArgs A, int32_t* dstore, int32_t* dcut) {
+//     positions b in (h_p, p] are flagged PM_NOCUT (difference array `dcut`);
+//   * the window start h_p itself is flagged PM_HSTART (the only positions whose running
+//     T_hi the ring must keep).
+__global__ void k_mark(PairArgs A, int32_t* dstore, int32_t* dcut, int32_t* hstart) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
   const int nF = A.nF[p], nG = A.nG[p];
@@ -414,19 +416,22 @@ __global__ void k_mark(PairArgs A, int32_t* dstore, int32_t* dcut) {
   atomicAdd(&dstore[b + h], 1);
   atomicAdd(&dstore[p + 1], -1);
   if (nF > 0) {
+    hstart[b + h] = 1;
     atomicAdd(&dcut[b + h + 1], 1);
     atomicAdd(&dcut[p + 1], -1);
   }
 }
-void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, cudaStream_t st) {
+void launch_mark(const PairArgs& a, int32_t* dstore, int32_t* dcut, int32_t* hstart,
+                 cudaStream_t st) {
   if (a.M <= 0) return;
-  k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, dstore, dcut);
+  k_mark<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, dstore, dcut, hstart);
 }
 
 // per-position metadata for the tile kernel: {flags, h, g, nF}; max window -> wmax;
 // E_F(p) as a 128-bit mask over [h, h+128) and E_G(p) over (p, p+128] (PM_OVF if longer)
-__global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                       unsigned int* wmax, uint32_t* finkey, int32_t* finval) {
+__global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut,
+                       const int32_t* hstart, int4* pm, unsigned int* wmax, uint32_t* finkey,
+                       int32_t* finval) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
   const int nF = A.nF[p], nG = A.nG[p];
@@ -435,17 +440,19 @@ __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut, i
   const int h = A.hpos[p], g = A.gpos[p];
   const bool ovf = (loc - h) > 128 || (g - loc) > 128;
   int fl = (nF ? PM_EF : 0) | (nG ? PM_EG : 0) | (cstore[p] > 0 ? PM_STORE : 0) |
-           (ccut[p] > 0 ? PM_NOCUT : 0) | (ovf ? PM_OVF : 0);
+           (ccut[p] > 0 ? PM_NOCUT : 0) | (ovf ? PM_OVF : 0) | (hstart[p] ? PM_HSTART : 0);
   pm[p] = make_int4(fl, h, g, nF);
   warp_max_u32(wmax, (unsigned)max(loc - h, g - loc));
   // deferred lower contribution of p is finalised at its last later partner b + g
   finkey[p] = nG ? (uint32_t)(b + g) : 0xffffffffu;
   finval[p] = (int32_t)p;
 }
-void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut, int4* pm,
-                 unsigned int* wmax, uint32_t* finkey, int32_t* finval, cudaStream_t st) {
+void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut,
+                 const int32_t* hstart, int4* pm, unsigned int* wmax, uint32_t* finkey,
+                 int32_t* finval, cudaStream_t st) {
   if (a.M <= 0) return;
-  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, pm, wmax, finkey, finval);
+  k_meta<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a, cstore, ccut, hstart, pm, wmax, finkey,
+                                                          finval);
 }
 
 // finalisation records in sorted order: everything the tile kernel needs about q'

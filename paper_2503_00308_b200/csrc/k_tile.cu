@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
           // (1 - a_hi) is read only through E_G of earlier partners (q has PM_EF), the
           // deferred lower term only at q's own finalisation (PM_EG)
           const int rs = RS<SBP>(qpos, 0, rmask);
-          rf[rs] = Tb;
+          if (pmf & PM_HSTART) rf[rs] = Tb;  // read only as some window's base
           rf[rs + SBP] = 1.f - alo;
           if (pmf & PM_EF) rf[rs + 2 * SBP] = 1.f - ahi;
           if (pmf & PM_EG) rf[rs + 3 * SBP] = Tl * alo;
