@@ -158,8 +158,9 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
 }
 
 // steps 14-16 for one pixel at offset (du0, du1) from the block centre: the lower / upper
-// forms of s as pairs S[k] = (s_lo,k, s_hi,k).  (m, r) pairs and the (s_lo, s_hi) pairs each
-// take one packed FFMA2 per term, in the same order as the scalar formulas.
+// forms of s as pairs S[k] = (s_lo,k, s_hi,k).  Each (m, r) term is one packed FFMA2 (same
+// order as the scalar formulas); R2's plane selection LS(q, 2p) / US(q, qmin + qmax) is
+// written select-free as tp m - |tp| r and sm m + |sm| r (two FFMA2 per coefficient).
 template <int NV>
 __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
                                         float2 (&S)[NV + 1]) {
