@@ -554,7 +554,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
                   P<int32_t>(ctx->finval), st);
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
-                      P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, 32, false);
+                      P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, bits_for(M), false);
       launch_fin_start(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->finstart), st);
       LAUNCHED(ctx, 1);
       launch_finrec(P<uint32_t>(ctx->finkey2), P<int32_t>(ctx->finval2), pa, P<int4>(ctx->pflag),

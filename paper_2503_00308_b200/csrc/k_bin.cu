@@ -444,7 +444,7 @@ __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut,
   pm[p] = make_int4(fl, h, g, nF);
   warp_max_u32(wmax, (unsigned)max(loc - h, g - loc));
   // deferred lower contribution of p is finalised at its last later partner b + g
-  finkey[p] = nG ? (uint32_t)(b + g) : 0xffffffffu;
+  finkey[p] = nG ? (uint32_t)(b + g) : (uint32_t)A.M;  // no finalisation: sorts last
   finval[p] = (int32_t)p;
 }
 void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut,
@@ -461,7 +461,7 @@ __global__ void k_finrec(const uint32_t* key, const int32_t* val, PairArgs A, co
                          const ulonglong2* mG, const void* hot, FinRec* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.M) return;
-  if (key[i] == 0xffffffffu) return;
+  if (key[i] >= (uint32_t)A.M) return;
   const int32_t gq = val[i];
   const int64_t b = A.tbegin[A.keys[gq]];
   const int4 m = pm[gq];
@@ -487,14 +487,14 @@ void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, c
 }
 
 // CSR of the finalisation lists over ALL positions: fin_rec[fs[p] .. fs[p+1]) are the
-// records finalised at p (fs[p] = lower bound of p in the sorted keys; no-fin keys sort last
-// as 0xffffffff and count as M).  Thread i fills fs over the key gap (key[i-1], key[i]].
+// records finalised at p (fs[p] = lower bound of p in the sorted keys; no-fin keys are M and
+// sort last).  Thread i fills fs over the key gap (key[i-1], key[i]].
 __global__ void k_fin_start(const uint32_t* key, int64_t M, int32_t* fs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i > M) return;
   auto K = [&](int64_t j) -> int64_t {
     const uint32_t k = key[j];
-    return k == 0xffffffffu ? M : (int64_t)k;
+    return k >= (uint64_t)M ? M : (int64_t)k;
   };
   const int64_t lo = i == 0 ? -1 : K(i - 1);
   const int64_t hi = i == M ? M : K(i);
