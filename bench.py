@@ -38,9 +38,17 @@ FP32_LANES = 128
 
 
 def f_ops(n: int) -> int:
-    """FP32 arithmetic ops (FMA = 1) of steps 14-19 per active (pixel, Gaussian) pair for n
-    box variables: x forms 4(n+1), conc x 4n, q McCormick 24(n+1)+12,
-    conc q 6n, squares 6(n+1)+15, conc s 2n+1, opacity 4, blend 10."""
+    """Algorithmic FP32 ops (FMA = 1) of steps 14-19 per active (pixel, Gaussian) pair for n
+    box variables, SURVEY.md §8(d)'s count (the roofline headline): x forms 4(n+1), conc x
+    4n, McCormick into q 24(n+1), conc q 6n, square forms 6(n+1), conc s 2n, +4 for the
+    exponent scaling / o multiply and +14 for the blend: 34(n+1) + 12n + 18 (328 at n = 6)."""
+    return 34 * (n + 1) + 12 * n + 18
+
+
+def f_ops_recount(n: int) -> int:
+    """The builder's recount of the same steps from the final oracle: the
+    McCormick constants and the square's constant terms add 12 + 15 + 1 - 4 ops:
+    34(n+1) + 12n + 42 (352 at n = 6).  Reported beside the headline, not instead of it."""
     return 34 * (n + 1) + 12 * n + 42
 
 
@@ -135,6 +143,24 @@ def oracle_sample(w, tiles, nthreads=0):
     return lo, hi, st, dt
 
 
+def oracle_full_image(w, tiles, nthreads=0):
+    """The oracle timed on the host cores as it stands, extrapolated to the whole image: the
+    per-Gaussian setup of every sub-box is timed alone (a render of no tile), the tile sample
+    with it, and the full-image time is t_setup + (t_sample - t_setup) * n_tiles / k.  Both
+    the cpu_baseline leg and the reference arm use this, so their values compare with each
+    other and with the GPU's full-image rate (the sample size changes only the noise).
+    Returns (full-image px/s, sample outputs, details)."""
+    _, nt = sample_tiles(w, 1.0)
+    t_setup = oracle_sample(w, np.zeros(0, np.int32), nthreads)[3]
+    lo, hi, st, t_k = oracle_sample(w, tiles, nthreads)
+    per_tile = max(t_k - t_setup, 1e-9) / max(len(tiles), 1)
+    full = t_setup + per_tile * nt
+    px = w.camera["W"] * w.camera["H"] * w.n_sub
+    det = {"t_setup_s": t_setup, "t_sample_s": t_k, "per_tile_s": per_tile,
+           "full_image_s": full, "sample_tiles": int(len(tiles)), "n_tiles": int(nt)}
+    return px / full, (lo, hi, st), det
+
+
 def tile_mask(w, tiles):
     tile = w.tile
     ntx = -(-w.camera["W"] // tile)
@@ -153,27 +179,26 @@ def run_reference(args):
         return 0
     w = make_config(args.config)
     P = w.n_sub
-    # size each step so the whole run ends within a few minutes
+    # size each step so the whole run ends within a few minutes: probe setup and tile cost
     nsteps = args.steps + args.warmup
     target = max(2.0, min(20.0, 150.0 / max(nsteps, 1)))
     _, nt = sample_tiles(w, 1.0)
-    t1 = oracle_sample(w, np.array([0], np.int32))[3]
-    t3 = oracle_sample(w, np.array([0, nt // 2, nt - 1], np.int32))[3]
-    per_tile = max((t3 - t1) / 2.0, 1e-3)
-    fixed = max(t1 - per_tile, 0.0)
-    k = int(max(1, min(nt, (target - fixed) / per_tile)))
+    _, _, det = oracle_full_image(w, np.array([0, nt // 2, nt - 1], np.int32))
+    k = int(max(1, min(nt, (target - 2 * det["t_setup_s"]) / det["per_tile_s"])))
     tiles, _ = sample_tiles(w, k / nt)
     for _ in range(args.warmup):
-        oracle_sample(w, tiles)
-    times = []
+        oracle_full_image(w, tiles)
+    vals, dets = [], []
     for _ in range(args.steps):
-        times.append(oracle_sample(w, tiles)[3])
-    px = int(tile_mask(w, tiles).sum()) * P
-    ms = 1000.0 * float(np.mean(times))
-    value = px / (ms / 1000.0)
+        v, _, d = oracle_full_image(w, tiles)
+        vals.append(v)
+        dets.append(d)
+    value = float(np.mean(vals))
+    ms = 1000.0 * w.camera["W"] * w.camera["H"] * P / value
     cores = os.cpu_count()
-    sample = (f"{len(tiles)} of {nt} tiles ({px // P} px x {P} sub-boxes) of {args.config}, "
-              f"evenly spaced; each step = full per-Gaussian setup + those tiles")
+    sample = (f"{len(tiles)} of {nt} tiles of {args.config} (evenly spaced) per step plus the full "
+              f"per-Gaussian setup of all {P} sub-boxes timed alone; value = full-image px/s "
+              f"extrapolated as t_setup + t_tiles * {nt}/{len(tiles)}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -182,7 +207,9 @@ def run_reference(args):
                        "res": f"{w.camera['W']}x{w.camera['H']}", "sub_boxes": P,
                        "tile": w.tile},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample,
+                             "t_setup_s": float(np.mean([d["t_setup_s"] for d in dets])),
+                             "per_tile_s": float(np.mean([d["per_tile_s"] for d in dets]))},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -317,7 +344,11 @@ def run_ours(args):
     roofline = {"bound": "alu", "kernel": "k_tile", "achieved": achieved / 1e12,
                 "peak": peak_ops / 1e12, "unit": "Tops/s (FP32 instr, FMA=1)",
                 "frac": achieved / peak_ops, "traffic": traffic,
-                "ops_per_active_pair": f_ops(n), "active_pairs_per_step": st["active_pairs"],
+                "ops_per_active_pair": f_ops(n), "ops_basis": "SURVEY.md §8(d): 34(n+1)+12n+18",
+                "frac_recount": (f_ops_recount(n) * st["active_pairs"] / (st["tile_kernel_ms"] / 1000.0)
+                                 / peak_ops if st["tile_kernel_ms"] > 0 else None),
+                "ops_per_active_pair_recount": f_ops_recount(n),
+                "active_pairs_per_step": st["active_pairs"],
                 "tile_kernel_ms_per_step": st["tile_kernel_ms"], "launches_per_step": st["n_sub"],
                 "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES} FP32 lanes x {sm_max:.0f} MHz "
                               "(MEASURED_PEAKS.json sm_max_mhz)",
@@ -390,13 +421,14 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             tiles, nt = sample_tiles(w, SAMPLE_FRACTION.get(args.config, 0.05))
-            olo, ohi, ost, dt = oracle_sample(w, tiles)
+            v, (olo, ohi, ost), det = oracle_full_image(w, tiles)
             m = tile_mask(w, tiles)
-            px = int(m.sum()) * P
-            cpu = {"value": px / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"{len(tiles)} of {nt} tiles of {args.config} ({int(m.sum())} px x "
-                             f"{P} sub-boxes), evenly spaced, incl. the full per-Gaussian setup",
-                   "seconds": dt}
+                             f"{P} sub-boxes, evenly spaced) plus the full per-Gaussian setup "
+                             f"timed alone; value = full-image px/s extrapolated as "
+                             f"t_setup + t_tiles * {nt}/{len(tiles)} (same rule as --impl "
+                             f"reference)", **det}
             d = np.maximum(np.abs(lo_np[m] - olo[m]), np.abs(hi_np[m] - ohi[m]))
             og = np.linalg.norm(ohi[m] - olo[m], axis=-1)
             widths.update({"oracle_sample_mpg": float(og.mean()),

@@ -248,6 +248,21 @@ typedef void* (*as_alloc_fn)(void* user, size_t bytes, void* stream);
 typedef void (*as_free_fn)(void* user, void* ptr, size_t bytes, void* stream);
 as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, void* user);
 
+/* ---- rare-path evidence (tests) ----
+ * enable = 1 makes subsequent renders count how often the tile kernel takes each slow path of
+ * the depth-exception machinery (rows a7/a9: Alg. 3 P:377-389 with uncertain Ind pairs,
+ * Table 2); 0 switches counting off; -1 leaves the setting.  out (host uint64
+ * [AS_DBG_N], may be NULL) receives the counts of the last render (zeros if counting was off):
+ *   0 upper-transmittance window re-multiplied from the 128-bit E_F mask (many operands or an
+ *     unsafe division), 1 division by the E_F factors refused (product below 1e-20 or running
+ *     product below 1e-25, reading H3), 2 window longer than 128 positions (global exception
+ *     lists), 3 such a window re-multiplied instead of divided, 4 finalisation with more than
+ *     60 E_G operands or a long list, 5 finalisation record beyond the 48 staged per batch,
+ *     6 finalisation through global E_G lists (window > 128), 7 T_hi window with more than 32
+ *     operands.  Counting costs atomics on those paths only. */
+#define AS_DBG_N 8
+as_status as_debug_counters(as_ctx* ctx, int32_t enable, uint64_t* out);
+
 /* Concrete render (Alg. 1 + BlendSort, reading G6/G8) at one point of the box: xi[n] in
  * [-1,1]^n are the box variables of the FULL box in order (perturbed axes tx,ty,tz,e0,e1,e2,
  * then group shifts), with the scene's nominal colours and opacities.  img: [H][W][3]

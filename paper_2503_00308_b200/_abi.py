@@ -101,6 +101,7 @@ def lib():
         "as_set_chunk_target": (i32, [P, i32]),
         "as_set_blend": (i32, [P, i32]),
         "as_set_inverse_mode": (i32, [P, i32]),
+        "as_debug_counters": (i32, [P, i32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -264,6 +264,16 @@ class Context:
         """0: interval blend; 1: + linear-relation blend on exception-free tiles (n <= 3)."""
         self._check(self._L.as_set_blend(self._ctx, int(mode)))
 
+    DEBUG_COUNTERS = ("thi_bits", "thi_div_unsafe", "thi_ovf", "thi_ovf_window", "fin_slow",
+                      "fin_unstaged", "fin_ovf", "tmode3")
+
+    def as_debug_counters(self, enable: int = -1):
+        """Rare-path counters of the last render (dict) and, with enable 0 / 1, switch
+        counting for later renders (include/absplat.h, as_debug_counters)."""
+        out = np.zeros(len(self.DEBUG_COUNTERS), np.uint64)
+        self._check(self._L.as_debug_counters(self._ctx, int(enable), out.ctypes.data))
+        return {k: int(v) for k, v in zip(self.DEBUG_COUNTERS, out)}
+
     def as_set_inverse_mode(self, backward: int = 0):
         """MatrixInv conic bounds: 0 forward forms, 1 back-substitution (NEXT-4)."""
         self._check(self._L.as_set_inverse_mode(self._ctx, int(backward)))

@@ -72,6 +72,8 @@ struct as_ctx {
   int k_max = 8;
   int inv_backward = 0;  // as_set_inverse_mode (NEXT-4 back-substitution)
   int blend_mode = 0;  // as_set_blend: 0 interval, 1 + linear on exception-free tiles
+  bool debug = false;  // as_debug_counters: rare-path counters of the tile kernel
+  DevBuf dbg;
   bool last_has_exc = false;
   int64_t last_M = 0;
   DevBuf tmp_lo, tmp_hi, tile_unc, lin_tiles;
@@ -580,6 +582,12 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   if (pt) CK(cudaEventRecord(ctx->ev[4], st));
   // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
   int grid = tile_grid(nv, G.ts, bs);
+  if (grid <= 0) {
+    (void)cudaGetLastError();
+    set_err(ctx, "tile kernel: shared-memory opt-in / occupancy query failed (n=%d, TS=%d, BS=%d)",
+            nv, G.ts, bs);
+    throw Err{AS_E_CUDA};
+  }
   const size_t npix = (size_t)G.ts * G.ts;
   if (has_exc) {  // ring memory: grid x R x threads float4 (cap the total at ~8 GB)
     const size_t per = (size_t)R * tile_threads(G.ts) * sizeof(float4);
@@ -648,6 +656,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.lo = lo;
   ta.hi = hi;
   ta.active = ctr + C_ACTIVE;
+  ta.dbg = ctx->debug ? P<unsigned long long>(ctx->dbg) : nullptr;
   ctx->last_items = (int)n_items;
   ctx->last_grid = grid;
   ctx->last_R = R;
@@ -726,6 +735,10 @@ void prepare_common(as_ctx* ctx, const BoxInfo& bi, const Geometry& G) {
   ensure(ctx, ctx->tslot, sizeof(int32_t) * G.ntiles);
   ensure(ctx, ctx->owner, sizeof(int32_t) * G.ntiles);
   CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, ctx->stream));
+  if (ctx->debug) {
+    ensure(ctx, ctx->dbg, sizeof(unsigned long long) * DBG_N);
+    CK(cudaMemsetAsync(ctx->dbg.p, 0, sizeof(unsigned long long) * DBG_N, ctx->stream));
+  }
   launch_pose(bi.bp, P<PoseDev>(ctx->pose), ctx->stream);
   LAUNCHED(ctx, 1);
 }
@@ -819,8 +832,11 @@ void tile_costs(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, std::vector<i
   CK(cudaStreamSynchronize(st));
   costs.assign(h.begin(), h.end());
   // counters of the cost pass must not leak into the render's stats; C_WSMAX (the pair
-  // window bound of the last sub-box's setup) stays valid for a render that reuses it
-  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_WSMAX, st));
+  // window bound of the last sub-box's setup) stays valid for a render that reuses it, and so
+  // do the setup's FAIL / straddle / drop counts when there is one sub-box (the render then
+  // skips its own setup)
+  if (bi.n_sub != 1) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_WSMAX, st));
+  else CK(cudaMemsetAsync(ctr + C_DROP + 1, 0, sizeof(unsigned long long) * (C_WSMAX - C_DROP - 1), st));
   CK(cudaMemsetAsync(ctr + C_WSMAX + 1, 0, sizeof(unsigned long long) * (C_NCOUNTERS - C_WSMAX - 1),
                      st));
 }
@@ -883,12 +899,31 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
                     &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->finstart, &ctx->finrec, &ctx->maskF,
-                    &ctx->maskG};
+                    &ctx->maskG, &ctx->dbg};
   for (DevBuf* b : bufs) release(ctx, *b);
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   delete ctx;
   return AS_OK;
+}
+
+as_status as_debug_counters(as_ctx* ctx, int32_t enable, uint64_t* out) {
+  if (!ctx) return AS_E_ARG;
+  try {
+    cudaSetDevice(ctx->device);
+    if (out) {
+      std::memset(out, 0, sizeof(uint64_t) * AS_DBG_N);
+      if (ctx->debug && ctx->dbg.p) {
+        CK(cudaMemcpyAsync(out, ctx->dbg.p, sizeof(uint64_t) * DBG_N, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+      }
+    }
+    if (enable >= 0) ctx->debug = enable != 0;
+    return AS_OK;
+  } catch (const Err& e) {
+    return e.st;
+  }
 }
 
 as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, void* user) {

@@ -345,7 +345,12 @@ struct TileArgs {
   float* lo;                  // row-major [H][W][3] (tile_slot == nullptr) or tile-major
   float* hi;
   unsigned long long* active; // active pair counter
+  unsigned long long* dbg;    // [DBG_N] rare-path counters (as_debug_counters) or nullptr
 };
+// rare-path counters of the tile kernel (as_debug_counters): evidence that every slow path
+// of the exception machinery runs in some parity case
+enum { DBG_THI_BITS = 0, DBG_THI_DIV_UNSAFE = 1, DBG_THI_OVF = 2, DBG_THI_OVF_WINDOW = 3,
+       DBG_FIN_SLOW = 4, DBG_FIN_UNSTAGED = 5, DBG_FIN_OVF = 6, DBG_TMODE3 = 7, DBG_N = 8 };
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st);
 void launch_merge(const TileArgs& a, cudaStream_t st);
 // NEXT-1 linear blend (n <= 3): intersect exception-free tiles' bounds in lo / hi

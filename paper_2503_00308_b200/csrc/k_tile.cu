@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
             for (; m1; m1 &= m1 - 1) S.tlo[nT++] = (unsigned char)(64 + __ffsll((long long)m1) - 1);
           } else {
             S.tmode = 3;
+            if (A.dbg) atomicAdd(A.dbg + DBG_TMODE3, 1ull);
           }
           S.nT = nT;
         }
@@ -660,15 +661,19 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
               if (dfac >= 1e-20f && Tb >= 1e-25f) {
                 tbv = Tb / dfac;
                 done = true;
+              } else if (A.dbg) {
+                atomicAdd(A.dbg + DBG_THI_DIV_UNSAFE, 1ull);
               }
             }
             if (!done) {  // many operands or unsafe division: window product from the bits
+              if (A.dbg) atomicAdd(A.dbg + DBG_THI_BITS, 1ull);
               const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
               const unsigned long long v1 =
                   wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
               tbv = rf[RS<SBP>(R.ph, 0, rmask)] * ring_prod<SBP>(rf, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask);
             }
           } else {  // long window: exception lists from global memory
+            if (A.dbg) atomicAdd(A.dbg + DBG_THI_OVF, 1ull);
             bool done = false;
             if (wlen > 2 * R.pnF + 8) {
               const float dfac = exc_prod<SBP>(rf, A.exc + R.peoff, R.pnF, 1, rmask);
@@ -677,6 +682,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
                 done = true;
               }
             }
+            if (!done && A.dbg) atomicAdd(A.dbg + DBG_THI_OVF_WINDOW, 1ull);
             if (!done)
               tbv = rf[RS<SBP>(R.ph, 0, rmask)] *
                     window_prod<SBP>(rf, R.ph, qpos, A.exc + R.peoff, R.pnF, rmask);
@@ -709,22 +715,26 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
 #pragma unroll 4
               for (int e = 0; e < F.n; ++e) tl *= rf[RS<SBP>(F.qq + F.off[e], 2, rmask)];
             } else {
+              if (A.dbg) atomicAdd(A.dbg + DBG_FIN_SLOW, 1ull);
               const FinRec& fr = A.fin_rec[F0 + f];
               if (!(fr.flags & PM_OVF)) {
                 tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
               } else {
+                if (A.dbg) atomicAdd(A.dbg + DBG_FIN_OVF, 1ull);
                 tl *= exc_prod<SBP>(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask);
               }
             }
           } else {
             const FinRec& fr = A.fin_rec[F0 + f];
             if (fr.qq < pbeg || fr.qq >= pend) continue;  // another chunk's position
+            if (A.dbg) atomicAdd(A.dbg + DBG_FIN_UNSTAGED, 1ull);
             clo = fr.clo;
             tl = rf[RS<SBP>(fr.qq, 3, rmask)];
             if (tl == 0.f) continue;
             if (!(fr.flags & PM_OVF)) {
               tl *= ring_prod<SBP>(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask);
             } else {
+              if (A.dbg) atomicAdd(A.dbg + DBG_FIN_OVF, 1ull);
               tl *= exc_prod<SBP>(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask);
             }
           }
@@ -1016,11 +1026,11 @@ size_t tile_smem_bytes(int nv, int ts, int bs) {
 
 template <int NV, int BX>
 static int grid_bx(int ts, int bs) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_tile<NV, BX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  // the dynamic shared-memory opt-in is per device: set it on the current one every time
+  // (a host-side attribute write), and report failure as grid 0
+  if (cudaFuncSetAttribute(k_tile<NV, BX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024) != cudaSuccess)
+    return 0;
   int per_sm = 0, dev = 0, nsm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<NV, BX>, BX * SBY,
                                                 smem_for<NV>(ts, bs));

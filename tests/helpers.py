@@ -112,3 +112,66 @@ def eval_form(f, n, xi):
 def mpg(lo, hi):
     """Mean Pixel Gap."""
     return float(np.linalg.norm(hi - lo, axis=-1).mean())
+
+
+D_MIN = 0.01  # near plane (reading G8)
+
+
+def concrete_render_np(w, e, t, shifts=None, tiebreak=True):
+    """Textbook 3DGS render at one pose in plain numpy fp64, independent of oracle/:
+    mu = K uc / d, Sigma_2D = Jc Sigma_c Jc^T with the EWA Jacobian Jc of the perspective map,
+    a = o exp(-1/2 (u - mu)^T Sigma_2D^-1 (u - mu)) at pixel centres u = index + 1/2 (G7),
+    Gaussians with d <= d_min culled (G8), front-to-back alpha blending in ascending depth
+    with ascending scene index on exact ties (Alg. 2 BlendSort; tie-break G6), black
+    background, no heuristics.  tiebreak=False blends equal depths with the
+    paper's strict Ind instead: tied Gaussians do not occlude each other."""
+    cam = w.camera
+    R = rot_c2w(e).T
+    uw = w.mean.astype(np.float64).copy()
+    if shifts is not None and w.scene_box is not None and w.scene_box["n_groups"] > 0:
+        g = w.scene_box["group_of"]
+        for k in range(w.scene_box["n_groups"]):
+            uw[g == k] += shifts[k] * np.asarray(w.scene_box["dir"][k], float)
+    uc = (uw - np.asarray(t, float)) @ R.T
+    d = uc[:, 2]
+    keep = d > D_MIN
+    c = w.chol.astype(np.float64)
+    n = len(c)
+    Mw = np.zeros((n, 3, 3))
+    Mw[:, 0, 0], Mw[:, 1, 0], Mw[:, 1, 1] = c[:, 0], c[:, 1], c[:, 2]
+    Mw[:, 2, 0], Mw[:, 2, 1], Mw[:, 2, 2] = c[:, 3], c[:, 4], c[:, 5]
+    Sw = Mw @ np.transpose(Mw, (0, 2, 1))
+    Sc = R[None] @ Sw @ R.T[None]
+    fx, fy, cx, cy = cam["fx"], cam["fy"], cam["cx"], cam["cy"]
+    ds = np.where(keep, d, 1.0)
+    Jc = np.zeros((n, 2, 3))
+    Jc[:, 0, 0] = fx / ds
+    Jc[:, 0, 2] = -fx * uc[:, 0] / ds ** 2
+    Jc[:, 1, 1] = fy / ds
+    Jc[:, 1, 2] = -fy * uc[:, 1] / ds ** 2
+    S2 = Jc @ Sc @ np.transpose(Jc, (0, 2, 1))
+    mu = np.stack([fx * uc[:, 0] / ds + cx, fy * uc[:, 1] / ds + cy], axis=1)
+    Si = np.linalg.inv(S2)
+    H, W = cam["H"], cam["W"]
+    ys, xs = np.mgrid[0:H, 0:W]
+    u = np.stack([xs + 0.5, ys + 0.5], axis=-1).reshape(-1, 2)
+    img = np.zeros((H * W, 3))
+    T = np.ones(H * W)
+    order = np.lexsort((np.arange(n), d))  # ascending depth, then index
+    ids = [i for i in order if keep[i]]
+    k = 0
+    while k < len(ids):
+        grp = [ids[k]]
+        while (not tiebreak and k + len(grp) < len(ids) and d[ids[k + len(grp)]] == d[ids[k]]):
+            grp.append(ids[k + len(grp)])
+        alphas = []
+        for i in grp:
+            r = u - mu[i]
+            s = np.einsum("pa,ab,pb->p", r, Si[i], r)
+            alphas.append(w.opacity[i] * np.exp(-0.5 * s))
+        for i, a in zip(grp, alphas):
+            img += (T * a)[:, None] * w.color[i].astype(np.float64)[None]
+        for a in alphas:
+            T = T * (1.0 - a)
+        k += len(grp)
+    return img.reshape(H, W, 3)

@@ -319,3 +319,84 @@ def make_config(name: str, N: Optional[int] = None, res: Optional[int] = None) -
         return _pack("C4", mean, chol, o, c, cam, box, tile=16, batch=24,
                      description="outdoor 750k, 800x800, 6-DoF box (t +-1 cm, Euler +-0.1 deg)")
     raise ValueError(f"unknown config {name!r}")
+
+
+# ----------------------------------------------------------------------------- edge-case scenes
+def nearplane_config(N: int = 48, res: int = 32, seed: int = 11, eps_tz: float = 4e-4,
+                     rot_deg: float = 0.0) -> Workload:
+    """Near-plane case (reading G8, d_min = 0.01): a C1-style random scene shrunk by 1/500 so
+    depths lie in [0.008, 0.012] m around d_min, with a camera-z translation box +-eps_tz
+    (optionally also a yaw box).  Gaussians with d_hi <= d_min are dropped, those whose depth
+    interval contains d_min 'straddle' (a_lo = 0, footprint from max(d_lo, d_min), O4), the
+    rest are ordinary.  The projection is scale invariant, so the nominal image is the
+    unshrunk scene's.  Nothing here evaluates the method."""
+    mean, chol, o, c = random_scene(seed, N, depth=(4.0, 6.0), xy=0.8, scale=(0.03, 0.12))
+    s = 1.0 / 500.0
+    mean = mean * s
+    chol = chol * s
+    f = float(res)
+    cam = dict(fx=f, fy=f, cx=res / 2.0, cy=res / 2.0, W=res, H=res, euler=[0.0, 0.0, 0.0],
+               t=[0.0, 0.0, 0.0])
+    box = _pose_box(eps_t=(0, 0, eps_tz), eps_R=(0, 0, math.radians(rot_deg)))
+    return _pack("near", mean, chol, o, c, cam, box, tile=16, batch=16,
+                 description=f"{N} Gaussians at depth 0.008-0.012 m, tz +-{eps_tz} m "
+                             f"(near plane d_min = 0.01)")
+
+
+def ties_config(N: int = 24, res: int = 32, seed: int = 12, rot_deg: float = 0.0,
+                eps_t: float = 0.01) -> Workload:
+    """Exact depth ties (reading G6, H4): a C1-style scene in which every Gaussian is
+    duplicated (same mean and covariance, a different colour and opacity), so each
+    duplicate pair has identical depth forms and an exact kappa tie, broken by the scene
+    index.  Box: camera-x translation +-eps_t (ties stay certain: d_i - d_j = 0 exactly) and,
+    with rot_deg > 0, a yaw box (identical non-constant forms: the pair is uncertain)."""
+    mean, chol, o, c = random_scene(seed, N, depth=(3.0, 5.0), xy=0.8, scale=(0.08, 0.3))
+    rng = np.random.default_rng(seed + 1000)
+    o2 = rng.uniform(0.3, 0.99, N)
+    c2 = rng.uniform(0, 1, (N, 3))
+    # interleave: Gaussian 2k and 2k+1 are the duplicate pair (plus a few far-apart copies)
+    perm = rng.permutation(N)
+    mean = np.concatenate([mean, mean[perm]])
+    chol = np.concatenate([chol, chol[perm]])
+    o = np.concatenate([o, o2])
+    c = np.concatenate([c, c2])
+    f = float(res)
+    cam = dict(fx=f, fy=f, cx=res / 2.0, cy=res / 2.0, W=res, H=res, euler=[0.0, 0.0, 0.0],
+               t=[0.0, 0.0, 0.0])
+    box = _pose_box(eps_t=(eps_t, 0, 0), eps_R=(0, 0, math.radians(rot_deg)))
+    return _pack("ties", mean, chol, o, c, cam, box, tile=16, batch=16,
+                 description=f"{N} duplicated Gaussian pairs (exact depth ties), tx +-{eps_t}"
+                             + (f", yaw +-{rot_deg} deg" if rot_deg else ""))
+
+
+def stacked_config(N: int = 200, res: int = 32, seed: int = 13, rot_deg: float = 0.5,
+                   depth_spread: float = 0.005, opacity=(0.9, 0.99),
+                   axis_frac: float = 0.0) -> Workload:
+    """Exception-machinery stress case: N nearly opaque Gaussians stacked in a thin slab
+    (depth 5 +- depth_spread m) in front of an identity camera, under a rotation box.  Almost every
+    pair in a tile is uncertain (Table 2 Ind '?'), so exception windows span most of the list
+    (long E_F / E_G lists, window lengths past the 128-position masks), and the transmittance
+    deep in the stack underflows far below 1e-25 (the guarded-division paths).  Nothing here
+    evaluates the method."""
+    rng = np.random.default_rng(seed)
+    mean = np.stack([rng.uniform(-0.15, 0.15, N), rng.uniform(-0.15, 0.15, N),
+                     5.0 + rng.uniform(-depth_spread, depth_spread, N)], axis=1)
+    # axis_frac of them on the optical axis column (|x| < 2 mm): their depth barely moves under
+    # yaw, so pairs among them stay certain while pairs with off-axis ones are uncertain
+    # (windows mixing kept and excepted positions)
+    on = rng.uniform(size=N) < axis_frac
+    mean[on, 0] = rng.uniform(-0.002, 0.002, int(on.sum()))
+    s = _loguniform(rng, 0.05, 0.2, (N, 3))
+    s[:, 2] *= 0.1
+    chol = _chol_from(_frame_with_normal(rng, np.tile([[0.0, 0.0, 1.0]], (N, 1))), s)
+    o = rng.uniform(opacity[0], opacity[1], N)
+    c = rng.uniform(0, 1, (N, 3))
+    f = 2.0 * res
+    cam = dict(fx=f, fy=f, cx=res / 2.0, cy=res / 2.0, W=res, H=res, euler=[0.0, 0.0, 0.0],
+               t=[0.0, 0.0, 0.0])
+    # rotation about the camera's vertical axis (Euler e1): depth changes by about x * angle,
+    # so the on-axis column's depths stay nearly fixed
+    box = _pose_box(eps_t=(0.005, 0, 0), eps_R=(0, math.radians(rot_deg), 0))
+    return _pack("stacked", mean, chol, o, c, cam, box, tile=16, batch=24,
+                 description=f"{N} near-opaque Gaussians in a {2 * depth_spread} m slab, "
+                             f"e1 +-{rot_deg} deg, on-axis fraction {axis_frac}")
