@@ -590,7 +590,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   }
   const size_t npix = (size_t)G.ts * G.ts;
   if (has_exc) {  // ring memory: grid x R x threads float4 (cap the total at ~8 GB)
-    const size_t per = (size_t)R * tile_threads(G.ts) * sizeof(float4);
+    const size_t per = (size_t)R * tile_ring_slot_bytes(G.ts);
     const size_t budget = (size_t)8 << 30;
     if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
     ensure(ctx, ctx->scratch, (size_t)grid * per);

@@ -362,6 +362,7 @@ void launch_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* u
 void launch_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n, bool first,
                   cudaStream_t st);
 int tile_threads(int ts);
+size_t tile_ring_slot_bytes(int ts);
 int tile_subblocks(int ts);
 int tile_grid(int nv, int ts, int bs);
 size_t tile_smem_bytes(int nv, int ts, int bs);

@@ -786,6 +786,643 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
 }
 
+// ======================================================================== v2 tile kernel
+// Work item = one 16x16 pixel block of a tile (TS >= 16) over one chunk of its list, 128
+// threads, TWO pixels per thread: lane (x, y) of warp quadrant (qx, qy) owns the pixels
+// (8 qx + x, 8 qy + y) and (8 qx + x, 8 qy + y + 4) -- same column, so the x_0 form and the
+// du_0 / x_0 part of every q coefficient are shared, and the per-Gaussian coefficients loaded
+// from shared memory serve both pixels.  The per-pixel arithmetic runs pixel-packed: every
+// FFMA2 / FADD2 lane is one of the two pixels (the coefficient is the broadcast operand), the
+// blend state and the exception ring hold float2 pairs.  Same steps and same per-pixel
+// operations as k_tile (which keeps TS = 8).
+constexpr int B2 = 16;   // block edge (pixels)
+constexpr int T2 = 128;  // threads per block
+constexpr int P2 = 256;  // pixels per block
+__host__ __device__ __forceinline__ int v2_x(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
+__host__ __device__ __forceinline__ int v2_y(int t) { return (t >> 6) * 8 + ((t >> 3) & 3); }
+
+template <int NV>
+struct alignas(16) SRec2 {
+  static constexpr int C = NV + 1;
+  static constexpr int CP = (C + 3) & ~3;
+  // lower x forms at the block centre: x_lo,a,k(u) = xb_a[k] + du_a d2[k]
+  float xb0[CP], xb1[CP], d2[CP];
+  // q_c's (mid, radius) coefficients as affine functions of (du0, du1, x0, |x0|, x1, |x1|):
+  //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
+  float4 A[3][C];    // (pm, pr, q0m, q0r)
+  float4 B[3][C];    // (wm0, wr0, q1m, q1r)
+  float2 W1[3][CP];  // (wm1, wr1)
+  float4 WC[3];      // concretised W_0c, W_1c as (mid0, half0, mid1, half1)
+  float o[2];
+  float clo[3], chi[3];
+  int flags;
+  int pmf, ph, pg, pnF, pnG;
+  int pfb, pfe;
+  long long peoff;
+  unsigned long long mf0, mf1;
+  int tmode;
+  int nT;
+  unsigned char tlo[TL8];
+  double r2;
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+template <int NV>
+__device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, double ucx,
+                                             double ucy, int part) {
+  constexpr int C = NV + 1;
+  constexpr int KP = (C + NPART - 1) / NPART;
+  const double uc[2] = {ucx, ucy};
+  double wl[6], wh[6];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    wl[e] = H->wc[e][0];
+    wh[e] = H->wc[e][1];
+  }
+  if (part == NPART - 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      S.WC[c] = make_float4((float)(0.5 * (wl[c] + wh[c])), (float)(0.5 * (wh[c] - wl[c])),
+                            (float)(0.5 * (wl[3 + c] + wh[3 + c])),
+                            (float)(0.5 * (wh[3 + c] - wl[3 + c])));
+  }
+#pragma unroll 1
+  for (int i = 0; i < KP; ++i) {
+    const int k = part + NPART * i;
+    if (k >= C) break;
+    const double d2l = H->d2[0][k], d2h = H->d2[1][k];
+    double blo[2], bhi[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      blo[a] = uc[a] * d2l - H->du[a][1][k];
+      bhi[a] = uc[a] * d2h - H->du[a][0][k];
+    }
+    float wa[6], wb[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      wa[e] = H->w[e][0][k];
+      wb[e] = H->w[e][1][k];
+    }
+    S.xb0[k] = (float)blo[0];
+    S.xb1[k] = (float)blo[1];
+    S.d2[k] = (float)d2l;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+      const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
+      const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
+      const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q1lo = w1l * (w1l >= 0 ? d2l : d2h);
+      const double q0hi = w0h * (w0h >= 0 ? d2h : d2l), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
+      const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
+      S.A[c][k] = make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
+                              (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+      S.B[c][k] = make_float4((float)(0.5 * (a0 + b0)), (float)(0.5 * (b0 - a0)),
+                              (float)(0.5 * (q1lo + q1hi)), (float)(0.5 * (q1hi - q1lo)));
+      S.W1[c][k] = make_float2((float)(0.5 * (a1 + b1)), (float)(0.5 * (b1 - a1)));
+    }
+  }
+}
+
+// steps 14-17 for the thread's two pixels (du0 shared; DU1 = (du1 of pixel 0, of pixel 1)):
+// returns (a_lo, a_hi) pairs.  Same per-pixel operations as s_forms / opacity.
+template <int NV>
+__device__ __forceinline__ void opacity2(const SRec2<NV>& R, float du0, float2 DU1, float2& alo,
+                                         float2& ahi) {
+  constexpr int C = NV + 1;
+  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel)
+  float x0 = fmaf(du0, R.d2[NV], R.xb0[NV]);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(du0, R.d2[k], R.xb0[k]));
+  float2 X1 = __ffma2_rn(DU1, bc(R.d2[NV]), bc(R.xb1[NV]));
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const float2 v = __ffma2_rn(DU1, bc(R.d2[k]), bc(R.xb1[k]));
+    X1 = __fadd2_rn(X1, f2(-fabsf(v.x), -fabsf(v.y)));
+  }
+  const float2 AX1 = f2(fabsf(X1.x), fabsf(X1.y));
+  const float2 D0 = bc(du0), X0 = f2(x0, fabsf(x0));
+  float2 SL[C], SH[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) SL[k] = SH[k] = f2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    // 15: q_c = mul(x0, W_0c) + mul(x1, W_1c) as (mid, radius) forms, per pixel
+    float2 M[C], RR[C];
+    const float4 wc = R.WC[c];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float4 a = R.A[c][k], b = R.B[c][k];
+      const float2 w1 = R.W1[c][k];
+      float2 mr = __ffma2_rn(D0, f2(a.z, a.w), f2(a.x, a.y));
+      mr = __ffma2_rn(X0, f2(b.x, b.y), mr);
+      if (k == NV) mr = __ffma2_rn(bc(-x0), f2(wc.x, wc.y), mr);  // - x0 conc W_0c
+      float2 m = __ffma2_rn(DU1, bc(b.z), bc(mr.x));
+      m = __ffma2_rn(X1, bc(w1.x), m);
+      float2 r = __ffma2_rn(DU1, bc(b.w), bc(mr.y));
+      r = __ffma2_rn(AX1, bc(w1.y), r);
+      if (k == NV) {  // - x1 conc W_1c
+        m = __ffma2_rn(X1, bc(-wc.z), m);
+        r = __ffma2_rn(X1, bc(-wc.w), r);
+      }
+      M[k] = m;
+      RR[k] = r;
+    }
+    // concretised q: q_lo = m - r, q_hi = m + r
+    float2 qmin = __fadd2_rn(M[NV], f2(-RR[NV].x, -RR[NV].y));
+    float2 qmax = __fadd2_rn(M[NV], RR[NV]);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const float2 ql = __fadd2_rn(M[k], f2(-RR[k].x, -RR[k].y));
+      const float2 qh = __fadd2_rn(M[k], RR[k]);
+      qmin = __fadd2_rn(qmin, f2(-fabsf(ql.x), -fabsf(ql.y)));
+      qmax = __fadd2_rn(qmax, f2(fabsf(qh.x), fabsf(qh.y)));
+    }
+    // 16: s += sq(q_c): lower tangent at p = clamp(0, qmin, qmax), upper chord (R2), with the
+    // side selection written as tp m - |tp| r and sm m + |sm| r
+    const float2 P = f2(fminf(fmaxf(0.f, qmin.x), qmax.x), fminf(fmaxf(0.f, qmin.y), qmax.y));
+    const float2 TP = __fadd2_rn(P, P), SM = __fadd2_rn(qmin, qmax);
+    const float2 NTP = f2(-fabsf(TP.x), -fabsf(TP.y)), ASM = f2(fabsf(SM.x), fabsf(SM.y));
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      SL[k] = __ffma2_rn(TP, M[k], SL[k]);
+      SL[k] = __ffma2_rn(NTP, RR[k], SL[k]);
+      SH[k] = __ffma2_rn(SM, M[k], SH[k]);
+      SH[k] = __ffma2_rn(ASM, RR[k], SH[k]);
+    }
+    SL[NV] = __ffma2_rn(f2(-P.x, -P.y), P, SL[NV]);
+    SH[NV] = __ffma2_rn(f2(-qmin.x, -qmin.y), qmax, SH[NV]);
+  }
+  float2 smin = SL[NV], smax = SH[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    smin = __fadd2_rn(smin, f2(-fabsf(SL[k].x), -fabsf(SL[k].y)));
+    smax = __fadd2_rn(smax, f2(fabsf(SH[k].x), fabsf(SH[k].y)));
+  }
+  // 17: a = o Exp(-s/2) concretised (O11)
+  alo = f2(R.o[0] * exp2f(-LOG2E_HALF * smax.x), R.o[0] * exp2f(-LOG2E_HALF * smax.y));
+  ahi = f2(R.o[1] * exp2f(-LOG2E_HALF * fmaxf(smin.x, 0.f)),
+           R.o[1] * exp2f(-LOG2E_HALF * fmaxf(smin.y, 0.f)));
+}
+
+// ring of the v2 kernel: [slot][component][thread] float2 (the thread's two pixels)
+__device__ __forceinline__ int RS2(int pos, int comp, int rmask) {
+  return ((pos & rmask) * 4 + comp) * T2;
+}
+__device__ __noinline__ float2 exc_prod2(const float2* rf, const int32_t* list, int n, int comp,
+                                         int rmask) {
+  float2 prod = f2(1.f, 1.f);
+  for (int e0 = 0; e0 < n; e0 += 8) {
+    int idx[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) idx[u] = e0 + u < n ? list[e0 + u] : -1;
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = idx[u] >= 0 ? rf[RS2(idx[u], comp, rmask)] : f2(1.f, 1.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) prod = mul2(prod, v[u]);
+  }
+  return prod;
+}
+__device__ __noinline__ float2 window_prod2(const float2* rf, int h, int q, const int32_t* ef,
+                                            int nf, int rmask) {
+  float2 prod = f2(1.f, 1.f);
+  int e = 0;
+  int nextF = nf > 0 ? ef[0] : 0x7fffffff;
+  for (int r0 = h; r0 < q; r0 += 8) {
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = r0 + u < q ? rf[RS2(r0 + u, 1, rmask)] : f2(1.f, 1.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u;
+      if (r >= q) break;
+      if (r == nextF) {
+        ++e;
+        nextF = e < nf ? ef[e] : 0x7fffffff;
+      } else {
+        prod = mul2(prod, v[u]);
+      }
+    }
+  }
+  return prod;
+}
+__device__ __forceinline__ float2 ring_prod2(const float2* rf, unsigned long long m0,
+                                             unsigned long long m1, int base, int comp,
+                                             int rmask) {
+  float2 prod = f2(1.f, 1.f);
+  while (m0 | m1) {
+    float2 v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int idx = -1;
+      if (m0) {
+        idx = base + __ffsll((long long)m0) - 1;
+        m0 &= m0 - 1;
+      } else if (m1) {
+        idx = base + 64 + __ffsll((long long)m1) - 1;
+        m1 &= m1 - 1;
+      }
+      v[t] = idx >= 0 ? rf[RS2(idx, comp, rmask)] : f2(1.f, 1.f);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) prod = mul2(prod, v[t]);
+  }
+  return prod;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_work;
+  __shared__ unsigned s_skip[8];
+  __shared__ int s_F[2];
+  const int ts = A.ts;
+  const int nsbx = ts / B2;
+  const int nsub = nsbx * nsbx;
+  const int BS = A.bs;
+  SRec2<NV>* srec = reinterpret_cast<SRec2<NV>*>(smem_raw);
+  double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][16] per column
+  double* cy2 = cx2 + (size_t)BS * B2;                 // [BS][16] per row
+  FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * B2);  // [FB]
+  const bool has_exc = A.pm != nullptr;
+  const int tid = threadIdx.x;
+  float2* rf = has_exc ? reinterpret_cast<float2*>(A.ring) + (size_t)blockIdx.x * A.R * 4 * T2 + tid
+                       : nullptr;
+  const int lx = v2_x(tid), ly = v2_y(tid);
+  const float du0 = (float)lx + 0.5f - 0.5f * B2;
+  const float2 DU1 = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
+  unsigned active = 0;
+  const int nwork = A.n_items * nsub;
+
+  for (;;) {
+    if (tid == 0) s_work = atomicAdd(A.counter, 1);
+    __syncthreads();
+    const int w = s_work;
+    __syncthreads();
+    if (w >= nwork) break;
+    const int islot = A.order[w / nsub];
+    const int sub = w % nsub;
+    const int4 it = A.items[islot];
+    if (it.x < 0) continue;
+    const int tile = it.x, pbeg = it.y, pend = it.z, iflags = it.w;
+    const int4 it2 = A.items2[islot];
+    const int scan0 = it2.x, scan1 = it2.y, anext = it2.z;
+    const int rmask = (1 << ((iflags >> 8) & 0xff)) - 1;
+    const int tx = tile % A.ntx, ty = tile / A.ntx;
+    const int ox = tx * ts + (sub % nsbx) * B2, oy = ty * ts + (sub / nsbx) * B2;
+    const int64_t tb = A.tbegin[tile];
+    const double ucx = ox + 0.5 * B2, ucy = oy + 0.5 * B2;
+    const bool iexc = has_exc && (iflags & IT_EXC);
+    const bool inA = (ox + lx < A.W) && (oy + ly < A.H);
+    const bool inB = (ox + lx < A.W) && (oy + ly + 4 < A.H);
+    const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + B2), (double)A.W) - 0.5;
+    const double by0 = oy + 0.5, by1 = fmin((double)(oy + B2), (double)A.H) - 0.5;
+    const bool block_live = ox < A.W && oy < A.H;
+    float2 Tb = f2(1.f, 1.f), Tl = f2(1.f, 1.f);
+    float2 ahc[3] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+    float2 alc[3] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+    float2 recb = f2(1.f, 1.f), recl = f2(1.f, 1.f);
+    bool rec = false;
+
+    for (int b0 = scan0; b0 < scan1; b0 += BS) {
+      const int nb = min(BS, scan1 - b0);
+      int f0l = 0, f1l = 0;
+      if (tid == 0 && iexc) {
+        f0l = A.finstart[tb + b0];
+        f1l = A.finstart[tb + b0 + nb];
+      }
+      __syncthreads();
+      // ---- phase A: metadata + cull tables (one thread per Gaussian, highest ids) and
+      //      staging (NPART threads per Gaussian), as in k_tile
+      for (int j = T2 - 1 - tid; j < nb; j += T2) {
+        const int64_t gp = tb + b0 + j;
+        const int32_t g = A.vals[gp];
+        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
+        SRec2<NV>& S = srec[j];
+        const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
+        const double r2 = H->r2;
+        bool skip;
+        {
+          const double dx = fmax(0.0, fmax(__dsub_rn(mxl, bx1), __dsub_rn(bx0, mxh)));
+          const double dy = fmax(0.0, fmax(__dsub_rn(myl, by1), __dsub_rn(by0, myh)));
+          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2;
+        }
+        const int bit = (b0 + j) & 255;
+        if (skip)
+          atomicOr(&s_skip[bit >> 5], 1u << (bit & 31));
+        else
+          atomicAnd(&s_skip[bit >> 5], ~(1u << (bit & 31)));
+        int pmf = 0;
+        if (iexc) {
+          const int4 m = A.pm[gp];
+          pmf = m.x;
+          S.ph = m.y;
+          S.pg = m.z;
+          S.pnF = m.w;
+          S.pnG = A.nG[gp];
+          S.peoff = A.eoff[gp];
+          S.pfb = A.finstart[gp];
+          S.pfe = A.finstart[gp + 1];
+          const ulonglong2 mf = A.mF[gp];
+          S.mf0 = mf.x;
+          S.mf1 = mf.y;
+        } else {
+          S.pfb = S.pfe = 0;
+        }
+        S.tmode = 0;
+        S.nT = 0;
+        S.pmf = pmf;
+        S.flags = H->flags | (skip ? F_SKIP : 0);
+        S.r2 = r2;
+        S.o[0] = H->o[0];
+        S.o[1] = H->o[1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          S.clo[c] = H->clo[c];
+          S.chi[c] = H->chi[c];
+        }
+        if (!skip) {
+#pragma unroll
+          for (int l = 0; l < B2; ++l) {
+            const double x = ox + l + 0.5;
+            const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
+            cx2[j * B2 + l] = __dmul_rn(dx, dx);
+            const double y = oy + l + 0.5;
+            const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
+            cy2[j * B2 + l] = __dmul_rn(dy, dy);
+          }
+        }
+      }
+      for (int jj = tid; jj < NPART * nb; jj += T2) {
+        const int j = jj / NPART, part = jj % NPART;
+        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
+        bool skip;
+        {
+          const double dx = fmax(0.0, fmax(__dsub_rn(H->mu[0], bx1), __dsub_rn(bx0, H->mu[2])));
+          const double dy = fmax(0.0, fmax(__dsub_rn(H->mu[1], by1), __dsub_rn(by0, H->mu[3])));
+          skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
+        }
+        if (!skip) stage_forms2<NV>(srec[j], H, ucx, ucy, part);
+      }
+      if (tid == 0) {
+        s_F[0] = f0l;
+        s_F[1] = f1l;
+      }
+      __syncthreads();
+      // ---- phase B: T_hi window operand lists (warp 0) and staged finalisation records
+      if (iexc) {
+        for (int j = tid < 32 ? tid : nb; j < nb; j += 32) {
+          SRec2<NV>& S = srec[j];
+          const int pmf = S.pmf, qpos = b0 + j;
+          if (!(pmf & PM_EF) || (S.flags & F_SKIP) || qpos < pbeg || qpos >= pend || (pmf & PM_OVF))
+            continue;
+          const int h = S.ph, wlen = qpos - h;
+          const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+          const unsigned long long v1 =
+              wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+          unsigned long long k0, k1;
+          skip_win(s_skip, h, k0, k1);
+          const unsigned long long e0 = S.mf0 & ~k0, e1 = S.mf1 & ~k1;
+          const unsigned long long g0 = ~S.mf0 & ~k0 & v0, g1 = ~S.mf1 & ~k1 & v1;
+          const int nef = __popcll(e0) + __popcll(e1), nkept = __popcll(g0) + __popcll(g1);
+          const bool dense = !(nkept > nef + 2);
+          unsigned long long m0 = dense ? g0 : e0;
+          unsigned long long m1 = dense ? g1 : e1;
+          const int cnt = dense ? nkept : nef;
+          int nT = 0;
+          if (cnt <= TL8) {
+            S.tmode = dense ? 1 : 2;
+            for (; m0; m0 &= m0 - 1) S.tlo[nT++] = (unsigned char)(__ffsll((long long)m0) - 1);
+            for (; m1; m1 &= m1 - 1) S.tlo[nT++] = (unsigned char)(64 + __ffsll((long long)m1) - 1);
+          } else {
+            S.tmode = 3;
+            if (A.dbg) atomicAdd(A.dbg + DBG_TMODE3, 1ull);
+          }
+          S.nT = nT;
+        }
+      }
+      const int F0 = s_F[0];
+      for (int t = tid - 32; t < min(s_F[1] - F0, FB); t += T2 - 32) {
+        if (t < 0) break;
+        const FinRec fr = A.fin_rec[F0 + t];
+        FinS& F = fins[t];
+        const int qq = fr.qq;
+        F.clo[0] = fr.clo[0];
+        F.clo[1] = fr.clo[1];
+        F.clo[2] = fr.clo[2];
+        F.qq = -1;
+        F.n = 0;
+        if (qq < pbeg || qq >= pend) continue;
+        if (fr.flags & PM_OVF) {
+          F.qq = qq;
+          F.n = -1;
+          continue;
+        }
+        const int qb = qq & 255;
+        if ((s_skip[qb >> 5] >> (qb & 31)) & 1u) continue;
+        F.qq = qq;
+        unsigned long long k0, k1;
+        skip_win(s_skip, qq + 1, k0, k1);
+        unsigned long long g0 = fr.mg.x & ~k0, g1 = fr.mg.y;
+        if (g1) {
+          g1 &= ~(1ull << (63 - __clzll((long long)g1)));
+          g1 &= ~k1;
+        } else {
+          g0 &= ~(1ull << (63 - __clzll((long long)fr.mg.x)));
+        }
+        if (__popcll(g0) + __popcll(g1) > EG8) {
+          F.n = -1;
+          continue;
+        }
+        int n = 0;
+        for (; g0; g0 &= g0 - 1) F.off[n++] = (unsigned char)__ffsll((long long)g0);
+        for (; g1; g1 &= g1 - 1) F.off[n++] = (unsigned char)(64 + __ffsll((long long)g1));
+        F.n = (short)n;
+      }
+      __syncthreads();
+      // ---- walk the batch in (kappa, index) order, two pixels per thread
+      for (int j = 0; j < nb; ++j) {
+        const SRec2<NV>& R = srec[j];
+        const int flags = R.flags, pmf = R.pmf;
+        const int qpos = b0 + j;
+        if (qpos == anext) {
+          recb = Tb;
+          recl = Tl;
+          rec = true;
+        }
+        if ((flags & F_SKIP) && pmf == 0) continue;
+        const bool main = qpos >= pbeg && qpos < pend;
+        float2 alo = f2(0.f, 0.f), ahi = f2(0.f, 0.f);
+        bool kA = false, kB = false;
+        if (!(flags & F_SKIP)) {
+          const double cx = cx2[j * B2 + lx];
+          kA = inA && !(__dadd_rn(cx, cy2[j * B2 + ly]) > R.r2);
+          kB = inB && !(__dadd_rn(cx, cy2[j * B2 + ly + 4]) > R.r2);
+          if (__any_sync(FULLM, kA || kB)) {
+            if (flags & F_FAIL) {
+              ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
+            } else {
+              float2 l, h;
+              opacity2<NV>(R, du0, DU1, l, h);
+              const bool st = flags & F_STRADDLE;
+              alo = f2(kA && !st ? l.x : 0.f, kB && !st ? l.y : 0.f);
+              ahi = f2(kA ? h.x : 0.f, kB ? h.y : 0.f);
+            }
+          }
+        }
+        active += main ? (unsigned)kA + (unsigned)kB : 0u;
+        if (pmf & PM_STORE) {
+          const int rs = RS2(qpos, 0, rmask);
+          if (pmf & PM_HSTART) rf[rs] = Tb;
+          rf[rs + T2] = f2(1.f - alo.x, 1.f - alo.y);
+          if (pmf & PM_EF) rf[rs + 2 * T2] = f2(1.f - ahi.x, 1.f - ahi.y);
+          if (pmf & PM_EG) rf[rs + 3 * T2] = mul2(Tl, alo);
+        }
+        float2 tbv = Tb;
+        if (main && (pmf & PM_EF) && !(flags & F_SKIP) && (ahi.x > 0.f || ahi.y > 0.f)) {
+          const int wlen = qpos - R.ph;
+          if (!(pmf & PM_OVF)) {
+            bool done = false;
+            if (R.tmode == 1) {
+              float2 pr = rf[RS2(R.ph, 0, rmask)];
+#pragma unroll 4
+              for (int t = 0; t < R.nT; ++t) pr = mul2(pr, rf[RS2(R.ph + R.tlo[t], 1, rmask)]);
+              tbv = pr;
+              done = true;
+            } else if (R.tmode == 2) {
+              float2 dfac = f2(1.f, 1.f);
+#pragma unroll 4
+              for (int t = 0; t < R.nT; ++t) dfac = mul2(dfac, rf[RS2(R.ph + R.tlo[t], 1, rmask)]);
+              if (dfac.x >= 1e-20f && dfac.y >= 1e-20f && Tb.x >= 1e-25f && Tb.y >= 1e-25f) {
+                tbv = f2(Tb.x / dfac.x, Tb.y / dfac.y);
+                done = true;
+              } else if (A.dbg) {
+                atomicAdd(A.dbg + DBG_THI_DIV_UNSAFE, 1ull);
+              }
+            }
+            if (!done) {
+              if (A.dbg) atomicAdd(A.dbg + DBG_THI_BITS, 1ull);
+              const unsigned long long v0 = wlen >= 64 ? ~0ull : ((1ull << wlen) - 1ull);
+              const unsigned long long v1 =
+                  wlen <= 64 ? 0ull : (wlen >= 128 ? ~0ull : ((1ull << (wlen - 64)) - 1ull));
+              tbv = mul2(rf[RS2(R.ph, 0, rmask)],
+                         ring_prod2(rf, ~R.mf0 & v0, ~R.mf1 & v1, R.ph, 1, rmask));
+            }
+          } else {
+            if (A.dbg) atomicAdd(A.dbg + DBG_THI_OVF, 1ull);
+            bool done = false;
+            if (wlen > 2 * R.pnF + 8) {
+              const float2 dfac = exc_prod2(rf, A.exc + R.peoff, R.pnF, 1, rmask);
+              if (dfac.x >= 1e-20f && dfac.y >= 1e-20f && Tb.x >= 1e-25f && Tb.y >= 1e-25f) {
+                tbv = f2(Tb.x / dfac.x, Tb.y / dfac.y);
+                done = true;
+              }
+            }
+            if (!done && A.dbg) atomicAdd(A.dbg + DBG_THI_OVF_WINDOW, 1ull);
+            if (!done)
+              tbv = mul2(rf[RS2(R.ph, 0, rmask)],
+                         window_prod2(rf, R.ph, qpos, A.exc + R.peoff, R.pnF, rmask));
+          }
+        }
+        const float2 wb = main ? mul2(tbv, ahi) : f2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ahc[c] = __ffma2_rn(wb, bc(R.chi[c]), ahc[c]);
+        if (main && !(pmf & PM_EG)) {
+          const float2 wl = mul2(Tl, alo);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) alc[c] = __ffma2_rn(wl, bc(R.clo[c]), alc[c]);
+        }
+        Tb = __ffma2_rn(f2(-Tb.x, -Tb.y), alo, Tb);
+        Tl = __ffma2_rn(f2(-Tl.x, -Tl.y), ahi, Tl);
+        for (int f = R.pfb - F0; f < R.pfe - F0; ++f) {
+          float2 tl;
+          const float* clo;
+          if (f < FB) {
+            const FinS& F = fins[f];
+            if (F.qq < 0) continue;
+            clo = F.clo;
+            tl = rf[RS2(F.qq, 3, rmask)];
+            if (tl.x == 0.f && tl.y == 0.f) continue;
+            if (F.n >= 0) {
+              tl = mul2(tl, f2(1.f - ahi.x, 1.f - ahi.y));
+#pragma unroll 4
+              for (int e = 0; e < F.n; ++e) tl = mul2(tl, rf[RS2(F.qq + F.off[e], 2, rmask)]);
+            } else {
+              if (A.dbg) atomicAdd(A.dbg + DBG_FIN_SLOW, 1ull);
+              const FinRec& fr = A.fin_rec[F0 + f];
+              if (!(fr.flags & PM_OVF)) {
+                tl = mul2(tl, ring_prod2(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask));
+              } else {
+                if (A.dbg) atomicAdd(A.dbg + DBG_FIN_OVF, 1ull);
+                tl = mul2(tl, exc_prod2(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask));
+              }
+            }
+          } else {
+            const FinRec& fr = A.fin_rec[F0 + f];
+            if (fr.qq < pbeg || fr.qq >= pend) continue;
+            if (A.dbg) atomicAdd(A.dbg + DBG_FIN_UNSTAGED, 1ull);
+            clo = fr.clo;
+            tl = rf[RS2(fr.qq, 3, rmask)];
+            if (tl.x == 0.f && tl.y == 0.f) continue;
+            if (!(fr.flags & PM_OVF)) {
+              tl = mul2(tl, ring_prod2(rf, fr.mg.x, fr.mg.y, fr.qq + 1, 2, rmask));
+            } else {
+              if (A.dbg) atomicAdd(A.dbg + DBG_FIN_OVF, 1ull);
+              tl = mul2(tl, exc_prod2(rf, A.exc + fr.eoff + fr.nF, fr.nG, 2, rmask));
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) alc[c] = __ffma2_rn(tl, bc(clo[c]), alc[c]);
+        }
+      }
+    }
+    // ---- epilogue (both pixels)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int py = oy + ly + 4 * e, px = ox + lx;
+      const bool in = e ? inB : inA;
+      const float hc[3] = {e ? ahc[0].y : ahc[0].x, e ? ahc[1].y : ahc[1].x, e ? ahc[2].y : ahc[2].x};
+      const float lc[3] = {e ? alc[0].y : alc[0].x, e ? alc[1].y : alc[1].x, e ? alc[2].y : alc[2].x};
+      if (iflags & IT_SINGLE) {
+        int64_t o = -1;
+        if (A.tile_slot) {
+          o = ((int64_t)A.tile_slot[tile] * ts * ts + (int64_t)(py - ty * ts) * ts + (px - tx * ts)) * 3;
+        } else if (in) {
+          o = ((int64_t)py * A.W + px) * 3;
+        }
+        if (o >= 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float l = fminf(fmaxf(lc[c] - A.ntau, 0.f), 1.f);
+            float h = fminf(fmaxf(hc[c] + A.ntau, 0.f), 1.f);
+            if (!in) l = h = 0.f;
+            if (A.first) {
+              A.lo[o + c] = l;
+              A.hi[o + c] = h;
+            } else {
+              A.lo[o + c] = fminf(A.lo[o + c], l);
+              A.hi[o + c] = fmaxf(A.hi[o + c], h);
+            }
+          }
+        }
+      } else {
+        const float2 rb = rec ? recb : Tb, rl = rec ? recl : Tl;
+        const int pix = (ly + 4 * e) * B2 + lx;
+        float4* dst = reinterpret_cast<float4*>(A.partial + (((size_t)islot * nsub + sub) * P2 + pix) * 8);
+        dst[0] = make_float4(hc[0], hc[1], hc[2], e ? rb.y : rb.x);
+        dst[1] = make_float4(lc[0], lc[1], lc[2], e ? rl.y : rl.x);
+      }
+    }
+  }
+  unsigned v = active;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULLM, v, s);
+  if ((tid & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
+}
+
 // ---------------------------------------------------------------- NEXT-1 linear blend
 // One CTA per (exception-free tile, 8x8 block), one thread per pixel: BlendInd with linear
 // relations along the sorted fold (Alg. 3; oracle blend_linear):
@@ -958,12 +1595,15 @@ __global__ void k_merge(TileArgs A) {
   const int tile = blockIdx.x;
   const int n = A.item_cnt[tile];
   if (n <= 1) return;
-  const int ts = A.ts, npix = ts * ts, SBX = block_w(ts), SBP = SBX * SBY;
-  const int nsbx = ts / SBX, nsub = nsbx * (ts / SBY);
+  const int ts = A.ts, npix = ts * ts;
+  const bool v2 = ts >= B2;  // k_tile2 layout: 16x16 blocks, row-major pixels
+  const int SBX = v2 ? B2 : block_w(ts), SBH = v2 ? B2 : SBY, SBP = SBX * SBH;
+  const int nsbx = ts / SBX, nsub = nsbx * (ts / SBH);
   const int tx = tile % A.ntx, ty = tile / A.ntx;
   for (int tp = threadIdx.x; tp < npix; tp += blockDim.x) {
     const int lx = tp % ts, ly = tp / ts;
-    const int sub = (ly / SBY) * nsbx + lx / SBX, pix = pix_of(lx % SBX, ly % SBY, SBX);
+    const int sub = (ly / SBH) * nsbx + lx / SBX;
+    const int pix = v2 ? (ly % SBH) * SBX + lx % SBX : pix_of(lx % SBX, ly % SBY, SBX);
     float Pb = 1.f, Pl = 1.f, h[3] = {0.f, 0.f, 0.f}, l[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < n; ++k) {
       const int64_t it = A.item_off[tile] + k;
@@ -1003,11 +1643,17 @@ __global__ void k_merge(TileArgs A) {
   }
 }
 
-int tile_threads(int ts) { return block_w(ts) * SBY; }
-int tile_subblocks(int ts) { return (ts / block_w(ts)) * (ts / SBY); }
+// TS >= 16: k_tile2 (16x16 blocks, two pixels per thread); TS = 8: k_tile (8x8 blocks)
+int tile_threads(int ts) { return ts >= B2 ? T2 : block_w(ts) * SBY; }
+int tile_subblocks(int ts) { return ts >= B2 ? (ts / B2) * (ts / B2) : (ts / block_w(ts)) * (ts / SBY); }
+size_t tile_ring_slot_bytes(int ts) {  // exception ring bytes per slot per CTA
+  return ts >= B2 ? (size_t)4 * T2 * sizeof(float2) : (size_t)tile_threads(ts) * sizeof(float4);
+}
 
 template <int NV>
 static size_t smem_for(int ts, int bs) {
+  if (ts >= B2)
+    return (size_t)bs * (sizeof(SRec2<NV>) + 2 * B2 * sizeof(double)) + FB * sizeof(FinS);
   return (size_t)bs * (sizeof(SRec<NV>) + (block_w(ts) + SBY) * sizeof(double)) +
          FB * sizeof(FinS);
 }
@@ -1039,7 +1685,19 @@ static int grid_bx(int ts, int bs) {
   return std::max(1, per_sm) * nsm;
 }
 template <int NV>
+static int grid_v2(int ts, int bs) {
+  if (cudaFuncSetAttribute(k_tile2<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024) != cudaSuccess)
+    return 0;
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile2<NV>, T2, smem_for<NV>(ts, bs));
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(1, per_sm) * nsm;
+}
+template <int NV>
 static int grid_one(int ts, int bs) {
+  if (ts >= B2) return grid_v2<NV>(ts, bs);
   return block_w(ts) == 16 ? grid_bx<NV, 16>(ts, bs) : grid_bx<NV, 8>(ts, bs);
 }
 
@@ -1057,7 +1715,9 @@ int tile_grid(int nv, int ts, int bs) {
 
 template <int NV>
 static void launch_one(const TileArgs& a, int grid, cudaStream_t st) {
-  if (block_w(a.ts) == 16)
+  if (a.ts >= B2)
+    k_tile2<NV><<<grid, T2, smem_for<NV>(a.ts, a.bs), st>>>(a);
+  else if (block_w(a.ts) == 16)
     k_tile<NV, 16><<<grid, 16 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);
   else
     k_tile<NV, 8><<<grid, 8 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);
