@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #ifdef _OPENMP
@@ -543,23 +544,14 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
           const double lm = lam[i * 4 + 2 * c + d];
           if (lm == 0.0) continue;
           for (int l = 0; l < 2; ++l) {
-            const double xl = Bl[(i - 1) * 4 + 2 * c + l], xh = Bh[(i - 1) * 4 + 2 * c + l];
+            const double xl = Bl[(i - 1) * 4 + 2 * c + l];
             const double yl = El[2 * l + d], yh = Eh[2 * l + d];
-            if (i == 2 && c == l && l == d) {  // E_cc * E_cc: R2 (tangent / chord)
-              if (lm >= 0) {
-                const double p = std::min(std::max(0.0, xl), xh);
-                mu[2 * c + c] += lm * 2.0 * p;
-                cst -= lm * p * p;
-              } else {
-                mu[2 * c + c] += lm * (xl + xh);
-                cst -= lm * xl * xh;
-              }
-            } else {  // R1: lower plane yl f + xl g - xl yl, upper plane yh f + xl g - xl yh
-              const double yy = lm >= 0 ? yl : yh;
-              lam[(i - 1) * 4 + 2 * c + l] += lm * yy;
-              mu[2 * l + d] += lm * xl;
-              cst -= lm * xl * yy;
-            }
+            // R1: lower plane yl f + xl g - xl yl, upper plane yh f + xl g - xl yh (squares
+            // E_cc E_cc included: their lower plane is the tangent at the lower end, reading O17)
+            const double yy = lm >= 0 ? yl : yh;
+            lam[(i - 1) * 4 + 2 * c + l] += lm * yy;
+            mu[2 * l + d] += lm * xl;
+            cst -= lm * xl * yy;
           }
         }
     Aff r = aff_zero();
@@ -570,6 +562,23 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
     }
     return r;
   };
+  // intermediate bounds by back-substitution too (CROWN): level by level, each
+  // entry of P^i is bounded by propagating it back to E with the (already refined) bounds
+  // of the levels below, intersected with its forward bound (both are sound)
+  for (int i = 2; i <= k; ++i)
+    for (int e = 0; e < 4; ++e)
+      for (int side = 0; side < 2; ++side) {
+        const double sg = side == 0 ? 1.0 : -1.0;
+        std::vector<double> lam((k + 1) * 4, 0.0);
+        lam[i * 4 + e] = sg;
+        const Aff b = backsub(lam, i, 0.0);
+        double lo = b.b;
+        for (int v = 0; v < n; ++v) lo -= std::fabs(b.A[v]);
+        if (side == 0)
+          Bl[i * 4 + e] = std::max(Bl[i * 4 + e], lo);
+        else
+          Bh[i * 4 + e] = std::min(Bh[i * 4 + e], -lo);
+      }
   for (int out = 0; out < 4; ++out) {
     const int oa = out / 2, ob = out % 2;
     for (int side = 0; side < 2; ++side) {
@@ -578,12 +587,22 @@ int matrix_inv(const Form* X, int n, int k, Form* conic, double& eps, double& rh
       for (int i = 1; i <= k; ++i)
         for (int m = 0; m < 2; ++m) lam[i * 4 + 2 * m + ob] = sg * X0[2 * oa + m];
       const Aff bnd = backsub(lam, k, sg * X0[out]);  // i = 0 term: X0 . I
+      // keep, per entry and side, the tighter (by concretisation) of the forward form and
+      // the back-substituted bound: both are sound
+      auto lower_of = [&](const Aff& a) {
+        double v = a.b;
+        for (int t = 0; t < n; ++t) v -= std::fabs(a.A[t]);
+        return v;
+      };
       if (side == 0) {
-        conic[out].lo = bnd;
-        conic[out].lo.b -= eps;
+        Aff cand = bnd;
+        cand.b -= eps;
+        if (lower_of(cand) > lower_of(conic[out].lo)) conic[out].lo = cand;
       } else {
-        conic[out].hi = aff_scale(bnd, -1.0);
-        conic[out].hi.b += eps;
+        Aff cand = aff_scale(bnd, -1.0);
+        cand.b += eps;
+        if (-lower_of(aff_scale(cand, -1.0)) < -lower_of(aff_scale(conic[out].hi, -1.0)))
+          conic[out].hi = cand;
       }
     }
   }

@@ -408,8 +408,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   unsigned long long* ctr = P<unsigned long long>(ctx->counters);
   // BS is a performance knob: clamp it to what fits in shared memory at this n, and to 128
   // (k_tile's 256-position skip ring covers a batch plus the 128 positions before it)
-  bs = std::min(bs, 128);
-  while (bs > 1 && tile_smem_bytes(nv, G.ts, bs) > 96 * 1024) bs >>= 1;
+  bs = tile_batch(nv, G.ts, bs);
   if (pt) CK(cudaEventRecord(ctx->ev[1], st));
   if (do_setup) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
@@ -657,6 +656,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.hi = hi;
   ta.active = ctr + C_ACTIVE;
   ta.dbg = ctx->debug ? P<unsigned long long>(ctx->dbg) : nullptr;
+  ta.kver = tile_kernel_version(G.ts);
   ctx->last_items = (int)n_items;
   ctx->last_grid = grid;
   ctx->last_R = R;

@@ -346,6 +346,7 @@ struct TileArgs {
   float* hi;
   unsigned long long* active; // active pair counter
   unsigned long long* dbg;    // [DBG_N] rare-path counters (as_debug_counters) or nullptr
+  int kver;                   // tile kernel version (tile_kernel_version): partial layout
 };
 // rare-path counters of the tile kernel (as_debug_counters): evidence that every slow path
 // of the exception machinery runs in some parity case
@@ -363,6 +364,8 @@ void launch_union(const float* slo, const float* shi, float* lo, float* hi, int6
                   cudaStream_t st);
 int tile_threads(int ts);
 size_t tile_ring_slot_bytes(int ts);
+int tile_kernel_version(int ts);
+int tile_batch(int nv, int ts, int bs);
 int tile_subblocks(int ts);
 int tile_grid(int nv, int ts, int bs);
 size_t tile_smem_bytes(int nv, int ts, int bs);

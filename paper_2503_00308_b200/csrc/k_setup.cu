@@ -412,11 +412,69 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
       L.add_const(xp, -eps, eps);      // l.6-7, union
       conic[2 * a + b] = xp;
     }
-  if (bwd && ok) {
-    // NEXT-4 (reading O17): each conic entry's lower / upper affine bound by propagating its
-    // coefficients backwards through Xp = X0 + X0 sum_i P^i, P^i = P^{i-1} E (R1 planes, R2 at
-    // i = 2 on the diagonal, forward bounds of the operands) down to E, affine in xi.  The
-    // recursion is on scalars (uniform over the lanes); the final substitution per lane.
+  if (bwd) {  // uniform over the warp (the refinement shuffles); FAIL Gaussians' results unused
+    // NEXT-4 (reading O17): lower affine bound of  cst + sum_{i=1..top} (init + [i == top] lam0) . P^i
+    // by propagating the coefficients backwards through P^i = P^{i-1} E with the fixed R1
+    // planes (squares included) and the operand bounds Bl / Bh, down to E (affine in xi).
+    // The recursion is on scalars (uniform over the lanes); the result is this lane's
+    // coefficient of the bound.
+    auto backsub = [&](int top, const double (&lam0)[4], const double (&init)[4], double cst) {
+      double lam[4], mu[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) lam[e] = lam0[e];
+#pragma unroll 1
+      for (int it = top; it >= 2; --it) {
+        double nxt[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) nxt[e] = init[e];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int dd = 0; dd < 2; ++dd) {
+            const double lm = lam[2 * c + dd];
+            if (lm == 0.0) continue;
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+              const double xl = Bl[it - 1][2 * c + l];
+              const double yl = Bl[1][2 * l + dd], yh = Bh[1][2 * l + dd];
+              const double yy = lm >= 0 ? yl : yh;
+              nxt[2 * c + l] += lm * yy;
+              mu[2 * l + dd] += lm * xl;
+              cst -= lm * xl * yy;
+            }
+          }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lam[e] = nxt[e];
+      }
+      double rl = L.cst() ? cst : 0.0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double ce = mu[e] + lam[e];  // P^1 = E
+        rl += ce * (ce >= 0 ? E[e].l : E[e].u);
+      }
+      return rl;
+    };
+    // intermediate bounds by back-substitution as well (CROWN), level by level,
+    // intersected with the forward ones; levels past this Gaussian's order run for the
+    // uniform shuffle trip count and are unused
+    const double zero4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int it = 2; it <= k_warp && it < KB; ++it)
+#pragma unroll 1
+      for (int e = 0; e < 4; ++e)
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          const double sg = side == 0 ? 1.0 : -1.0;
+          double unit[4] = {0.0, 0.0, 0.0, 0.0};
+          unit[e] = sg;
+          const double rl = backsub(it, unit, zero4, 0.0);
+          double lo, hi;
+          L.conc(HL{rl, rl}, lo, hi);
+          if (side == 0)
+            Bl[it][e] = fmax(Bl[it][e], lo);
+          else
+            Bh[it][e] = fmin(Bh[it][e], -lo);
+        }
 #pragma unroll 1
     for (int out = 0; out < 4; ++out) {
       const int oa = out >> 1, ob = out & 1;
@@ -424,57 +482,23 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
       for (int side = 0; side < 2; ++side) {
         const double sg = side == 0 ? 1.0 : -1.0;  // lower bound of sg * Conic_ab
         double init[4] = {0.0, 0.0, 0.0, 0.0};
-        init[0 + ob] = sg * X0[2 * oa];      // coefficient on P^i_{0 ob}
+        init[0 + ob] = sg * X0[2 * oa];      // coefficient on P^i_{0 ob}, every level
         init[2 + ob] = sg * X0[2 * oa + 1];  // on P^i_{1 ob}
-        double lam[4], mu[4] = {0.0, 0.0, 0.0, 0.0};
-        double cst = sg * X0[out];  // i = 0: X0 . I
-#pragma unroll
-        for (int e = 0; e < 4; ++e) lam[e] = init[e];
-#pragma unroll 1
-        for (int it = k_own; it >= 2; --it) {
-          double nxt[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) nxt[e] = init[e];
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int dd = 0; dd < 2; ++dd) {
-              const double lm = lam[2 * c + dd];
-              if (lm == 0.0) continue;
-#pragma unroll
-              for (int l = 0; l < 2; ++l) {
-                const double xl = Bl[it - 1][2 * c + l], xh = Bh[it - 1][2 * c + l];
-                const double yl = Bl[1][2 * l + dd], yh = Bh[1][2 * l + dd];
-                if (it == 2 && c == l && l == dd) {  // E_cc * E_cc: R2
-                  if (lm >= 0) {
-                    const double pp = fmin(fmax(0.0, xl), xh);
-                    mu[2 * c + c] += lm * 2.0 * pp;
-                    cst -= lm * pp * pp;
-                  } else {
-                    mu[2 * c + c] += lm * (xl + xh);
-                    cst -= lm * xl * xh;
-                  }
-                } else {  // R1 planes
-                  const double yy = lm >= 0 ? yl : yh;
-                  nxt[2 * c + l] += lm * yy;
-                  mu[2 * l + dd] += lm * xl;
-                  cst -= lm * xl * yy;
-                }
-              }
-            }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) lam[e] = nxt[e];
+        const double rl = backsub(k_own, init, init, sg * X0[out]);  // i = 0: X0 . I
+        // per entry and side the tighter (by concretisation) of the forward form and the
+        // back-substituted bound (both sound)
+        double a0, a1, b0, b1;
+        if (side == 0) {
+          const double cand = rl - (L.cst() ? eps : 0.0);
+          L.conc(HL{cand, cand}, a0, a1);
+          L.conc(HL{conic[out].l, conic[out].l}, b0, b1);
+          if (ok && a0 > b0) conic[out].l = cand;
+        } else {
+          const double cand = -rl + (L.cst() ? eps : 0.0);
+          L.conc(HL{cand, cand}, a0, a1);
+          L.conc(HL{conic[out].u, conic[out].u}, b0, b1);
+          if (ok && a1 < b1) conic[out].u = cand;
         }
-        double rl = L.cst() ? cst : 0.0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double ce = mu[e] + lam[e];  // P^1 = E
-          rl += ce * (ce >= 0 ? E[e].l : E[e].u);
-        }
-        if (side == 0)
-          conic[out].l = rl - (L.cst() ? eps : 0.0);
-        else
-          conic[out].u = -rl + (L.cst() ? eps : 0.0);
       }
     }
   }

@@ -786,6 +786,41 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.active, (unsigned long long)v);
 }
 
+// ---- bulk-async (TMA engine) staging helpers: 1-D cp.async.bulk global -> shared with an
+// mbarrier completing on the transferred bytes (SASS: UBLKCP / SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// order this thread's earlier generic-proxy accesses to shared memory before async-proxy
+// (bulk copy) writes to it
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ======================================================================== v2 tile kernel
 // Work item = one 16x16 pixel block of a tile (TS >= 16) over one chunk of its list, 128
 // threads, TWO pixels per thread: lane (x, y) of warp quadrant (qx, qy) owns the pixels
@@ -1047,10 +1082,20 @@ __global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
   double* cx2 = reinterpret_cast<double*>(srec + BS);  // [BS][16] per column
   double* cy2 = cx2 + (size_t)BS * B2;                 // [BS][16] per row
   FinS* fins = reinterpret_cast<FinS*>(cy2 + (size_t)BS * B2);  // [FB]
+  // raw per-Gaussian records of the next batch, gathered by the bulk-copy engine while the
+  // current batch is walked (one mbarrier phase per batch)
+  HotRec<NV>* raw = reinterpret_cast<HotRec<NV>*>(fins + FB);     // [BS]
+  __shared__ __align__(8) unsigned long long s_bar;
   const bool has_exc = A.pm != nullptr;
   const int tid = threadIdx.x;
   float2* rf = has_exc ? reinterpret_cast<float2*>(A.ring) + (size_t)blockIdx.x * A.R * 4 * T2 + tid
                        : nullptr;
+  constexpr unsigned HSZ = sizeof(HotRec<NV>);
+  const HotRec<NV>* hot = reinterpret_cast<const HotRec<NV>*>(A.hot);
+  if (tid == 0) mbar_init(&s_bar, 1);
+  fence_proxy_async();
+  __syncthreads();
+  unsigned phase = 0;
   const int lx = v2_x(tid), ly = v2_y(tid);
   const float du0 = (float)lx + 0.5f - 0.5f * B2;
   const float2 DU1 = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
@@ -1086,21 +1131,36 @@ __global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
     float2 alc[3] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
     float2 recb = f2(1.f, 1.f), recl = f2(1.f, 1.f);
     bool rec = false;
+    // gather the item's first batch (later batches are prefetched during the previous walk)
+    if (scan0 < scan1) {
+      const int nb0 = min(BS, scan1 - scan0);
+      if (tid < nb0) {
+        const int32_t g = A.vals[tb + scan0 + tid];
+        fence_proxy_async();
+        bulk_g2s(raw + tid, hot + g, HSZ, &s_bar);
+      }
+      if (tid == 0) mbar_expect_tx(&s_bar, nb0 * HSZ);
+    }
 
     for (int b0 = scan0; b0 < scan1; b0 += BS) {
       const int nb = min(BS, scan1 - b0);
+      const int nbn = min(BS, scan1 - (b0 + nb));  // next batch (0: none)
       int f0l = 0, f1l = 0;
       if (tid == 0 && iexc) {
         f0l = A.finstart[tb + b0];
         f1l = A.finstart[tb + b0 + nb];
       }
+      // the next batch's Gaussian ids, loaded now so the copies can be issued right after
+      // this batch's records are staged
+      const int32_t gnext = tid < nbn ? A.vals[tb + b0 + nb + tid] : 0;
       __syncthreads();
+      mbar_wait(&s_bar, phase);  // this batch's raw records have landed
+      phase ^= 1u;
       // ---- phase A: metadata + cull tables (one thread per Gaussian, highest ids) and
       //      staging (NPART threads per Gaussian), as in k_tile
       for (int j = T2 - 1 - tid; j < nb; j += T2) {
         const int64_t gp = tb + b0 + j;
-        const int32_t g = A.vals[gp];
-        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + g;
+        const HotRec<NV>* H = raw + j;
         SRec2<NV>& S = srec[j];
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
         const double r2 = H->r2;
@@ -1158,7 +1218,7 @@ __global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
       }
       for (int jj = tid; jj < NPART * nb; jj += T2) {
         const int j = jj / NPART, part = jj % NPART;
-        const HotRec<NV>* H = reinterpret_cast<const HotRec<NV>*>(A.hot) + A.vals[tb + b0 + j];
+        const HotRec<NV>* H = raw + j;
         bool skip;
         {
           const double dx = fmax(0.0, fmax(__dsub_rn(H->mu[0], bx1), __dsub_rn(bx0, H->mu[2])));
@@ -1172,6 +1232,12 @@ __global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
         s_F[1] = f1l;
       }
       __syncthreads();
+      // raw records consumed: gather the next batch's while this one is walked
+      if (tid < nbn) {
+        fence_proxy_async();
+        bulk_g2s(raw + tid, hot + gnext, HSZ, &s_bar);
+      }
+      if (tid == 0 && nbn > 0) mbar_expect_tx(&s_bar, nbn * HSZ);
       // ---- phase B: T_hi window operand lists (warp 0) and staged finalisation records
       if (iexc) {
         for (int j = tid < 32 ? tid : nb; j < nb; j += 32) {
@@ -1596,7 +1662,9 @@ __global__ void k_merge(TileArgs A) {
   const int n = A.item_cnt[tile];
   if (n <= 1) return;
   const int ts = A.ts, npix = ts * ts;
-  const bool v2 = ts >= B2;  // k_tile2 layout: 16x16 blocks, row-major pixels
+  // partial layout of the kernel that wrote them: k_tile2 16x16 blocks (row-major pixels),
+  // k_tile its 16x8 / 8x8 blocks
+  const bool v2 = A.kver == 2;
   const int SBX = v2 ? B2 : block_w(ts), SBH = v2 ? B2 : SBY, SBP = SBX * SBH;
   const int nsbx = ts / SBX, nsub = nsbx * (ts / SBH);
   const int tx = tile % A.ntx, ty = tile / A.ntx;
@@ -1643,19 +1711,40 @@ __global__ void k_merge(TileArgs A) {
   }
 }
 
-// TS >= 16: k_tile2 (16x16 blocks, two pixels per thread); TS = 8: k_tile (8x8 blocks)
-int tile_threads(int ts) { return ts >= B2 ? T2 : block_w(ts) * SBY; }
-int tile_subblocks(int ts) { return ts >= B2 ? (ts / B2) * (ts / B2) : (ts / block_w(ts)) * (ts / SBY); }
-size_t tile_ring_slot_bytes(int ts) {  // exception ring bytes per slot per CTA
-  return ts >= B2 ? (size_t)4 * T2 * sizeof(float2) : (size_t)tile_threads(ts) * sizeof(float4);
+// kernel version: 2 = k_tile2 (TS >= 16: 16x16 blocks, two pixels per thread), 1 = k_tile
+// (TS = 8).  A warp-independent variant (every warp its own 8x8 quadrant work items, no CTA
+// barrier) measured 44 ms on C4 against k_tile2's 27.5 ms (4x the staging per pixel, each
+// warp waiting on its own record loads) and was removed.
+int tile_kernel_version(int ts) { return ts >= B2 ? 2 : 1; }
+int tile_threads(int ts) { return tile_kernel_version(ts) == 2 ? T2 : block_w(ts) * SBY; }
+int tile_subblocks(int ts) {
+  return tile_kernel_version(ts) == 2 ? (ts / B2) * (ts / B2) : (ts / block_w(ts)) * (ts / SBY);
 }
+size_t tile_ring_slot_bytes(int ts) {  // exception ring bytes per slot per CTA
+  return tile_kernel_version(ts) == 2 ? (size_t)4 * T2 * sizeof(float2)
+                                      : (size_t)tile_threads(ts) * sizeof(float4);
+}
+int tile_batch(int nv, int ts, int bs);
 
 template <int NV>
 static size_t smem_for(int ts, int bs) {
   if (ts >= B2)
-    return (size_t)bs * (sizeof(SRec2<NV>) + 2 * B2 * sizeof(double)) + FB * sizeof(FinS);
+    return (size_t)bs * (sizeof(SRec2<NV>) + 2 * B2 * sizeof(double) + sizeof(HotRec<NV>)) +
+           FB * sizeof(FinS);
   return (size_t)bs * (sizeof(SRec<NV>) + (block_w(ts) + SBY) * sizeof(double)) +
          FB * sizeof(FinS);
+}
+
+// BS clamped to what fits (<= 96 KB of shared memory) and to 128 (the 256-position skip
+// ring covers a batch plus the 128 positions before it)
+int tile_batch(int nv, int ts, int bs) {
+  bs = std::min(bs, 128);
+  if (tile_kernel_version(ts) == 2) {  // k_tile2: keep four CTAs per SM (registers allow four)
+    while (bs > 1 && tile_smem_bytes(nv, ts, bs) > 54 * 1024) --bs;
+    return bs;
+  }
+  while (bs > 1 && tile_smem_bytes(nv, ts, bs) > 96 * 1024) bs >>= 1;
+  return bs;
 }
 
 size_t tile_smem_bytes(int nv, int ts, int bs) {
@@ -1697,7 +1786,7 @@ static int grid_v2(int ts, int bs) {
 }
 template <int NV>
 static int grid_one(int ts, int bs) {
-  if (ts >= B2) return grid_v2<NV>(ts, bs);
+  if (tile_kernel_version(ts) == 2) return grid_v2<NV>(ts, bs);
   return block_w(ts) == 16 ? grid_bx<NV, 16>(ts, bs) : grid_bx<NV, 8>(ts, bs);
 }
 
@@ -1715,7 +1804,7 @@ int tile_grid(int nv, int ts, int bs) {
 
 template <int NV>
 static void launch_one(const TileArgs& a, int grid, cudaStream_t st) {
-  if (a.ts >= B2)
+  if (a.kver == 2)
     k_tile2<NV><<<grid, T2, smem_for<NV>(a.ts, a.bs), st>>>(a);
   else if (block_w(a.ts) == 16)
     k_tile<NV, 16><<<grid, 16 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);

@@ -111,3 +111,37 @@ def regions(sass_csv, dis, fn, spans):
         acc[name][1] += ns
     for k, (a, b) in sorted(acc.items(), key=lambda kv: -kv[1][1]):
         print(f"{k:20s} instr {100*a/ti:6.2f}%  stall-samples {100*b/ts:6.2f}%")
+
+
+def stall_regions(sass_csv, dis, fn, spans, kinds=("stall_wait", "stall_long_sb", "stall_barrier",
+                                                    "stall_selected", "stall_not_selected",
+                                                    "stall_math", "stall_short_sb")):
+    """Per region: samples of each stall reason (share of all samples)."""
+    m = line_map(dis, fn, "")
+    rows = list(csv.reader(open(sass_csv)))
+    hdr = rows[1]
+    ia = hdr.index("Address")
+    ik = [hdr.index(k) for k in kinds]
+    base = None
+    acc = defaultdict(lambda: [0.0] * len(kinds))
+    tot = 0.0
+    for r in rows[2:]:
+        try:
+            addr = int(r[ia], 16)
+        except (ValueError, IndexError):
+            continue
+        base = addr if base is None else base
+        src, _ = m.get(addr - base, (None, "?"))
+        name = "other"
+        if src:
+            for nm, sp in spans.items():
+                if any(f in src[0] and lo <= src[1] <= hi for f, lo, hi in sp):
+                    name = nm
+                    break
+        for j, i in enumerate(ik):
+            v = float(r[i] or 0)
+            acc[name][j] += v
+            tot += v
+    print(f"{'region':16s} " + " ".join(f"{k.replace('stall_',''):>9s}" for k in kinds))
+    for k, vals in sorted(acc.items(), key=lambda kv: -sum(kv[1])):
+        print(f"{k:16s} " + " ".join(f"{100*v/tot:9.2f}" for v in vals))
