@@ -241,11 +241,60 @@ def count_launches(step):
         return None, {"error": str(ex)}
 
 
+def emulate_world(ctx, args, w, tile, batch, shard):
+    """Per-rank device time of an N-rank render, every rank run in turn on this one GPU (no
+    rank waits on another: SURVEY §8(e) readiness without an N-GPU node).  Tiles: each rank
+    runs what it would run alone (setup, tile cost count, device LPT, its tiles) through
+    as_render_shard; sub-boxes: its sub-box range through as_render_subboxes.  The collective
+    is not included: its bytes are reported with the 770 GB/s per-direction NVLink figure of
+    B200_PROFILING.md as an estimate."""
+    import torch
+    N = args.emulate_world
+    H, W = w.camera["H"], w.camera["W"]
+    nt = ctx.n_tiles(tile)
+    per = -(-nt // N)
+    cap = per + max(1, per // 4)
+    lo_tm = torch.empty((cap, tile * tile, 3), dtype=torch.float32, device=f"cuda:{ctx.device}")
+    hi_tm = torch.empty_like(lo_tm)
+    img_lo = torch.empty((H, W, 3), dtype=torch.float32, device=f"cuda:{ctx.device}")
+    img_hi = torch.empty_like(img_lo)
+    from paper_2503_00308_b200.dist import subbox_range
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{ctx.device}")
+
+    def one(r):
+        if shard == "subboxes":
+            b, e = subbox_range(w.n_sub, r, N)
+            ctx.as_render_subboxes(b, e, tile, batch, img_lo, img_hi, stats=False)
+        else:
+            ctx.as_render_shard(tile, batch, r, N, cap, lo_tm, hi_tm, stats=False)
+
+    ms = []
+    for r in range(N):
+        one(r)  # warm-up of this rank's buffers
+        t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0.record()
+            one(r)
+            e1.record()
+            torch.cuda.synchronize()
+            t.append(e0.elapsed_time(e1))
+        ms.append(float(np.median(t)))
+    gbytes = (2 * N * cap * tile * tile * 3 * 4) if shard != "subboxes" else 2 * H * W * 3 * 4
+    return {"N": N, "axis": shard, "ms_per_rank": ms, "max_ms": max(ms),
+            "collective_bytes_per_rank": gbytes,
+            "collective_ms_estimate_770GBps": gbytes / 770e9 * 1e3,
+            "note": "ranks run one after another on one GPU; speedup = single-GPU ms / "
+                    "(max_ms + collective estimate), computed by the reader"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2503_00308_b200 import Context
-    from paper_2503_00308_b200.dist import ShardedRenderer, SubboxShardedRenderer
+    from paper_2503_00308_b200.dist import init_comm, subbox_range
     from workloads import make_config
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -275,20 +324,15 @@ def run_ours(args):
     shard = args.shard
     if shard == "auto":  # sub-boxes when the partition covers every rank (no replicated work)
         shard = "subboxes" if P >= world else "tiles"
-    if world == 1:
-        sr = None
-    elif shard == "subboxes":
-        sr = SubboxShardedRenderer(ctx, rank, world, tile=tile, batch=batch)
-    else:
-        sr = ShardedRenderer(ctx, rank, world, tile=tile, batch=batch)
-    parallelism = (f"sub-box ranges over {world} GPU(s), one all-reduce min/max"
-                   if sr is not None and shard == "subboxes" else
-                   f"image tiles over {world} GPU(s), LPT owner map, one all-gather")
+    if world > 1:  # the library's own communicator: the collective runs inside as_render_bounds
+        init_comm(ctx, rank, world, axis=2 if shard == "subboxes" else 1)
+    parallelism = (f"sub-box ranges over {world} GPU(s), one NCCL all-reduce min/max inside "
+                   f"the library" if shard == "subboxes" else
+                   f"image tiles over {world} GPU(s), device LPT owner map, one NCCL all-gather "
+                   f"inside the library")
 
     def step(stats=True):
-        if sr is None:
-            return ctx.as_render_bounds(tile, batch, lo, hi, stats=stats)[2]
-        return sr.step(stats=stats)[2]
+        return ctx.as_render_bounds(tile, batch, lo, hi, stats=stats)[2]
 
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     for _ in range(args.warmup):
@@ -374,13 +418,7 @@ def run_ours(args):
         def e2e_step():
             ctx.as_load_scene(mean, chol, opac, col)
             ctx.as_set_scene_box(w.scene_box)
-            if sr is None:
-                ctx.as_render_bounds(tile, batch, hlo, hhi, stats=False)
-            else:
-                olo, ohi, _ = sr.step(stats=False)
-                if rank == 0:
-                    hlo.copy_(olo)
-                    hhi.copy_(ohi)
+            ctx.as_render_bounds(tile, batch, hlo, hhi, stats=False)
         e2e_step()
         torch.cuda.synchronize()
         times = []
@@ -407,14 +445,17 @@ def run_ours(args):
 
     # ---- bound widths (metric part 2) and CPU baseline (rank 0, N=1)
     out = None
-    fin = sr.step(stats=False) if sr is not None else None  # collective: every rank takes part
+    step(stats=False)  # collective: every rank takes part; full images on every rank
+    emu = None
+    if args.emulate_world > 1 and world == 1:
+        eshard = args.shard if args.shard != "auto" else (
+            "subboxes" if P >= args.emulate_world else "tiles")
+        emu = emulate_world(ctx, args, w, tile, batch, eshard)
+    if emu is not None:
+        emu["speedup_estimate"] = ms / (emu["max_ms"] + emu["collective_ms_estimate_770GBps"])
     if rank == 0:
-        if sr is not None:
-            lo_np = fin[0].cpu().numpy().astype(np.float64)
-            hi_np = fin[1].cpu().numpy().astype(np.float64)
-        else:
-            lo_np = lo.cpu().numpy().astype(np.float64)
-            hi_np = hi.cpu().numpy().astype(np.float64)
+        lo_np = lo.cpu().numpy().astype(np.float64)
+        hi_np = hi.cpu().numpy().astype(np.float64)
         gap = np.linalg.norm(hi_np - lo_np, axis=-1)
         widths = {"mpg": float(gap.mean()), "xpg": float(gap.max()),
                   "mean_channel_width": float((hi_np - lo_np).mean())}
@@ -447,11 +488,13 @@ def run_ours(args):
                           "chunk_target": args.chunk_target or "auto"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": gpu_launches, "launch_kernels": names, "clocks": clocks,
+               "emulated_world": emu,
                "bound_width": widths,
                "stats": {k: st[k] for k in ("pairs", "active_pairs", "uncertain_pairs", "fails",
                                             "straddles", "dropped", "kmax", "ms_setup", "ms_bin",
                                             "ms_pairs", "ms_tile", "device_bytes", "n_items",
-                                            "grid", "ring_len", "max_window")}}
+                                            "grid", "ring_len", "max_window", "ms_gather",
+                                            "world", "n_owned", "peak_bytes")}}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -476,6 +519,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--chunk-target", type=int, default=0,
                     help="positions per (tile, chunk) work item (0 = automatic)")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="N > 1: also time every rank of an N-rank render on this one GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -37,7 +37,8 @@ typedef enum {
   AS_E_NUMERIC = 3, /* reserved: numerical failure that has no sound fallback */
   AS_E_CUDA = 4,    /* a CUDA runtime call failed */
   AS_E_OOM = 5,     /* device allocation failed */
-  AS_E_STATE = 6    /* call order violated (e.g. render before as_load_scene) */
+  AS_E_STATE = 6,   /* call order violated (e.g. render before as_load_scene) */
+  AS_E_COMM = 7     /* NCCL unavailable or a collective failed (multi-GPU contexts) */
 } as_status;
 
 /* Camera.  Extrinsics as XYZ Euler angles of the camera->world
@@ -111,6 +112,11 @@ typedef struct {
   int32_t grid;            /* persistent CTAs of the tile kernel (last sub-box) */
   int32_t ring_len;        /* exception ring length R (last sub-box; 1 = no exceptions) */
   int32_t max_window;      /* longest exception window, positions (max over sub-boxes) */
+  double ms_gather;        /* multi-GPU: the collective (all-gather of bound tiles or
+                              all-reduce min/max of sub-box unions) and the untile */
+  int32_t world;           /* ranks of the context's communicator (1 = single GPU) */
+  int32_t n_owned;         /* tiles this rank rendered (tile sharding), else n_tiles */
+  size_t peak_bytes;       /* device bytes held by the context at its largest */
 } as_stats;
 
 /* Flags */
@@ -234,6 +240,31 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
  * (ties: lower rank).  owner: int32 [n_tiles]. */
 as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, int32_t cap,
                         int32_t* owner);
+
+/* ---- multi-GPU: one process (or host thread) per GPU, one NCCL communicator per context
+ * (north_star (3): image tiles across GPUs with ONE gather of the bound images; SURVEY.md
+ * §8(b), §8(e)).  NCCL is resolved at run time (libnccl.so.2, the copy the process already
+ * loaded if any); AS_E_COMM when it is unavailable or a call fails.
+ *   as_nccl_id: writes a fresh NCCL unique id (128 bytes) into id; call on one rank and pass
+ *     the bytes to every rank by any out-of-band channel.
+ *   as_comm_init: joins rank `rank` of `world` (1 <= world <= 128) on the context's device
+ *     (collective: every rank calls it with the same id).  A context joined with world > 1
+ *     renders in parallel: as_render_bounds / as_render_subboxes split the work over the
+ *     ranks, run ONE collective on the context stream and write the complete lo / hi on
+ *     every rank.  Axis (as_set_shard_axis): 1 = image tiles -- every rank runs the
+ *     per-Gaussian setup and a per-tile cost count, the deterministic device LPT owner map
+ *     (identical on every rank, that of as_lpt_assign with cap = ceil(n_tiles/world) +
+ *     max(1, ceil(n_tiles/world)/4)) picks this rank's tiles, they are rendered into a compact
+ *     tile-major buffer, one ncclAllGather of the bound tiles and an on-device untile follow;
+ *     2 = sub-boxes -- rank r renders the union over its contiguous balanced range of the
+ *     sub-boxes (as_render_subboxes semantics) and one ncclAllReduce MIN on lo / MAX on hi
+ *     completes the union (step 22); 0 (default) = sub-boxes when there are at
+ *     least `world` sub-boxes, else tiles.  With world == 1 an explicit axis still runs the
+ *     collective path (single-rank communicator), which tests it on one GPU.
+ *   The result is bitwise identical to the single-GPU render for both axes. */
+as_status as_nccl_id(uint8_t id[128]);
+as_status as_comm_init(as_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]);
+as_status as_set_shard_axis(as_ctx* ctx, int32_t axis);
 
 /* ---- device scratch allocator ----
  * All device memory the context holds (scene copy, per-Gaussian records, pair lists, sort

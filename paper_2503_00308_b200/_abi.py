@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libabsplat.so")
+# ABSPLAT_LIB: an alternative in-tree build of the same library (A/B performance runs)
+LIB_PATH = os.environ.get("ABSPLAT_LIB") or os.path.join(HERE, "libabsplat.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "absplat.h")
 
 AS_PTR_DEVICE = 1
@@ -16,7 +17,7 @@ AS_ASYNC = 2
 AS_MAX_VARS = 9
 
 STATUS = {0: "AS_OK", 1: "AS_E_ARG", 2: "AS_E_SCENE", 3: "AS_E_NUMERIC", 4: "AS_E_CUDA",
-          5: "AS_E_OOM", 6: "AS_E_STATE"}
+          5: "AS_E_OOM", 6: "AS_E_STATE", 7: "AS_E_COMM"}
 
 
 class AsCamera(C.Structure):
@@ -46,7 +47,8 @@ class AsStats(C.Structure):
                 ("ms_bin", C.c_double), ("ms_pairs", C.c_double), ("ms_tile", C.c_double),
                 ("ms_total", C.c_double), ("tile_kernel_ms", C.c_double),
                 ("device_bytes", C.c_size_t), ("n_items", C.c_int32), ("grid", C.c_int32),
-                ("ring_len", C.c_int32), ("max_window", C.c_int32)]
+                ("ring_len", C.c_int32), ("max_window", C.c_int32), ("ms_gather", C.c_double),
+                ("world", C.c_int32), ("n_owned", C.c_int32), ("peak_bytes", C.c_size_t)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -102,6 +104,9 @@ def lib():
         "as_set_blend": (i32, [P, i32]),
         "as_set_inverse_mode": (i32, [P, i32]),
         "as_debug_counters": (i32, [P, i32, P]),
+        "as_nccl_id": (i32, [P]),
+        "as_comm_init": (i32, [P, i32, i32, P]),
+        "as_set_shard_axis": (i32, [P, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

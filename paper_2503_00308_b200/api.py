@@ -274,6 +274,19 @@ class Context:
         self._check(self._L.as_debug_counters(self._ctx, int(enable), out.ctypes.data))
         return {k: int(v) for k, v in zip(self.DEBUG_COUNTERS, out)}
 
+    def as_comm_init(self, rank: int, world: int, uid: bytes):
+        """Join rank `rank` of `world` with the 128-byte NCCL id from as_nccl_id (collective).
+        Afterwards as_render_bounds / as_render_subboxes shard the work over the ranks and
+        return the complete images on every rank (include/absplat.h)."""
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        self._check(self._L.as_comm_init(self._ctx, int(rank), int(world), buf))
+
+    def as_set_shard_axis(self, axis: int = 0):
+        """Multi-GPU axis: 0 auto, 1 image tiles (all-gather), 2 sub-boxes (all-reduce)."""
+        self._check(self._L.as_set_shard_axis(self._ctx, int(axis)))
+
     def as_set_inverse_mode(self, backward: int = 0):
         """MatrixInv conic bounds: 0 forward forms, 1 back-substitution (NEXT-4)."""
         self._check(self._L.as_set_inverse_mode(self._ctx, int(backward)))
@@ -380,6 +393,16 @@ def as_untile(W: int, H: int, tile: int, world: int, max_tiles: int, owned, n_ow
         msg = L.as_last_error(c).decode() if c is not None else "as_untile failed"
         raise AbsplatError(st, msg)
     return lo, hi
+
+
+def as_nccl_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for as_comm_init; AbsplatError(AS_E_COMM) when the
+    process cannot load NCCL."""
+    buf = (C.c_uint8 * 128)()
+    st = _abi.lib().as_nccl_id(buf)
+    if st != 0:
+        raise AbsplatError(st, "as_nccl_id: NCCL unavailable")
+    return bytes(buf)
 
 
 def as_version() -> int:

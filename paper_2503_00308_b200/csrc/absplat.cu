@@ -3,12 +3,15 @@
 // sort -> bin -> tile sort -> pair classification -> tile kernel), tile sharding (LPT owner
 // map, compact tile-major outputs, untile), and the concrete renderer used by tests.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -59,7 +62,7 @@ struct as_ctx {
   DevBuf item_off, items, items2, item_key, item_key2, item_idx, item_order, item_cnt, partial, work_counter;
   DevBuf finkey, finkey2, finval, finval2, finstart, finrec, maskF, maskG;
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
-  size_t bytes = 0;
+  size_t bytes = 0, peak_bytes = 0;
   int64_t launches = 0;
   int last_items = 0, last_grid = 0, last_R = 1, max_window = 0, last_wmax = 0;
   cudaEvent_t ev[8] = {};
@@ -74,6 +77,14 @@ struct as_ctx {
   int blend_mode = 0;  // as_set_blend: 0 interval, 1 + linear on exception-free tiles
   bool debug = false;  // as_debug_counters: rare-path counters of the tile kernel
   DevBuf dbg;
+  // multi-GPU (as_comm_init): NCCL communicator of this rank, shard axis, gather buffers,
+  // the device owner map / slots of the LPT assignment
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, world = 1;
+  int shard_axis = 0;    // as_set_shard_axis: 0 auto, 1 tiles, 2 sub-boxes
+  DevBuf gsend, grecv, lptkey, lptkey2, lptid, lptid2, tslot_all, nown;
+  double last_gather_ms = 0.0;
+  int last_n_owned = 0;
   bool last_has_exc = false;
   int64_t last_M = 0;
   DevBuf tmp_lo, tmp_hi, tile_unc, lin_tiles;
@@ -144,6 +155,7 @@ void ensure(as_ctx* ctx, DevBuf& b, size_t bytes) {
   }
   b.cap = want;
   ctx->bytes += want;
+  ctx->peak_bytes = std::max(ctx->peak_bytes, ctx->bytes);
 }
 void release(as_ctx* ctx, DevBuf& b) { free_buf(ctx, b); }
 
@@ -374,10 +386,6 @@ __global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned
     const int64_t k = te[i] - tb[i];
     if (k > 0) atomicMax(out, (unsigned long long)k);
   }
-}
-__global__ void k_slot_map(const int32_t* list, int n, int32_t* slot_of_tile) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) slot_of_tile[list[i]] = i;
 }
 
 // counters layout (unsigned long long[16])
@@ -781,6 +789,10 @@ void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_r
   out->grid = ctx->last_grid;
   out->ring_len = ctx->last_R;
   out->max_window = ctx->max_window;
+  out->ms_gather = ctx->last_gather_ms;
+  out->world = ctx->world;
+  out->n_owned = n_tiles_rendered;
+  out->peak_bytes = ctx->peak_bytes;
   (void)G;
 }
 
@@ -802,12 +814,83 @@ void lpt(int n, const int64_t* costs, int world, int cap, int32_t* owner) {
   }
 }
 
-// per-tile cost pass over all sub-boxes (setup + count), host costs out
-void tile_costs(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, std::vector<int64_t>& costs) {
+
+// ---------------------------------------------------------------- device owner map (a11)
+// Longest-processing-time assignment on the device, identical to lpt() above: tiles in
+// descending cost (ties: lower id first, the stable radix order), each to the least-loaded
+// rank with room (ties: lower rank).  One warp: lane r holds ranks r, r + 32; the argmin is
+// a warp min over (load << 7 | rank).  Then the ranks' slots in ascending tile id
+// (__match_any over each 32-tile chunk) and the per-rank counts.
+__global__ void k_lpt(const int32_t* ids, const unsigned long long* nkeys, int n, int world,
+                      int cap, int32_t* owner, int32_t* slot, int32_t* nown) {
+  __shared__ int sbase[128];
+  const int lane = threadIdx.x;
+  unsigned long long load[4] = {0, 0, 0, 0};
+  int cnt[4] = {0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long cost = ~nkeys[i];
+    const int t = ids[i];
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = lane + 32 * q;
+      if (r < world && cnt[q] < cap) best = min(best, (load[q] << 7) | (unsigned long long)r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const int r = (int)(best & 127ull);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (lane + 32 * q == r) {
+        load[q] += cost + 1;
+        ++cnt[q];
+      }
+    if (lane == 0) owner[t] = r;
+  }
+  for (int r = lane; r < 128; r += 32) sbase[r] = 0;
+  __syncwarp();
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int t = c0 + lane;
+    const bool ok = t < n;
+    const int r = ok ? owner[t] : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const unsigned peers = __match_any_sync(0xffffffffu, r) & act;
+    const int base = ok ? sbase[r] : 0;
+    __syncwarp();
+    if (ok) {
+      slot[t] = base + __popc(peers & ((1u << lane) - 1u));
+      if ((peers & ((1u << lane) - 1u)) == 0) sbase[r] = base + __popc(peers);
+    }
+    __syncwarp();
+  }
+  for (int r = lane; r < world; r += 32) nown[r] = sbase[r];
+}
+// this rank's tile -> compact slot map (-1: another rank's), and the gathered-buffer slot map
+// of every tile (rank-major [world][2][cap] layout: lo block then hi block per rank)
+__global__ void k_slot_maps(const int32_t* owner, const int32_t* slot, int n, int rank, int cap,
+                            int32_t* tslot, int32_t* gslot) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int r = owner[t];
+  if (tslot) tslot[t] = r == rank ? slot[t] : -1;
+  if (gslot) gslot[t] = r * 2 * cap + slot[t];
+}
+__global__ void k_cost_key(const unsigned long long* cost, int n, unsigned long long* key,
+                           int32_t* id) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    key[t] = ~cost[t];  // ascending ~cost == descending cost, stable ties keep the id order
+    id[t] = t;
+  }
+}
+
+// per-tile costs (pairs summed over the sub-boxes [s0, s1)) into ctx->tcost, no host sync;
+// with a single sub-box its setup is left in place for the render to reuse
+void tile_costs_dev(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int s0, int s1) {
   cudaStream_t st = ctx->stream;
   CK(cudaMemsetAsync(ctx->tcost.p, 0, sizeof(unsigned long long) * G.ntiles, st));
   unsigned long long* ctr = P<unsigned long long>(ctx->counters);
-  for (int s = 0; s < bi.n_sub; ++s) {
+  for (int s = s0; s < s1; ++s) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
     run_setup(ctx, bi, s);
     BinArgs ba{};
@@ -826,20 +909,81 @@ void tile_costs(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, std::vector<i
     launch_count(ba, st);
     LAUNCHED(ctx, 1);
   }
-  std::vector<unsigned long long> h(G.ntiles);
-  CK(cudaMemcpyAsync(h.data(), ctx->tcost.p, sizeof(unsigned long long) * G.ntiles,
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  costs.assign(h.begin(), h.end());
-  // counters of the cost pass must not leak into the render's stats; C_WSMAX (the pair
-  // window bound of the last sub-box's setup) stays valid for a render that reuses it, and so
-  // do the setup's FAIL / straddle / drop counts when there is one sub-box (the render then
-  // skips its own setup)
-  if (bi.n_sub != 1) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_WSMAX, st));
+  if (s1 - s0 != 1) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_WSMAX, st));
   else CK(cudaMemsetAsync(ctr + C_DROP + 1, 0, sizeof(unsigned long long) * (C_WSMAX - C_DROP - 1), st));
   CK(cudaMemsetAsync(ctr + C_WSMAX + 1, 0, sizeof(unsigned long long) * (C_NCOUNTERS - C_WSMAX - 1),
                      st));
 }
+
+// device LPT owner map of the current costs (ctx->tcost): ctx->owner, ctx->tslot_all (slot of
+// every tile in its owner's compact list), ctx->nown (tiles per rank)
+void device_lpt(as_ctx* ctx, const Geometry& G, int world, int cap) {
+  cudaStream_t st = ctx->stream;
+  const int n = G.ntiles;
+  ensure(ctx, ctx->lptkey, sizeof(unsigned long long) * n);
+  ensure(ctx, ctx->lptkey2, sizeof(unsigned long long) * n);
+  ensure(ctx, ctx->lptid, sizeof(int32_t) * n);
+  ensure(ctx, ctx->lptid2, sizeof(int32_t) * n);
+  ensure(ctx, ctx->tslot_all, sizeof(int32_t) * n);
+  ensure(ctx, ctx->nown, sizeof(int32_t) * 128);
+  k_cost_key<<<(n + 255) / 256, 256, 0, st>>>(P<unsigned long long>(ctx->tcost), n,
+                                               P<unsigned long long>(ctx->lptkey),
+                                               P<int32_t>(ctx->lptid));
+  LAUNCHED(ctx, 1);
+  cub_sort_keys64(ctx, P<unsigned long long>(ctx->lptkey), P<unsigned long long>(ctx->lptkey2),
+                  P<int32_t>(ctx->lptid), P<int32_t>(ctx->lptid2), n, 64);
+  k_lpt<<<1, 32, 0, st>>>(P<int32_t>(ctx->lptid2), P<unsigned long long>(ctx->lptkey2), n, world,
+                          cap, P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all),
+                          P<int32_t>(ctx->nown));
+  LAUNCHED(ctx, 1);
+}
+
+// ---------------------------------------------------------------- NCCL (loaded at run time)
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+// the process's NCCL (the one torch already loaded, if any: same soname), resolved once
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return;
+    }
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather &&
+             api.allReduce && api.errorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
+}
+
+#define NCK(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) {                                                             \
+      set_err(ctx, "%s failed: %s (%s:%d)", #call, nccl_api().errorString(r_), __FILE__, \
+              __LINE__);                                                                 \
+      throw Err{AS_E_COMM};                                                              \
+    }                                                                                    \
+  } while (0)
 
 void rot_c2w_host(const double e[3], double R[9]) {
   const double c0 = std::cos(e[0]), s0 = std::sin(e[0]), c1 = std::cos(e[1]), s1 = std::sin(e[1]);
@@ -899,11 +1043,66 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->item_key, &ctx->item_key2, &ctx->item_idx, &ctx->item_order,
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
                     &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->finstart, &ctx->finrec, &ctx->maskF,
-                    &ctx->maskG, &ctx->dbg};
+                    &ctx->maskG, &ctx->dbg, &ctx->gsend, &ctx->grecv, &ctx->lptkey,
+                    &ctx->lptkey2, &ctx->lptid, &ctx->lptid2, &ctx->tslot_all, &ctx->nown};
   for (DevBuf* b : bufs) release(ctx, *b);
+  if (ctx->comm && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)ctx->comm);
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   delete ctx;
+  return AS_OK;
+}
+
+as_status as_nccl_id(uint8_t id[128]) {
+  if (!id) return AS_E_ARG;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return AS_E_COMM;
+  ncclUniqueId u;
+  if (api.getUniqueId(&u) != ncclSuccess) return AS_E_COMM;
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  std::memcpy(id, &u, 128);
+  return AS_OK;
+}
+
+as_status as_comm_init(as_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]) {
+  if (!ctx) return AS_E_ARG;
+  if (!id || world < 1 || world > 128 || rank < 0 || rank >= world) {
+    set_err(ctx, "as_comm_init: bad arguments (rank %d, world %d)", rank, world);
+    return AS_E_ARG;
+  }
+  const NcclApi& api = nccl_api();
+  if (!api.ok) {
+    set_err(ctx, "as_comm_init: %s", api.why.c_str());
+    return AS_E_COMM;
+  }
+  try {
+    cudaSetDevice(ctx->device);
+    if (ctx->comm) {
+      api.commDestroy((ncclComm_t)ctx->comm);
+      ctx->comm = nullptr;
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclComm_t c = nullptr;
+    NCK(api.commInitRank(&c, world, u, rank));
+    ctx->comm = c;
+    ctx->rank = rank;
+    ctx->world = world;
+    return AS_OK;
+  } catch (const Err& e) {
+    ctx->rank = 0;
+    ctx->world = 1;
+    return e.st;
+  }
+}
+
+as_status as_set_shard_axis(as_ctx* ctx, int32_t axis) {
+  if (!ctx) return AS_E_ARG;
+  if (axis < 0 || axis > 2) {
+    set_err(ctx, "as_set_shard_axis: axis must be 0 (auto), 1 (tiles) or 2 (sub-boxes)");
+    return AS_E_ARG;
+  }
+  ctx->shard_axis = axis;
   return AS_OK;
 }
 
@@ -1363,6 +1562,42 @@ as_status as_subbox_count(as_ctx* ctx, int32_t* n_sub) {
 }
 
 namespace {
+// union over the sub-boxes [b, e) on this GPU into device images dlo / dhi (identities for an
+// empty range); the single-GPU body of a render
+void render_local(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int32_t batch, int b, int e,
+                  float* dlo, float* dhi, PhaseTimes* pt, int64_t& pairs) {
+  cudaStream_t s = ctx->stream;
+  const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
+  k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), G.ntiles);
+  LAUNCHED(ctx, 1);
+  if (b >= e) {  // empty union: the identities of min / max (step 22)
+    k_fill2<<<(unsigned)((img + 255) / 256), 256, 0, s>>>(dlo, 1.f, dhi, 0.f, (int64_t)img);
+    LAUNCHED(ctx, 1);
+  }
+  const bool linear = ctx->blend_mode == 1;
+  if (linear) {
+    ensure(ctx, ctx->tmp_lo, sizeof(float) * img);
+    ensure(ctx, ctx->tmp_hi, sizeof(float) * img);
+  }
+  for (int sb = b; sb < e; ++sb) {
+    int64_t M = 0;
+    if (!linear) {
+      render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
+                    nullptr, dlo, dhi, sb == b, M, pt);
+    } else {  // intersection per sub-box, then the union (step 22)
+      float* tl = P<float>(ctx->tmp_lo);
+      float* th = P<float>(ctx->tmp_hi);
+      render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
+                    nullptr, tl, th, true, M, pt);
+      ctx->last_M = M;
+      linear_pass(ctx, bi, G, batch, tl, th);
+      launch_union(tl, th, dlo, dhi, (int64_t)img, sb == b, s);
+      LAUNCHED(ctx, 1);
+    }
+    pairs += M;
+  }
+}
+
 as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int32_t s1,
                        float* lo, float* hi, int32_t flags, as_stats* stats) {
   as_status st = check_ready(ctx);
@@ -1388,12 +1623,23 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
     set_err(ctx, "AS_ASYNC requires device outputs");
     return AS_E_ARG;
   }
+  // multi-GPU axis: 0 none, 1 image tiles (all-gather), 2 sub-boxes (all-reduce min / max)
+  const int world = ctx->world, rank = ctx->rank;
+  int axis = 0;
+  if (ctx->comm && (world > 1 || ctx->shard_axis != 0))
+    axis = ctx->shard_axis != 0 ? ctx->shard_axis : (s1 - s0 >= world ? 2 : 1);
+  if (axis == 1 && ctx->blend_mode != 0) {
+    set_err(ctx, "tile sharding: the linear blend is available on the sub-box axis only");
+    return AS_E_ARG;
+  }
   try {
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
     const Geometry G = geometry(ctx, tile);
     ctx->launches = 0;
     ctx->max_window = 0;
+    ctx->last_gather_ms = 0.0;
+    ctx->last_n_owned = G.ntiles;
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
     const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
@@ -1404,35 +1650,56 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       dlo = P<float>(ctx->img_lo);
       dhi = P<float>(ctx->img_hi);
     }
-    k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), G.ntiles);
-    LAUNCHED(ctx, 1);
     PhaseTimes pt;
     int64_t pairs = 0;
-    if (s0 >= s1) {  // empty union: the identities of min / max (step 22)
-      k_fill2<<<(unsigned)((img + 255) / 256), 256, 0, s>>>(dlo, 1.f, dhi, 0.f, (int64_t)img);
+    int n_done = s1 > s0 ? s1 - s0 : 0;  // sub-boxes rendered by this rank
+    if (axis == 2) {
+      // rank r: contiguous balanced range of [s0, s1); an empty range gives the identities
+      const int ns = s1 - s0, q = ns / world, rm = ns % world;
+      const int b = s0 + rank * q + std::min(rank, rm), e = b + q + (rank < rm ? 1 : 0);
+      n_done = e - b;
+      render_local(ctx, bi, G, batch, b, e, dlo, dhi, stats ? &pt : nullptr, pairs);
+      CK(cudaEventRecord(ctx->ev[3], s));
+      NCK(nccl_api().allReduce(dlo, dlo, img, ncclFloat, ncclMin, (ncclComm_t)ctx->comm, s));
+      NCK(nccl_api().allReduce(dhi, dhi, img, ncclFloat, ncclMax, (ncclComm_t)ctx->comm, s));
+      CK(cudaEventRecord(ctx->ev[4], s));
+    } else if (axis == 1) {
+      // every rank: setup + per-tile costs, the same device LPT owner map, its own tiles
+      // into a compact tile-major buffer, ONE all-gather, the untile on the device
+      const int per = (G.ntiles + world - 1) / world;
+      const int cap = per + std::max(1, per / 4);
+      tile_costs_dev(ctx, bi, G, s0, s1);
+      device_lpt(ctx, G, world, cap);
+      ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
+      k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
+          P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
+          P<int32_t>(ctx->tslot), P<int32_t>(ctx->untile_map));
       LAUNCHED(ctx, 1);
-    }
-    const bool linear = ctx->blend_mode == 1;
-    if (linear) {
-      ensure(ctx, ctx->tmp_lo, sizeof(float) * img);
-      ensure(ctx, ctx->tmp_hi, sizeof(float) * img);
-    }
-    for (int sb = s0; sb < s1; ++sb) {
-      int64_t M = 0;
-      if (!linear) {
-        render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                      nullptr, dlo, dhi, sb == s0, M, stats ? &pt : nullptr);
-      } else {  // intersection per sub-box, then the union (step 22)
-        float* tl = P<float>(ctx->tmp_lo);
-        float* th = P<float>(ctx->tmp_hi);
-        render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                      nullptr, tl, th, true, M, stats ? &pt : nullptr);
-        ctx->last_M = M;
-        linear_pass(ctx, bi, G, batch, tl, th);
-        launch_union(tl, th, dlo, dhi, (int64_t)img, sb == s0, s);
-        LAUNCHED(ctx, 1);
+      const size_t tm = (size_t)cap * tile * tile * 3;
+      ensure(ctx, ctx->gsend, sizeof(float) * 2 * tm);
+      ensure(ctx, ctx->grecv, sizeof(float) * 2 * tm * world);
+      float* slo = P<float>(ctx->gsend);
+      float* shi = slo + tm;
+      // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
+      k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
+      LAUNCHED(ctx, 1);
+      for (int sb = s0; sb < s1; ++sb) {
+        int64_t M = 0;
+        render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
+                      P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0, M,
+                      stats ? &pt : nullptr);
+        pairs += M;
       }
-      pairs += M;
+      CK(cudaEventRecord(ctx->ev[3], s));
+      NCK(nccl_api().allGather(slo, P<float>(ctx->grecv), 2 * tm, ncclFloat,
+                               (ncclComm_t)ctx->comm, s));
+      const float* rl = P<float>(ctx->grecv);
+      launch_untile(rl, rl + tm, P<int32_t>(ctx->untile_map), tile, G.ntx, G.nty, ctx->cam.W,
+                    ctx->cam.H, dlo, dhi, s);
+      LAUNCHED(ctx, 1);
+      CK(cudaEventRecord(ctx->ev[4], s));
+    } else {
+      render_local(ctx, bi, G, batch, s0, s1, dlo, dhi, stats ? &pt : nullptr, pairs);
     }
     if (!(flags & AS_PTR_DEVICE)) {
       CK(cudaMemcpyAsync(lo, dlo, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
@@ -1443,9 +1710,19 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       CK(cudaEventSynchronize(ctx->ev[6]));
       float tot = 0;
       CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+      if (axis != 0) {
+        float g = 0;
+        CK(cudaEventElapsedTime(&g, ctx->ev[3], ctx->ev[4]));
+        ctx->last_gather_ms = g;
+      }
+      if (axis == 1) {
+        int32_t no = 0;
+        CK(cudaMemcpy(&no, P<int32_t>(ctx->nown) + rank, sizeof no, cudaMemcpyDeviceToHost));
+        ctx->last_n_owned = no;
+      }
       BoxInfo br = bi;
-      br.n_sub = s1 > s0 ? s1 - s0 : 0;
-      fill_stats(ctx, br, G, G.ntiles, pairs, pt, tot, stats);
+      br.n_sub = n_done;
+      fill_stats(ctx, br, G, ctx->last_n_owned, pairs, pt, tot, stats);
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;
@@ -1482,9 +1759,14 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
       return AS_E_ARG;
     }
     prepare_common(ctx, bi, G);
-    std::vector<int64_t> c;
-    tile_costs(ctx, bi, G, c);
-    lpt(G.ntiles, c.data(), world, max_tiles, owner);
+    tile_costs_dev(ctx, bi, G, 0, bi.n_sub);
+    device_lpt(ctx, G, world, max_tiles);
+    CK(cudaMemcpyAsync(owner, ctx->owner.p, sizeof(int32_t) * G.ntiles, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    std::vector<unsigned long long> c(G.ntiles);
+    CK(cudaMemcpyAsync(c.data(), ctx->tcost.p, sizeof(unsigned long long) * G.ntiles,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     if (costs) std::copy(c.begin(), c.end(), costs);
     return AS_OK;
   } catch (const Err& e) {
@@ -1520,52 +1802,58 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
     ctx->max_window = 0;
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
-    // ---- owner map (identical on every rank): LPT over per-tile pair counts
-    std::vector<int32_t> own(G.ntiles, 0);
+    // ---- owner map (identical on every rank): LPT over per-tile pair counts, on the device
     if (world > 1) {
-      std::vector<int64_t> c;
-      tile_costs(ctx, bi, G, c);
-      lpt(G.ntiles, c.data(), world, max_tiles, own.data());
-    }
-    std::vector<int32_t> mine;
-    for (int t = 0; t < G.ntiles; ++t)
-      if (own[t] == rank) mine.push_back(t);
-    const int nm = (int)mine.size();
-    CK(cudaMemcpyAsync(ctx->owner.p, own.data(), sizeof(int32_t) * G.ntiles,
-                       cudaMemcpyHostToDevice, s));
-    if (nm > 0)
-      CK(cudaMemcpyAsync(ctx->tlist.p, mine.data(), sizeof(int32_t) * nm, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(ctx->tslot.p, 0xff, sizeof(int32_t) * G.ntiles, s));
-    if (nm > 0) {
-      k_slot_map<<<(nm + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), nm, P<int32_t>(ctx->tslot));
+      tile_costs_dev(ctx, bi, G, 0, bi.n_sub);
+      device_lpt(ctx, G, world, max_tiles);
+    } else {
+      ensure(ctx, ctx->tslot_all, sizeof(int32_t) * G.ntiles);
+      CK(cudaMemsetAsync(ctx->owner.p, 0, sizeof(int32_t) * G.ntiles, s));
+      k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tslot_all), G.ntiles);
       LAUNCHED(ctx, 1);
     }
-    const size_t tm = (size_t)std::max(nm, 1) * tile * tile * 3;
+    k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->owner),
+                                                        P<int32_t>(ctx->tslot_all), G.ntiles,
+                                                        rank, max_tiles, P<int32_t>(ctx->tslot),
+                                                        nullptr);
+    LAUNCHED(ctx, 1);
+    const size_t tmax = (size_t)max_tiles * tile * tile * 3;
     float *dlo = lo_tm, *dhi = hi_tm;
     if (!(flags & AS_PTR_DEVICE)) {
-      ensure(ctx, ctx->img_lo, sizeof(float) * tm);
-      ensure(ctx, ctx->img_hi, sizeof(float) * tm);
+      ensure(ctx, ctx->img_lo, sizeof(float) * tmax);
+      ensure(ctx, ctx->img_hi, sizeof(float) * tmax);
       dlo = P<float>(ctx->img_lo);
       dhi = P<float>(ctx->img_hi);
     }
     PhaseTimes pt;
     int64_t pairs = 0;
-    if (nm > 0) {
-      for (int sb = 0; sb < bi.n_sub; ++sb) {
-        int64_t M = 0;
-        const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0
-        render_subbox(ctx, bi, sb, need_setup, G, batch, P<int32_t>(ctx->owner), rank,
-                      P<int32_t>(ctx->tlist), nm, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0, M,
-                      stats ? &pt : nullptr);
-        pairs += M;
-      }
+    for (int sb = 0; sb < bi.n_sub; ++sb) {
+      int64_t M = 0;
+      const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0
+      render_subbox(ctx, bi, sb, need_setup, G, batch, P<int32_t>(ctx->owner), rank,
+                    P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0, M,
+                    stats ? &pt : nullptr);
+      pairs += M;
     }
+    // the owned tile ids (host output): the owner map comes back once the render is queued
+    std::vector<int32_t> own(G.ntiles);
+    CK(cudaMemcpyAsync(own.data(), ctx->owner.p, sizeof(int32_t) * G.ntiles,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int nm = 0;
+    for (int t = 0; t < G.ntiles; ++t)
+      if (own[t] == rank) {
+        if (nm >= max_tiles) {
+          set_err(ctx, "as_render_shard: more than max_tiles tiles assigned");
+          return AS_E_ARG;
+        }
+        owned[nm++] = t;
+      }
+    *n_owned = nm;
     if (!(flags & AS_PTR_DEVICE) && nm > 0) {
       CK(cudaMemcpyAsync(lo_tm, dlo, sizeof(float) * nm * tile * tile * 3, cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(hi_tm, dhi, sizeof(float) * nm * tile * tile * 3, cudaMemcpyDeviceToHost, s));
     }
-    for (int k = 0; k < nm; ++k) owned[k] = mine[k];
-    *n_owned = nm;
     if (stats) {
       CK(cudaEventRecord(ctx->ev[6], s));
       CK(cudaEventSynchronize(ctx->ev[6]));

@@ -29,6 +29,10 @@
 
 #include "internal.cuh"
 
+#ifndef KT2_MINB  // k_tile2 CTAs per SM (launch bounds; the batch size is clamped to match)
+#define KT2_MINB 4
+#endif
+
 namespace absplat {
 
 namespace {
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ float2 ring_prod2(const float2* rf, unsigned long lon
 }
 
 template <int NV>
-__global__ void __launch_bounds__(T2, 4) k_tile2(TileArgs A) {
+__global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
   __shared__ unsigned s_skip[8];
@@ -1739,8 +1743,8 @@ static size_t smem_for(int ts, int bs) {
 // ring covers a batch plus the 128 positions before it)
 int tile_batch(int nv, int ts, int bs) {
   bs = std::min(bs, 128);
-  if (tile_kernel_version(ts) == 2) {  // k_tile2: keep four CTAs per SM (registers allow four)
-    while (bs > 1 && tile_smem_bytes(nv, ts, bs) > 54 * 1024) --bs;
+  if (tile_kernel_version(ts) == 2) {  // k_tile2: as many CTAs per SM as the registers allow
+    while (bs > 1 && tile_smem_bytes(nv, ts, bs) > (size_t)(220 / KT2_MINB - 1) * 1024) --bs;
     return bs;
   }
   while (bs > 1 && tile_smem_bytes(nv, ts, bs) > 96 * 1024) bs >>= 1;

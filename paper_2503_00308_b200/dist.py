@@ -1,6 +1,15 @@
 """Sharding over GPUs (north_star (3)), one process per GPU, the scene
 replicated on every rank.
 
+* In the library (the product path): `init_comm` hands rank 0's NCCL unique id to every
+  rank (torch.distributed is only the out-of-band channel for those 128 bytes) and joins the
+  context's communicator (as_comm_init); from then on as_render_bounds shards the image
+  tiles (or the sub-boxes) over the ranks and runs the one collective itself, on the
+  context's stream, leaving the full bound images on every rank.
+* The Python-side drivers below (ShardedRenderer / SubboxShardedRenderer) run the same
+  decomposition with torch.distributed collectives on the library's per-rank outputs; they
+  serve the gloo CPU tests and bench's --emulate-world timing.
+
 * Tiles (ShardedRenderer): image tiles assigned by the library's deterministic LPT owner map,
   each rank rendering only its tiles into a compact tile-major buffer, then ONE all-gather of
   the bound tiles (NCCL over NVLink / NVSwitch) and an untile on the root.
@@ -17,6 +26,25 @@ from __future__ import annotations
 import numpy as np
 
 from .api import Context, as_untile
+
+
+def share_bytes(payload, rank: int, group=None, src: int = 0) -> bytes:
+    """Broadcast `payload` (bytes, meaningful on rank `src`) to every rank of the default
+    torch.distributed group (or `group`); returns the bytes on every rank."""
+    import torch.distributed as dist
+    obj = [payload if rank == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return bytes(obj[0])
+
+
+def init_comm(ctx: Context, rank: int, world: int, group=None, axis: int = 0):
+    """Join the library communicator of `ctx` (rank `rank` of `world`); axis as
+    Context.as_set_shard_axis.  Collective over the torch.distributed group."""
+    from .api import as_nccl_id
+    uid = share_bytes(as_nccl_id() if rank == 0 else None, rank, group)
+    ctx.as_comm_init(rank, world, uid)
+    ctx.as_set_shard_axis(axis)
+    return ctx
 
 
 class ShardedRenderer:

@@ -158,3 +158,31 @@ def test_subbox_sharded_gloo(world):
     res = sorted(q.get(timeout=5) for _ in range(world))
     assert sum(r[1] for r in res) == 8
     assert all(r[2] and r[3] for r in res)
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_00308_b200.dist import share_bytes
+        payload = bytes(range(128)) if rank == 0 else None
+        got = share_bytes(payload, rank)
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_id_distribution_gloo():
+    """dist.init_comm's out-of-band step: rank 0's 128-byte NCCL id reaches every rank
+    unchanged (world 2, gloo; the NCCL communicator itself needs GPUs)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0] == res[1] == bytes(range(128))
