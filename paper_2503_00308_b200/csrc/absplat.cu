@@ -84,6 +84,8 @@ struct as_ctx {
   int shard_axis = 0;    // as_set_shard_axis: 0 auto, 1 tiles, 2 sub-boxes
   DevBuf gsend, grecv, lptkey, lptkey2, lptid, lptid2, tslot_all, nown;
   double last_gather_ms = 0.0;
+  int64_t last_nexc = 0;
+  int last_out_tiles = 0;  // tile-major output capacity (checked build bounds)
   int last_n_owned = 0;
   bool last_has_exc = false;
   int64_t last_M = 0;
@@ -531,6 +533,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       // explicit lists only for positions with a partner more than 128 positions away
       cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
       const int64_t nexc = read_i64(ctx, P<int64_t>(ctx->eoff) + M);
+      ctx->last_nexc = nexc;
       pa.off = P<int64_t>(ctx->eoff);
       ensure(ctx, ctx->exc, sizeof(int32_t) * std::max<int64_t>(nexc, 1));
       pa.exc = P<int32_t>(ctx->exc);
@@ -665,6 +668,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.active = ctr + C_ACTIVE;
   ta.dbg = ctx->debug ? P<unsigned long long>(ctx->dbg) : nullptr;
   ta.kver = tile_kernel_version(G.ts);
+  ta.M = M;
+  ta.nexc = has_exc ? ctx->last_nexc : 0;
+  ta.n_partial = (int64_t)(8 * npix * n_items);
+  ta.n_out = tslot ? (int64_t)ctx->last_out_tiles * G.ts * G.ts * 3 : (int64_t)ctx->cam.W * ctx->cam.H * 3;
   ctx->last_items = (int)n_items;
   ctx->last_grid = grid;
   ctx->last_R = R;
@@ -1683,6 +1690,7 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
       k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
       LAUNCHED(ctx, 1);
+      ctx->last_out_tiles = cap;
       for (int sb = s0; sb < s1; ++sb) {
         int64_t M = 0;
         render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
@@ -1827,6 +1835,7 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
     }
     PhaseTimes pt;
     int64_t pairs = 0;
+    ctx->last_out_tiles = max_tiles;
     for (int sb = 0; sb < bi.n_sub; ++sb) {
       int64_t M = 0;
       const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0

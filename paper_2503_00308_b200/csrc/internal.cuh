@@ -9,6 +9,7 @@
 // loop runs in fp32 on tile-centred forms (H2).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/absplat.h"
@@ -16,6 +17,25 @@
 namespace absplat {
 
 constexpr int NVMAX = AS_MAX_VARS;
+
+// Device-side invariant checks of the checked build (-DABSPLAT_CHECKS, libabsplat_checked.so):
+// index bounds of every gathered / ring / list access in the tile kernels, trapping on the
+// first violation.  compute-sanitizer is closed on this GPU pool; the parity suite runs
+// against the checked build instead (tools/checked_build.sh).
+#ifdef ABSPLAT_CHECKS
+#define DCHECK(cond)                                                                     \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define DCHECK(cond) \
+  do {               \
+  } while (0)
+#endif
 constexpr double TAU = 1e-12;   // per-pixel cull threshold on a (G12)
 constexpr double DMIN = 0.01;   // near plane (G8)
 constexpr int KTAYLOR = 8;      // MatrixInv order
@@ -347,6 +367,10 @@ struct TileArgs {
   unsigned long long* active; // active pair counter
   unsigned long long* dbg;    // [DBG_N] rare-path counters (as_debug_counters) or nullptr
   int kver;                   // tile kernel version (tile_kernel_version): partial layout
+  int64_t M;                  // pairs (positions) of the sub-box: bound of the per-position arrays
+  int64_t nexc;               // entries of exc[]
+  int64_t n_partial;          // floats of partial[]
+  int64_t n_out;              // floats of lo / hi (row-major image or tile-major slots)
 };
 // rare-path counters of the tile kernel (as_debug_counters): evidence that every slow path
 // of the exception machinery runs in some parity case

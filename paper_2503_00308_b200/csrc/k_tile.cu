@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
     const int4 it2 = A.items2[islot];
     const int scan0 = it2.x, scan1 = it2.y, anext = it2.z;  // scan [A, L), record at A_next
     const int rmask = (1 << ((iflags >> 8) & 0xff)) - 1;     // per-item ring length - 1
+    DCHECK(islot >= 0 && islot < A.n_items && tile >= 0 && tile < A.ntiles);
+    DCHECK(0 <= scan0 && scan0 <= pbeg && pbeg <= pend && pend <= scan1 && rmask < A.R);
+    DCHECK(A.tbegin[tile] + scan1 <= A.tend[tile]);
     const int tx = tile % A.ntx, ty = tile / A.ntx;
     const int ox = tx * ts + (sub % nsbx) * SBX, oy = ty * ts + (sub / nsbx) * SBY;  // origin
     const int64_t tb = A.tbegin[tile];
@@ -650,6 +653,8 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         // (a_hi = 0 on this pixel: its upper contribution is exactly 0, no T_hi needed)
         if (main && (pmf & PM_EF) && !(flags & F_SKIP) && ahi > 0.f) {
           const int wlen = qpos - R.ph;
+          DCHECK(wlen > 0 && wlen <= rmask && R.ph >= scan0);
+          DCHECK(!(pmf & PM_OVF) || (R.peoff >= 0 && R.peoff + R.pnF <= A.nexc));
           if (!(pmf & PM_OVF)) {
             bool done = false;
             if (R.tmode == 1) {  // dense: T_hi before h times the kept factors
@@ -711,6 +716,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
           if (f < FB) {
             const FinS& F = fins[f];
             if (F.qq < 0) continue;  // another chunk's position, or culled in this block
+            DCHECK(qpos - F.qq > 0 && qpos - F.qq <= rmask && F.qq >= scan0);
             clo = F.clo;
             tl = rf[RS<SBP>(F.qq, 3, rmask)];
             if (tl == 0.f) continue;  // q' missed this pixel (a_lo = 0): the term is exactly 0
@@ -1120,6 +1126,9 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
     const int4 it2 = A.items2[islot];
     const int scan0 = it2.x, scan1 = it2.y, anext = it2.z;
     const int rmask = (1 << ((iflags >> 8) & 0xff)) - 1;
+    DCHECK(islot >= 0 && islot < A.n_items && tile >= 0 && tile < A.ntiles);
+    DCHECK(0 <= scan0 && scan0 <= pbeg && pbeg <= pend && pend <= scan1);
+    DCHECK(A.tbegin[tile] + scan1 <= A.tend[tile] && rmask < A.R);
     const int tx = tile % A.ntx, ty = tile / A.ntx;
     const int ox = tx * ts + (sub % nsbx) * B2, oy = ty * ts + (sub / nsbx) * B2;
     const int64_t tb = A.tbegin[tile];
@@ -1164,6 +1173,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
       //      staging (NPART threads per Gaussian), as in k_tile
       for (int j = T2 - 1 - tid; j < nb; j += T2) {
         const int64_t gp = tb + b0 + j;
+        DCHECK(gp >= 0 && gp < A.M);
         const HotRec<NV>* H = raw + j;
         SRec2<NV>& S = srec[j];
         const double mxl = H->mu[0], myl = H->mu[1], mxh = H->mu[2], myh = H->mu[3];
@@ -1346,6 +1356,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         active += main ? (unsigned)kA + (unsigned)kB : 0u;
         if (pmf & PM_STORE) {
           const int rs = RS2(qpos, 0, rmask);
+          DCHECK(rf != nullptr);
           if (pmf & PM_HSTART) rf[rs] = Tb;
           rf[rs + T2] = f2(1.f - alo.x, 1.f - alo.y);
           if (pmf & PM_EF) rf[rs + 2 * T2] = f2(1.f - ahi.x, 1.f - ahi.y);
@@ -1354,6 +1365,8 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         float2 tbv = Tb;
         if (main && (pmf & PM_EF) && !(flags & F_SKIP) && (ahi.x > 0.f || ahi.y > 0.f)) {
           const int wlen = qpos - R.ph;
+          DCHECK(wlen > 0 && wlen <= rmask && R.ph >= scan0);
+          DCHECK(!(pmf & PM_OVF) || (R.peoff >= 0 && R.peoff + R.pnF <= A.nexc));
           if (!(pmf & PM_OVF)) {
             bool done = false;
             if (R.tmode == 1) {
@@ -1413,6 +1426,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
           if (f < FB) {
             const FinS& F = fins[f];
             if (F.qq < 0) continue;
+            DCHECK(qpos - F.qq > 0 && qpos - F.qq <= rmask && F.qq >= scan0);
             clo = F.clo;
             tl = rf[RS2(F.qq, 3, rmask)];
             if (tl.x == 0.f && tl.y == 0.f) continue;
@@ -1434,6 +1448,8 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
             const FinRec& fr = A.fin_rec[F0 + f];
             if (fr.qq < pbeg || fr.qq >= pend) continue;
             if (A.dbg) atomicAdd(A.dbg + DBG_FIN_UNSTAGED, 1ull);
+            DCHECK(qpos - fr.qq > 0 && qpos - fr.qq <= rmask && fr.qq >= scan0);
+            DCHECK(!(fr.flags & PM_OVF) || fr.eoff + fr.nF + fr.nG <= A.nexc);
             clo = fr.clo;
             tl = rf[RS2(fr.qq, 3, rmask)];
             if (tl.x == 0.f && tl.y == 0.f) continue;
@@ -1464,6 +1480,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
           o = ((int64_t)py * A.W + px) * 3;
         }
         if (o >= 0) {
+          DCHECK(o + 3 <= A.n_out);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             float l = fminf(fmaxf(lc[c] - A.ntau, 0.f), 1.f);
@@ -1481,6 +1498,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
       } else {
         const float2 rb = rec ? recb : Tb, rl = rec ? recl : Tl;
         const int pix = (ly + 4 * e) * B2 + lx;
+        DCHECK((int64_t)(((size_t)islot * nsub + sub) * P2 + pix) * 8 + 8 <= A.n_partial);
         float4* dst = reinterpret_cast<float4*>(A.partial + (((size_t)islot * nsub + sub) * P2 + pix) * 8);
         dst[0] = make_float4(hc[0], hc[1], hc[2], e ? rb.y : rb.x);
         dst[1] = make_float4(lc[0], lc[1], lc[2], e ? rl.y : rl.x);
@@ -1679,6 +1697,8 @@ __global__ void k_merge(TileArgs A) {
     float Pb = 1.f, Pl = 1.f, h[3] = {0.f, 0.f, 0.f}, l[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < n; ++k) {
       const int64_t it = A.item_off[tile] + k;
+      DCHECK(it >= 0 && it < A.n_items &&
+             (int64_t)(((size_t)it * nsub + sub) * SBP + pix) * 8 + 8 <= A.n_partial);
       const float4* src =
           reinterpret_cast<const float4*>(A.partial + (((size_t)it * nsub + sub) * SBP + pix) * 8);
       const float4 a = src[0], b = src[1];

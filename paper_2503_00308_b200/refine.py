@@ -101,3 +101,84 @@ def refine_fails(ctx, pose_box: dict, scene_box, max_subboxes: int = 64,
         parts = np.asarray(new)
     ctx.as_set_subboxes(parts)
     return parts, history
+
+
+def bisect_widest(box: np.ndarray, full: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Split a sub-box [9, 2] in half along its widest axis relative to the full box (lowest
+    axis on ties), any axis: the width-driven rule (every perturbed axis widens the bound)."""
+    rel = np.full(9, -1.0)
+    for a in range(9):
+        fw = full[a, 1] - full[a, 0]
+        if fw > 0:
+            rel[a] = (box[a, 1] - box[a, 0]) / fw
+    a = int(np.argmax(rel))
+    mid = 0.5 * (box[a, 0] + box[a, 1])
+    lo, hi = box.copy(), box.copy()
+    lo[a, 1] = mid
+    hi[a, 0] = mid
+    return lo, hi
+
+
+def _mpg(lo, hi) -> float:
+    """Mean Pixel Gap of bound images (torch or numpy [H, W, 3])."""
+    if hasattr(lo, "cpu"):
+        import torch
+        return float(torch.linalg.vector_norm(hi - lo, dim=-1).mean())
+    return float(np.linalg.norm(np.asarray(hi) - np.asarray(lo), axis=-1).mean())
+
+
+def _union(images):
+    lo = images[0][0]
+    hi = images[0][1]
+    if hasattr(lo, "cpu"):
+        import torch
+        for l, h in images[1:]:
+            lo = torch.minimum(lo, l)
+            hi = torch.maximum(hi, h)
+        return lo, hi
+    for l, h in images[1:]:
+        lo = np.minimum(lo, l)
+        hi = np.maximum(hi, h)
+    return lo, hi
+
+
+def refine_width(ctx, pose_box: dict, scene_box, tile: int = 16, batch: int = 64,
+                 max_subboxes: int = 16):
+    """Width-driven refinement ("split sub-boxes where ... width is
+    large"; partitions are the paper's main tightness lever): starting from the
+    box's uniform partition, repeatedly bisect the sub-box whose own bound image has the largest
+    Mean Pixel Gap, along its widest relative axis, until `max_subboxes`.  Each sub-box is
+    rendered once (its two halves when it is split) through as_set_subboxes +
+    as_render_subboxes(s, s + 1); the union (step 22) is the elementwise min / max of the kept
+    images.
+
+    Returns (partition [P, 9, 2] installed in ctx, history): history[i] = (number of
+    sub-boxes, MPG of the union, sum of the sub-box render times in ms)."""
+    full = box_bounds(pose_box, scene_box)
+    parts = [b for b in uniform_partition(pose_box, scene_box)]
+    imgs, mpgs, ms = [], [], []
+
+    def render_one(box):
+        ctx.as_set_subboxes(np.asarray([box]))
+        lo, hi, st = ctx.as_render_subboxes(0, 1, tile, batch)
+        return lo, hi, _mpg(lo, hi), (st["ms_total"] if st else 0.0)
+
+    for b in parts:
+        lo, hi, m, t = render_one(b)
+        imgs.append((lo, hi))
+        mpgs.append(m)
+        ms.append(t)
+    history = [(len(parts), _mpg(*_union(imgs)), float(sum(ms)))]
+    while len(parts) < max_subboxes:
+        i = int(np.argmax(mpgs))
+        a, b = bisect_widest(parts[i], full)
+        la, ha, ma, ta = render_one(a)
+        lb, hb, mb, tb = render_one(b)
+        parts[i:i + 1] = [a, b]
+        imgs[i:i + 1] = [(la, ha), (lb, hb)]
+        mpgs[i:i + 1] = [ma, mb]
+        ms[i:i + 1] = [ta, tb]
+        history.append((len(parts), _mpg(*_union(imgs)), float(sum(ms))))
+    out = np.asarray(parts)
+    ctx.as_set_subboxes(out)
+    return out, history

@@ -90,3 +90,15 @@ def test_host_untile_roundtrip(W, H, tile, world):
     bad[0, 0] = bad[world - 1, 0]  # a tile owned twice / one missing
     with pytest.raises(ap.AbsplatError):
         ap.as_untile(W, H, tile, world, cap, bad, n_owned, tm_lo, tm_hi)
+
+
+def test_checked_build_is_the_same_abi():
+    """The checked build (device bounds checks, tools/checked_run.sh) exports the same ABI."""
+    from paper_2503_00308_b200 import build as b
+    lib = b.LIB_CHECKED
+    if not os.path.exists(lib):
+        pytest.skip("checked build not present")
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert set(_abi.declared_functions()) <= exported
