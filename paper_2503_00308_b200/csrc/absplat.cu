@@ -828,15 +828,29 @@ void lpt(int n, const int64_t* costs, int world, int cap, int32_t* owner) {
 // rank with room (ties: lower rank).  One warp: lane r holds ranks r, r + 32; the argmin is
 // a warp min over (load << 7 | rank).  Then the ranks' slots in ascending tile id
 // (__match_any over each 32-tile chunk) and the per-rank counts.
-__global__ void k_lpt(const int32_t* ids, const unsigned long long* nkeys, int n, int world,
-                      int cap, int32_t* owner, int32_t* slot, int32_t* nown) {
+constexpr int LPT_CHUNK = 2048;  // sorted (cost, id) entries staged in shared memory at a time
+__global__ void __launch_bounds__(256) k_lpt(const int32_t* ids, const unsigned long long* nkeys,
+                                             int n, int world, int cap, int32_t* owner,
+                                             int32_t* slot, int32_t* nown) {
   __shared__ int sbase[128];
-  const int lane = threadIdx.x;
+  __shared__ unsigned long long skey[LPT_CHUNK];
+  __shared__ int sid[LPT_CHUNK];
+  const int lane = threadIdx.x & 31;
+  const bool w0 = threadIdx.x < 32;
   unsigned long long load[4] = {0, 0, 0, 0};
   int cnt[4] = {0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) {
-    const unsigned long long cost = ~nkeys[i];
-    const int t = ids[i];
+  for (int c0 = 0; c0 < n; c0 += LPT_CHUNK) {
+    const int m = min(LPT_CHUNK, n - c0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {  // coalesced staging by the block
+      skey[k] = nkeys[c0 + k];
+      sid[k] = ids[c0 + k];
+    }
+    __syncthreads();
+    if (!w0) continue;
+  for (int i = 0; i < m; ++i) {
+    const unsigned long long cost = ~skey[i];
+    const int t = sid[i];
     unsigned long long best = ~0ull;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -854,6 +868,9 @@ __global__ void k_lpt(const int32_t* ids, const unsigned long long* nkeys, int n
       }
     if (lane == 0) owner[t] = r;
   }
+  }
+  __syncthreads();
+  if (!w0) return;
   for (int r = lane; r < 128; r += 32) sbase[r] = 0;
   __syncwarp();
   for (int c0 = 0; c0 < n; c0 += 32) {
@@ -939,7 +956,7 @@ void device_lpt(as_ctx* ctx, const Geometry& G, int world, int cap) {
   LAUNCHED(ctx, 1);
   cub_sort_keys64(ctx, P<unsigned long long>(ctx->lptkey), P<unsigned long long>(ctx->lptkey2),
                   P<int32_t>(ctx->lptid), P<int32_t>(ctx->lptid2), n, 64);
-  k_lpt<<<1, 32, 0, st>>>(P<int32_t>(ctx->lptid2), P<unsigned long long>(ctx->lptkey2), n, world,
+  k_lpt<<<1, 256, 0, st>>>(P<int32_t>(ctx->lptid2), P<unsigned long long>(ctx->lptkey2), n, world,
                           cap, P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all),
                           P<int32_t>(ctx->nown));
   LAUNCHED(ctx, 1);

@@ -73,6 +73,7 @@ struct PoseDev {
   double t[3][NVMAX + 1];  // exact affine
   double g[3][NVMAX + 1];  // exact affine
   double gslope[NVMAX];
+  double Rcl[9];  // concretised lower bound of each R form (uniform over the Gaussians)
   int n;
 };
 

@@ -100,6 +100,11 @@ __global__ void k_pose(BoxParams bp, PoseDev* out) {
           P.Ru[3 * a + b][i] = sl;
         }
     }
+  for (int e = 0; e < 9; ++e) {
+    double v = P.Rl[e][NVMAX];
+    for (int i = 0; i < n; ++i) v -= fabs(P.Rl[e][i]);
+    P.Rcl[e] = v;
+  }
   // translation: t0 + Mf * offset, Mf = I or R_c2w(nominal Euler) (reading O10)
   double Mf[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   if (bp.t_frame == 1) rc2w(bp.euler0, -1, Mf);
@@ -197,6 +202,21 @@ struct Lane {
     acc.u += yh * ((yh >= 0) ? x.u : x.l) + xl * ((xl >= 0) ? y.u : y.l);
     add_const(acc, -(xl * yl), -(xl * yh));
   }
+  // the same with the operands' concretised bounds given (each form is concretised once and
+  // reused by every product it enters: the shuffle reductions dominate this kernel)
+  __device__ __forceinline__ void mul_acc_b(HL& acc, const HL& x, double xl, const HL& y, double yl,
+                                            double yh) const {
+    acc.l += yl * ((yl >= 0) ? x.l : x.u) + xl * ((xl >= 0) ? y.l : y.u);
+    acc.u += yh * ((yh >= 0) ? x.u : x.l) + xl * ((xl >= 0) ? y.u : y.l);
+    add_const(acc, -(xl * yl), -(xl * yh));
+  }
+  __device__ __forceinline__ void sq_acc_b(HL& acc, const HL& x, double xl, double xh) const {
+    const double p = fmin(fmax(0.0, xl), xh);
+    const double tp = 2.0 * p, sh = xl + xh;
+    acc.l += tp * ((tp >= 0) ? x.l : x.u);
+    acc.u += sh * ((sh >= 0) ? x.u : x.l);
+    add_const(acc, -(p * p), -(xl * xh));
+  }
   // acc += x*x: tangent at p = clamp(0, x_lo, x_hi), chord (G2)
   __device__ __forceinline__ void sq_acc(HL& acc, const HL& x) const {
     double xl, xh;
@@ -249,12 +269,17 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
     }
     v[b] = HL{c, c};
   }
+  double vl[3], vh[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) L.conc(v[b], vl[b], vh[b]);
+  const double* Rlo = sp.Rcl;  // the R forms' lower bounds, from k_pose
   HL uc[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     HL acc{0.0, 0.0};
 #pragma unroll
-    for (int b = 0; b < 3; ++b) L.mul_acc(acc, pose_R(3 * a + b), v[b]);
+    for (int b = 0; b < 3; ++b)
+      L.mul_acc_b(acc, pose_R(3 * a + b), Rlo[3 * a + b], v[b], vl[b], vh[b]);
     uc[a] = acc;
   }
   // ---- l.4 J, l.5 up = K uc, l.7 d = uc_2
@@ -268,32 +293,42 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
   // ---- l.3 Mc = Mmul(R, Mw) (exact, Mw constant), l.6 Mp = Mmul(J, Mc)
   const float* ch = A.chol + 6 * i;
   const double Mw[9] = {ch[0], 0.0, 0.0, ch[1], ch[2], 0.0, ch[3], ch[4], ch[5]};
+  double j00l, j02l, j11l, j12l, tmp;
+  L.conc(J00, j00l, tmp);
+  L.conc(J02, j02l, tmp);
+  L.conc(J11, j11l, tmp);
+  L.conc(J12, j12l, tmp);
   HL Mp[2][3];
+  double Mpl[2][3], Mph[2][3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     HL Mc[3];
+    double mcl[3], mch[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       HL acc{0.0, 0.0};
 #pragma unroll
       for (int b = 0; b < 3; ++b) L.axpy(acc, pose_R(3 * a + b), Mw[3 * b + c]);
       Mc[a] = acc;
+      L.conc(acc, mcl[a], mch[a]);
     }
     HL m0{0.0, 0.0}, m1{0.0, 0.0};
-    L.mul_acc(m0, J00, Mc[0]);
-    L.mul_acc(m0, J02, Mc[2]);
-    L.mul_acc(m1, J11, Mc[1]);
-    L.mul_acc(m1, J12, Mc[2]);
+    L.mul_acc_b(m0, J00, j00l, Mc[0], mcl[0], mch[0]);
+    L.mul_acc_b(m0, J02, j02l, Mc[2], mcl[2], mch[2]);
+    L.mul_acc_b(m1, J11, j11l, Mc[1], mcl[1], mch[1]);
+    L.mul_acc_b(m1, J12, j12l, Mc[2], mcl[2], mch[2]);
     Mp[0][c] = m0;
     Mp[1][c] = m1;
+    L.conc(m0, Mpl[0][c], Mph[0][c]);
+    L.conc(m1, Mpl[1][c], Mph[1][c]);
   }
   // ---- l.8 X = Mmul(Mp, Mp^T) (X01 once, mirrored: G5)
   HL X00{0.0, 0.0}, X01{0.0, 0.0}, X11{0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    L.sq_acc(X00, Mp[0][c]);
-    L.sq_acc(X11, Mp[1][c]);
-    L.mul_acc(X01, Mp[0][c], Mp[1][c]);
+    L.sq_acc_b(X00, Mp[0][c], Mpl[0][c], Mph[0][c]);
+    L.sq_acc_b(X11, Mp[1][c], Mpl[1][c], Mph[1][c]);
+    L.mul_acc_b(X01, Mp[0][c], Mpl[0][c], Mp[1][c], Mpl[1][c], Mph[1][c]);
   }
   // ---- l.8 Conic = MatrixInv(X; X0, k) (Alg. 4)
   bool ok = true;
@@ -318,12 +353,11 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
       if (a == b) L.add_const(e, 1.0, 1.0);
       E[2 * a + b] = e;
     }
-  double ss = 0.0;
+  double ss = 0.0, Elo[4], Ehi[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    double lo, hi;
-    L.conc(E[e], lo, hi);
-    const double m = fmax(fabs(lo), fabs(hi));
+    L.conc(E[e], Elo[e], Ehi[e]);
+    const double m = fmax(fabs(Elo[e]), fabs(Ehi[e]));
     ss += m * m;
   }
   const double rho = sqrt(ss);
@@ -357,7 +391,16 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
   const bool bwd = A.inv_backward != 0;
   if (bwd) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) L.conc(E[e], Bl[1][e], Bh[1][e]);
+    for (int e = 0; e < 4; ++e) {
+      Bl[1][e] = Elo[e];
+      Bh[1][e] = Ehi[e];
+    }
+  }
+  double Plo[4], Phi[4];  // concretised P^{it-1} (level 1: E)
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    Plo[e] = Elo[e];
+    Phi[e] = Ehi[e];
   }
 #pragma unroll 1
   for (int it = 2; it <= k_warp; ++it) {
@@ -366,16 +409,16 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
     for (int a = 0; a < 2; ++a) {
       HL q0{0.0, 0.0}, q1{0.0, 0.0};  // row a of P^it = P^{it-1} E (O5)
       if (it == 2 && a == 0) {
-        L.sq_acc(q0, P[0]);
+        L.sq_acc_b(q0, P[0], Plo[0], Phi[0]);
       } else {
-        L.mul_acc(q0, P[2 * a + 0], E[0]);
+        L.mul_acc_b(q0, P[2 * a + 0], Plo[2 * a + 0], E[0], Elo[0], Ehi[0]);
       }
-      L.mul_acc(q0, P[2 * a + 1], E[2]);
-      L.mul_acc(q1, P[2 * a + 0], E[1]);
+      L.mul_acc_b(q0, P[2 * a + 1], Plo[2 * a + 1], E[2], Elo[2], Ehi[2]);
+      L.mul_acc_b(q1, P[2 * a + 0], Plo[2 * a + 0], E[1], Elo[1], Ehi[1]);
       if (it == 2 && a == 1) {
-        L.sq_acc(q1, P[3]);
+        L.sq_acc_b(q1, P[3], Plo[3], Phi[3]);
       } else {
-        L.mul_acc(q1, P[2 * a + 1], E[3]);
+        L.mul_acc_b(q1, P[2 * a + 1], Plo[2 * a + 1], E[3], Elo[3], Ehi[3]);
       }
       P[2 * a + 0] = q0;
       P[2 * a + 1] = q1;
@@ -386,15 +429,12 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
         S[2 * a + 1].u += q1.u;
       }
     }
-    if (bwd) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        double lo, hi;
-        L.conc(P[e], lo, hi);
-        if (it < KB) {
-          Bl[it][e] = lo;
-          Bh[it][e] = hi;
-        }
+    for (int e = 0; e < 4; ++e) {
+      L.conc(P[e], Plo[e], Phi[e]);
+      if (bwd && it < KB) {
+        Bl[it][e] = Plo[e];
+        Bh[it][e] = Phi[e];
       }
     }
   }
@@ -506,13 +546,19 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
   HotRec<NV>* H = reinterpret_cast<HotRec<NV>*>(A.hot) + i;
   float wv[6][2];
   float wcv[6][2];
+  double cnl[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double h;
+    L.conc(conic[e], cnl[e], h);
+  }
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       HL acc{0.0, 0.0};
-      L.mul_acc(acc, conic[2 * a + 0], Mp[0][c]);
-      L.mul_acc(acc, conic[2 * a + 1], Mp[1][c]);
+      L.mul_acc_b(acc, conic[2 * a + 0], cnl[2 * a + 0], Mp[0][c], Mpl[0][c], Mph[0][c]);
+      L.mul_acc_b(acc, conic[2 * a + 1], cnl[2 * a + 1], Mp[1][c], Mpl[1][c], Mph[1][c]);
       double lo, hi;
       L.conc(acc, lo, hi);
       if (!(fabs(lo) <= WCAP && fabs(hi) <= WCAP)) ok = false;  // reading O3
@@ -521,15 +567,15 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
       wcv[3 * a + c][0] = (float)lo;
       wcv[3 * a + c][1] = (float)hi;
     }
-  HL D2{0.0, 0.0}, DU0{0.0, 0.0}, DU1{0.0, 0.0};
-  L.sq_acc(D2, d);
-  L.mul_acc(DU0, d, up0);
-  L.mul_acc(DU1, d, up1);
-  // ---- depth decisions, key, footprint (steps 10-12; G8, G12, O4)
   double dl, dh, u0l, u0h, u1l, u1h;
   L.conc(d, dl, dh);
   L.conc(up0, u0l, u0h);
   L.conc(up1, u1l, u1h);
+  HL D2{0.0, 0.0}, DU0{0.0, 0.0}, DU1{0.0, 0.0};
+  L.sq_acc_b(D2, d, dl, dh);
+  L.mul_acc_b(DU0, d, dl, up0, u0l, u0h);
+  L.mul_acc_b(DU1, d, dl, up1, u1l, u1h);
+  // ---- depth decisions, key, footprint (steps 10-12; G8, G12, O4)
   const double dcl = __shfl_sync(FULL, d.l, NV, W), dcu = __shfl_sync(FULL, d.u, NV, W);
   double s1 = L.slope() ? fabs(d.l - sp.gslope[k]) : 0.0;
   double s2 = L.slope() ? fabs(d.u - sp.gslope[k]) : 0.0;
