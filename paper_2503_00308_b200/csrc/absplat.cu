@@ -82,7 +82,7 @@ struct as_ctx {
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
   int shard_axis = 0;    // as_set_shard_axis: 0 auto, 1 tiles, 2 sub-boxes
-  DevBuf gsend, grecv, lptkey, lptkey2, lptid, lptid2, tslot_all, nown;
+  DevBuf gsend, grecv, lptkey, lptkey2, lptid, lptid2, tslot_all, nown, chunk_stats;
   double last_gather_ms = 0.0;
   int64_t last_nexc = 0;
   int last_out_tiles = 0;  // tile-major output capacity (checked build bounds)
@@ -629,10 +629,12 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ensure(ctx, ctx->item_order, sizeof(int32_t) * n_items);
   ensure(ctx, ctx->item_cnt, sizeof(int32_t) * G.ntiles);
   ensure(ctx, ctx->partial, sizeof(float) * 8 * npix * n_items);
+  ensure(ctx, ctx->chunk_stats, sizeof(int4) * n_items);
   launch_chunks(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), has_exc ? P<int4>(ctx->pflag) : nullptr,
-                P<int64_t>(ctx->item_off), G.ntiles, target, owner, rank, P<int4>(ctx->items),
-                P<int4>(ctx->items2), P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
-  LAUNCHED(ctx, 1);
+                P<int64_t>(ctx->item_off), G.ntiles, n_items, target, owner, rank,
+                P<int4>(ctx->chunk_stats), P<int4>(ctx->items), P<int4>(ctx->items2),
+                P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
+  LAUNCHED(ctx, 2);
   k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
   LAUNCHED(ctx, 1);
   cub_sort_keys32(ctx, P<uint32_t>(ctx->item_key), P<uint32_t>(ctx->item_key2),
@@ -851,15 +853,23 @@ __global__ void __launch_bounds__(256) k_lpt(const int32_t* ids, const unsigned 
   for (int i = 0; i < m; ++i) {
     const unsigned long long cost = ~skey[i];
     const int t = sid[i];
-    unsigned long long best = ~0ull;
+    int r;
+    if (world <= 32 && __all_sync(0xffffffffu, load[0] < 0x80000000ull)) {
+      // one rank per lane, loads below 2^31: a warp min (REDUX) and the lowest lane holding it
+      const unsigned v = (lane < world && cnt[0] < cap) ? (unsigned)load[0] : 0xffffffffu;
+      const unsigned mn = __reduce_min_sync(0xffffffffu, v);
+      r = __ffs(__ballot_sync(0xffffffffu, v == mn)) - 1;
+    } else {
+      unsigned long long best = ~0ull;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = lane + 32 * q;
-      if (r < world && cnt[q] < cap) best = min(best, (load[q] << 7) | (unsigned long long)r);
+      for (int q = 0; q < 4; ++q) {
+        const int rr = lane + 32 * q;
+        if (rr < world && cnt[q] < cap) best = min(best, (load[q] << 7) | (unsigned long long)rr);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      r = (int)(best & 127ull);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-    const int r = (int)(best & 127ull);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (lane + 32 * q == r) {
@@ -1068,7 +1078,8 @@ as_status as_destroy(as_ctx* ctx) {
                     &ctx->item_cnt, &ctx->partial, &ctx->work_counter, &ctx->finkey,
                     &ctx->finkey2, &ctx->finval, &ctx->finval2, &ctx->finstart, &ctx->finrec, &ctx->maskF,
                     &ctx->maskG, &ctx->dbg, &ctx->gsend, &ctx->grecv, &ctx->lptkey,
-                    &ctx->lptkey2, &ctx->lptid, &ctx->lptid2, &ctx->tslot_all, &ctx->nown};
+                    &ctx->lptkey2, &ctx->lptid, &ctx->lptid2, &ctx->tslot_all, &ctx->nown,
+                    &ctx->chunk_stats};
   for (DevBuf* b : bufs) release(ctx, *b);
   if (ctx->comm && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)ctx->comm);
   for (int k = 0; k < 8; ++k)

@@ -328,9 +328,9 @@ void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t 
 void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
                       int64_t* caps, cudaStream_t st);
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                   const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
-                   int4* items, int4* items2, int32_t* item_cnt, uint32_t* item_key,
-                   cudaStream_t st);
+                   const int64_t* item_off, int ntiles, int64_t n_items, int target,
+                   const int32_t* owner, int rank, int4* stats, int4* items, int4* items2,
+                   int32_t* item_cnt, uint32_t* item_key, cudaStream_t st);
 
 struct TileArgs {
   const void* hot;            // HotRec<NV>[N]

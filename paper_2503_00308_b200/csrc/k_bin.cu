@@ -519,69 +519,6 @@ void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t 
 // [A_k, L_k) for any chunk length).  One warp per tile.
 //   items[i]  = {tile, s, e, flags | log2(ring length) << 8}
 //   items2[i] = {A, L, A_next, 0}
-__global__ void k_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                         const int64_t* item_off, int ntiles, int target, const int32_t* owner,
-                         int rank, int4* items, int4* items2, int32_t* item_cnt,
-                         uint32_t* item_key) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= ntiles) return;
-  const int64_t b = tbegin[t];
-  const int K = (int)(tend[t] - b);
-  const int64_t o = item_off[t];
-  const int64_t cap = item_off[t + 1] - o;
-  const bool mine = owner == nullptr || owner[t] == rank;
-  const int n = mine ? (K > 0 ? (K + target - 1) / target : 1) : 0;
-  int prevA = 0;
-  for (int k = n - 1; k >= 0; --k) {  // backwards so A_next is known
-    const int s = k * target, e = min(K, s + target);
-    int A = s, L = e, wmax = 0;
-    bool exc = false;
-    if (pm) {
-      // each lane folds a strided share of the chunk (loads pipelined), one reduction per chunk
-      int a = s, l = e, wl = 0;
-      bool ex = false;
-#pragma unroll 4
-      for (int i = s + lane; i < e; i += 32) {
-        const int4 m = pm[b + i];
-        if (m.x != 0) {
-          ex = true;
-          if (m.x & PM_EF) a = min(a, m.y);
-          if (m.x & PM_EG) l = max(l, m.z + 1);
-          wl = max(wl, max(i - m.y, m.z - i));
-        }
-      }
-      for (int sh = 16; sh > 0; sh >>= 1) {
-        a = min(a, __shfl_xor_sync(0xffffffffu, a, sh));
-        l = max(l, __shfl_xor_sync(0xffffffffu, l, sh));
-        wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, sh));
-      }
-      A = min(A, a);
-      L = max(L, l);
-      wmax = max(wmax, wl);
-      exc = __any_sync(0xffffffffu, ex);
-    }
-    int lr = 0;
-    while ((1 << lr) <= wmax) ++lr;
-    const int Anext = (k == n - 1) ? e : prevA;
-    // scan starts must not decrease (chunk k records its running product at A_{k+1} inside
-    // its own scan): extend the lookback to the next chunk's start when that reaches further
-    if (k < n - 1) A = min(A, prevA);
-    if (lane == 0) {
-      int fl = (exc ? IT_EXC : 0) | (n == 1 ? IT_SINGLE : 0) | (lr << 8);
-      items[o + k] = make_int4(t, s, e, fl);
-      items2[o + k] = make_int4(A, L, Anext, 0);
-      item_key[o + k] = (uint32_t)(L - A);
-    }
-    prevA = A;
-  }
-  for (int j = n + lane; j < cap; j += 32) {  // unused slots: empty items, sorted last
-    items[o + j] = make_int4(-1, 0, 0, 0);
-    items2[o + j] = make_int4(0, 0, 0, 0);
-    item_key[o + j] = 0;
-  }
-  if (lane == 0) item_cnt[t] = n;
-}
 __global__ void k_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
                             int64_t* caps) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -593,12 +530,92 @@ void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, in
                       int64_t* caps, cudaStream_t st) {
   k_item_caps<<<(ntiles + 255) / 256, 256, 0, st>>>(tbegin, tend, ntiles, target, caps);
 }
+// Chunk statistics in parallel (warp per work item): the lookback / lookahead margins a, l
+// of the chunk's exception windows, its longest window and whether it has any exception.
+__global__ void k_chunk_stats(const int64_t* tbegin, const int64_t* tend, const int4* pm,
+                              const int64_t* item_off, int ntiles, int64_t n_items, int target,
+                              const int32_t* owner, int rank, int4* stats) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n_items) return;
+  int lo = 0, hi = ntiles - 1;  // tile t with item_off[t] <= j < item_off[t + 1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (item_off[mid] <= j) lo = mid; else hi = mid - 1;
+  }
+  const int t = lo;
+  const int64_t b = tbegin[t];
+  const int K = (int)(tend[t] - b);
+  const bool mine = owner == nullptr || owner[t] == rank;
+  const int k = (int)(j - item_off[t]);
+  const int s = k * target, e = min(K, s + target);
+  int a = s, l = e, wl = 0;
+  bool ex = false;
+  if (mine && pm) {
+#pragma unroll 4
+    for (int i = s + lane; i < e; i += 32) {
+      const int4 m = pm[b + i];
+      if (m.x != 0) {
+        ex = true;
+        if (m.x & PM_EF) a = min(a, m.y);
+        if (m.x & PM_EG) l = max(l, m.z + 1);
+        wl = max(wl, max(i - m.y, m.z - i));
+      }
+    }
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      a = min(a, __shfl_xor_sync(0xffffffffu, a, sh));
+      l = max(l, __shfl_xor_sync(0xffffffffu, l, sh));
+      wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, sh));
+    }
+    ex = __any_sync(0xffffffffu, ex);
+  }
+  if (lane == 0) stats[j] = make_int4(a, l, wl, ex ? 1 : 0);
+}
+// per tile, back to front (A_next known, scan starts non-decreasing): the work items
+__global__ void k_chunk_items(const int64_t* tbegin, const int64_t* tend, const int4* pm,
+                              const int64_t* item_off, int ntiles, int target,
+                              const int32_t* owner, int rank, const int4* stats, int4* items,
+                              int4* items2, int32_t* item_cnt, uint32_t* item_key) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int K = (int)(tend[t] - tbegin[t]);
+  const int64_t o = item_off[t];
+  const int64_t cap = item_off[t + 1] - o;
+  const bool mine = owner == nullptr || owner[t] == rank;
+  const int n = mine ? (K > 0 ? (K + target - 1) / target : 1) : 0;
+  int prevA = 0;
+  for (int k = n - 1; k >= 0; --k) {
+    const int s = k * target, e = min(K, s + target);
+    const int4 st = stats[o + k];
+    int A = min(s, st.x);
+    const int L = max(e, st.y);
+    int lr = 0;
+    while ((1 << lr) <= st.z) ++lr;
+    const int Anext = (k == n - 1) ? e : prevA;
+    if (k < n - 1) A = min(A, prevA);
+    const int fl = ((pm && st.w) ? IT_EXC : 0) | (n == 1 ? IT_SINGLE : 0) | (lr << 8);
+    items[o + k] = make_int4(t, s, e, fl);
+    items2[o + k] = make_int4(A, L, Anext, 0);
+    item_key[o + k] = (uint32_t)(L - A);
+    prevA = A;
+  }
+  for (int64_t jj = n; jj < cap; ++jj) {  // unused slots: empty items, sorted last
+    items[o + jj] = make_int4(-1, 0, 0, 0);
+    items2[o + jj] = make_int4(0, 0, 0, 0);
+    item_key[o + jj] = 0;
+  }
+  item_cnt[t] = n;
+}
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                   const int64_t* item_off, int ntiles, int target, const int32_t* owner, int rank,
-                   int4* items, int4* items2, int32_t* item_cnt, uint32_t* item_key,
-                   cudaStream_t st) {
-  k_chunks<<<(ntiles + 3) / 4, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, target, owner,
-                                             rank, items, items2, item_cnt, item_key);
+                   const int64_t* item_off, int ntiles, int64_t n_items, int target,
+                   const int32_t* owner, int rank, int4* stats, int4* items, int4* items2,
+                   int32_t* item_cnt, uint32_t* item_key, cudaStream_t st) {
+  if (n_items > 0)
+    k_chunk_stats<<<(unsigned)((n_items + 3) / 4), 128, 0, st>>>(
+        tbegin, tend, pm, item_off, ntiles, n_items, target, owner, rank, stats);
+  k_chunk_items<<<(ntiles + 127) / 128, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, target,
+                                                      owner, rank, stats, items, items2, item_cnt,
+                                                      item_key);
 }
 
 // ------------------------------------------------------------------------- untile (a11)
