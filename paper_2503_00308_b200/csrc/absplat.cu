@@ -178,7 +178,6 @@ size_t hot_size(int nv) {
 }
 size_t pair_size(int nv) { return sizeof(double) * (2 * (nv + 1) + 2); }
 
-bool finite_f(float v) { return std::isfinite(v); }
 
 // ---------------------------------------------------------------- box (a0)
 struct BoxInfo {
@@ -372,15 +371,6 @@ int bits_for(int64_t v) {
 __global__ void k_seq(int32_t* v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = i;
-}
-__global__ void k_tile_keys(const int32_t* list, int n, const int64_t* tb, const int64_t* te,
-                            uint32_t* key) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int t = list[i];
-    const int64_t k = te[t] - tb[t];
-    key[i] = (uint32_t)(k > 0x7fffffff ? 0x7fffffff : k);
-  }
 }
 __global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned long long* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
