@@ -190,13 +190,15 @@ as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward);
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
 
 /* ---- blend mode ----
- * mode 0 (default): the interval blend (reading O7).  mode 1: additionally, on tiles whose
- * Gaussian list has no uncertain depth pair, BlendInd is evaluated with linear relations
- * along the sorted fold (a = o Exp(-s/2) with Table 2's tangent / chord kept linear in the box
- * variables, T and pc as affine forms through McCormick products, Alg. 3) and the
- * result is intersected with the interval bounds, per sub-box, before the union.  Supported
- * for boxes with at most 3 variables and full-image renders (as_render_bounds /
- * as_render_subboxes); AS_E_ARG otherwise. */
+ * mode 0 (default): the interval blend (reading O7).  mode 1: additionally BlendInd is
+ * evaluated with linear relations along the sorted fold (a = o Exp(-s/2) with Table 2's
+ * tangent / chord kept linear in the box variables, T as an affine form through McCormick
+ * products, Alg. 3): a position without uncertain depth partners contributes
+ * Mul(T, a) c, one with uncertain partners (Table 2's Ind "?") its interval-blend term
+ * [T_lo a_lo c_lo, T_hi a_hi c_hi] (reading O20); the result is intersected with the interval
+ * bounds, per sub-box, before the union.  Boxes with up to 9 variables; full-image renders
+ * (as_render_bounds / as_render_subboxes, and the sub-box sharding axis); AS_E_ARG for tile
+ * sharding. */
 as_status as_set_blend(as_ctx* ctx, int32_t mode);
 
 /* ---- work split (performance knob, like tile and batch) ----

@@ -881,9 +881,11 @@ void build_tile_list(const Problem& P, const SubData& S, int ts, int tile, bool 
     }
 }
 
-// steps 18-19, windowed form: prefix products + exception windows (uses step 13 structure)
+// steps 18-19, windowed form: prefix products + exception windows (uses step 13 structure).
+// unc_only: sum the contributions of the uncertain positions only (E_F or E_G non-empty;
+// reading O20's interval part)
 void blend_windowed(const SubData& S, const TileList& T, const double* alo, const double* ahi,
-                    double pc_lo[3], double pc_hi[3]) {
+                    double pc_lo[3], double pc_hi[3], bool unc_only = false) {
   const int K = (int)T.L.size();
   std::vector<double> Pb(K + 1), Pl(K + 1);
   Pb[0] = 1.0;
@@ -912,6 +914,7 @@ void blend_windowed(const SubData& S, const TileList& T, const double* alo, cons
     }
     Tl = Pl[p];
     for (int q : T.EG[p]) Tl *= 1.0 - ahi[q];
+    if (unc_only && ef.empty() && T.EG[p].empty()) continue;
     const GRec& G = S.G[T.L[p]];
     for (int c = 0; c < 3; ++c) {
       pc_hi[c] += Tb * ahi[p] * G.c_hi[c];
@@ -982,24 +985,31 @@ bool opacity_form(const GRec& G, const double u[2], int n, Form& a) {
   return true;
 }
 
-// BlendInd (Alg. 3) with linear relations along the sorted fold, for a tile list
-// whose pairs are all certain (then F(i) = before(i) and the fold is a prefix):
-// T_0 = 1, pc_c += Mul(T_i, a_i) c_i (R1; c in [c_lo, c_hi] >= 0 scales the lower / upper
-// form), T_{i+1} = Mul(T_i, 1 - a_i) (R1).  Culled Gaussians (a = 0) are skipped.
-void blend_linear(const SubData& S, const std::vector<int64_t>& L, const std::vector<char>& act,
-                  const std::vector<Form>& a, double pc_lo[3], double pc_hi[3]) {
+// BlendInd (Alg. 3) with linear relations along the sorted fold (reading O20):
+// T_0 = 1, T_{i+1} = Mul(T_i, 1 - a_i) (R1) over every position.  A certain position i (no
+// uncertain partner: F(i) = before(i), every later Gaussian certainly behind) contributes
+// Mul(T_i, a_i) c_i (R1; c in [c_lo, c_hi] >= 0 scales the lower / upper form); an uncertain
+// one contributes its interval term [T_lo a_lo c_lo, T_hi a_hi c_hi] of the interval blend,
+// passed in as unc_lo / unc_hi (zero on exception-free lists, where this is the plain fold).
+// Culled Gaussians (a = 0) are skipped.
+void blend_linear(const SubData& S, const TileList& TL, const std::vector<char>& act,
+                  const std::vector<Form>& a, const double unc_lo[3], const double unc_hi[3],
+                  double pc_lo[3], double pc_hi[3]) {
   const int n = S.B.n;
+  const std::vector<int64_t>& L = TL.L;
   Form T = constant(1.0);
   Form pc[3] = {constant(0.0), constant(0.0), constant(0.0)};
   for (size_t p = 0; p < L.size(); ++p) {
     if (!act[p]) continue;
     const GRec& G = S.G[L[p]];
-    const Form ta = mul(T, a[p], n);
-    for (int c = 0; c < 3; ++c) {
-      Form t;
-      t.lo = aff_scale(ta.lo, G.c_lo[c]);
-      t.hi = aff_scale(ta.hi, G.c_hi[c]);
-      pc[c] = add(pc[c], t);
+    if (TL.EF[p].empty() && TL.EG[p].empty()) {
+      const Form ta = mul(T, a[p], n);
+      for (int c = 0; c < 3; ++c) {
+        Form t;
+        t.lo = aff_scale(ta.lo, G.c_lo[c]);
+        t.hi = aff_scale(ta.hi, G.c_hi[c]);
+        pc[c] = add(pc[c], t);
+      }
     }
     Form om;  // 1 - a
     om.lo = aff_scale(a[p].hi, -1.0);
@@ -1009,8 +1019,8 @@ void blend_linear(const SubData& S, const std::vector<int64_t>& L, const std::ve
     T = mul(T, om, n);
   }
   for (int c = 0; c < 3; ++c) {
-    pc_lo[c] = aff_min(pc[c].lo, n);
-    pc_hi[c] = aff_max(pc[c].hi, n);
+    pc_lo[c] = aff_min(pc[c].lo, n) + unc_lo[c];
+    pc_hi[c] = aff_max(pc[c].hi, n) + unc_hi[c];
   }
 }
 
@@ -1085,14 +1095,16 @@ int render_tiles_impl(const Problem& P, int ts, const std::vector<int>& tiles, i
           else
             blend_windowed(S, T, alo.data(), ahi.data(), pl, ph);
           finalise((double)P.N, pl, ph);
-          if (mode == 2 && T.uncertain == 0) {
-            // NEXT-1: linear-relation blend on exception-free lists, intersected with the
-            // interval blend (both sound)
+          if (mode == 2) {
+            // NEXT-1: linear-relation blend (certain positions as forms, uncertain ones as
+            // interval terms, O20), intersected with the interval blend (both sound)
             std::vector<char> act(K);
             std::vector<Form> af(K);
             for (int p = 0; p < K; ++p) act[p] = opacity_form(S.G[T.L[p]], u, S.B.n, af[p]);
+            double ul[3] = {0, 0, 0}, uh[3] = {0, 0, 0};
+            if (T.uncertain > 0) blend_windowed(S, T, alo.data(), ahi.data(), ul, uh, true);
             double ql[3], qh[3];
-            blend_linear(S, T.L, act, af, ql, qh);
+            blend_linear(S, T, act, af, ul, uh, ql, qh);
             finalise((double)P.N, ql, qh);
             for (int c = 0; c < 3; ++c) {
               pl[c] = std::max(pl[c], ql[c]);

@@ -89,7 +89,8 @@ struct as_ctx {
   int last_n_owned = 0;
   bool last_has_exc = false;
   int64_t last_M = 0;
-  DevBuf tmp_lo, tmp_hi, tile_unc, lin_tiles;
+  DevBuf tmp_lo, tmp_hi, lin_tiles, unc_lo, unc_hi;
+  bool last_unc = false;  // unc_lo / unc_hi hold the last sub-box's uncertain terms
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
   as_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -673,6 +674,26 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   if (pt) CK(cudaEventRecord(ctx->ev[5], st));
   launch_merge(ta, st);
   LAUNCHED(ctx, 1);
+  // NEXT-1 (O20): the uncertain positions' interval terms as raw per-pixel sums, for the
+  // linear blend that follows (full-image renders only)
+  ctx->last_unc = false;
+  if (ctx->blend_mode == 1 && has_exc && !tslot) {
+    const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
+    ensure(ctx, ctx->unc_lo, sizeof(float) * img);
+    ensure(ctx, ctx->unc_hi, sizeof(float) * img);
+    TileArgs tu = ta;
+    tu.unc_only = 1;
+    tu.first = 1;
+    tu.lo = P<float>(ctx->unc_lo);
+    tu.hi = P<float>(ctx->unc_hi);
+    tu.active = ctr + C_SCENE;  // scratch: the active pairs were counted by the first pass
+    tu.dbg = nullptr;
+    CK(cudaMemsetAsync(ctx->work_counter.p, 0, sizeof(int), st));
+    launch_tile(nv, tu, grid, st);
+    launch_merge(tu, st);
+    LAUNCHED(ctx, 2);
+    ctx->last_unc = true;
+  }
   (void)tlist;
   (void)n_list;
   if (pt) {
@@ -1055,7 +1076,7 @@ as_status as_destroy(as_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->mean, &ctx->chol, &ctx->opacity, &ctx->color, &ctx->st_mean,
                     &ctx->st_chol, &ctx->st_opacity, &ctx->st_color, &ctx->group_of,
-                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->priv_lo, &ctx->priv_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->tile_unc, &ctx->lin_tiles, &ctx->pose, &ctx->hot,
+                    &ctx->col_lo, &ctx->col_hi, &ctx->op_lo, &ctx->op_hi, &ctx->priv_lo, &ctx->priv_hi, &ctx->subs, &ctx->tmp_lo, &ctx->tmp_hi, &ctx->lin_tiles, &ctx->unc_lo, &ctx->unc_hi, &ctx->pose, &ctx->hot,
                     &ctx->pair, &ctx->kkey, &ctx->kkey2, &ctx->kval, &ctx->order, &ctx->counts,
                     &ctx->offsets, &ctx->cub_tmp, &ctx->keys, &ctx->keys2, &ctx->vals,
                     &ctx->vals2, &ctx->tbegin, &ctx->tend, &ctx->tcost, &ctx->tkey, &ctx->tkey2,
@@ -1510,26 +1531,19 @@ namespace {
 // tiles with the linear-relation blend
 void linear_pass(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int batch, float* lo,
                  float* hi) {
+  // NEXT-1 (O20): every non-empty tile, longest lists first (blocks are scheduled roughly in
+  // launch order, so the long tiles do not form the tail); certain positions through the
+  // linear fold, uncertain ones through the interval terms of the pass in render_subbox
   cudaStream_t st = ctx->stream;
-  const int64_t M = ctx->last_M;
-  ensure(ctx, ctx->tile_unc, sizeof(int32_t) * G.ntiles);
   ensure(ctx, ctx->lin_tiles, sizeof(int32_t) * G.ntiles);
-  CK(cudaMemsetAsync(ctx->tile_unc.p, 0, sizeof(int32_t) * G.ntiles, st));
-  if (ctx->last_has_exc)
-    launch_tile_unc(P<int4>(ctx->pflag), P<uint32_t>(ctx->keys2), M, P<int32_t>(ctx->tile_unc), st);
-  std::vector<int32_t> unc(G.ntiles);
   std::vector<int64_t> tb(G.ntiles), te(G.ntiles);
-  CK(cudaMemcpyAsync(unc.data(), ctx->tile_unc.p, sizeof(int32_t) * G.ntiles,
-                     cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(tb.data(), ctx->tbegin.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(te.data(), ctx->tend.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   std::vector<int32_t> list;
   for (int t = 0; t < G.ntiles; ++t)
-    if (!unc[t] && te[t] > tb[t]) list.push_back(t);
+    if (te[t] > tb[t]) list.push_back(t);
   if (list.empty()) return;
-  // longest lists first: blocks are scheduled roughly in launch order, so the long tiles do
-  // not form the tail
   std::stable_sort(list.begin(), list.end(),
                    [&](int32_t a, int32_t b) { return te[a] - tb[a] > te[b] - tb[b]; });
   CK(cudaMemcpyAsync(ctx->lin_tiles.p, list.data(), sizeof(int32_t) * list.size(),
@@ -1539,13 +1553,16 @@ void linear_pass(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int batch, f
   ta.vals = P<int32_t>(ctx->vals2);
   ta.tbegin = P<int64_t>(ctx->tbegin);
   ta.tend = P<int64_t>(ctx->tend);
+  ta.pm = ctx->last_unc ? P<int4>(ctx->pflag) : nullptr;
   ta.ts = G.ts;
   ta.ntx = G.ntx;
   ta.W = ctx->cam.W;
   ta.H = ctx->cam.H;
   ta.bs = std::min(batch, 16);
   ta.ntau = (float)((double)ctx->N * TAU);
-  launch_tile_lin(bi.n_vars, ta, P<int32_t>(ctx->lin_tiles), (int)list.size(), lo, hi, st);
+  launch_tile_lin(bi.n_vars, ta, P<int32_t>(ctx->lin_tiles), (int)list.size(), lo, hi,
+                  ctx->last_unc ? P<float>(ctx->unc_lo) : nullptr,
+                  ctx->last_unc ? P<float>(ctx->unc_hi) : nullptr, st);
   LAUNCHED(ctx, 1);
   CK(cudaStreamSynchronize(st));  // list (host) must outlive the copy above
 }

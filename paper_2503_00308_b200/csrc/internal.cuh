@@ -372,6 +372,9 @@ struct TileArgs {
   int64_t nexc;               // entries of exc[]
   int64_t n_partial;          // floats of partial[]
   int64_t n_out;              // floats of lo / hi (row-major image or tile-major slots)
+  // NEXT-1 (reading O20): 1 = sum the interval terms of the uncertain positions only (E_F or
+  // E_G non-empty) and write the raw sums (no +- N tau, no clamp) -- the linear blend adds them
+  int unc_only;
 };
 // rare-path counters of the tile kernel (as_debug_counters): evidence that every slow path
 // of the exception machinery runs in some parity case
@@ -379,12 +382,10 @@ enum { DBG_THI_BITS = 0, DBG_THI_DIV_UNSAFE = 1, DBG_THI_OVF = 2, DBG_THI_OVF_WI
        DBG_FIN_SLOW = 4, DBG_FIN_UNSTAGED = 5, DBG_FIN_OVF = 6, DBG_TMODE3 = 7, DBG_N = 8 };
 void launch_tile(int nv, const TileArgs& a, int grid, cudaStream_t st);
 void launch_merge(const TileArgs& a, cudaStream_t st);
-// NEXT-1 linear blend (n <= 3): intersect exception-free tiles' bounds in lo / hi
-constexpr int NV_LINEAR_MAX = 3;
+// NEXT-1 linear blend (n <= 9, reading O20): intersect every tile's bounds in lo / hi
+constexpr int NV_LINEAR_MAX = 9;
 void launch_tile_lin(int nv, const TileArgs& a, const int32_t* tiles, int n_tiles, float* lo,
-                     float* hi, cudaStream_t st);
-void launch_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc,
-                     cudaStream_t st);
+                     float* hi, const float* unc_lo, const float* unc_hi, cudaStream_t st);
 void launch_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n, bool first,
                   cudaStream_t st);
 int tile_threads(int ts);

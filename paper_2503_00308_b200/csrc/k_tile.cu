@@ -697,11 +697,12 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
                     window_prod<SBP>(rf, R.ph, qpos, A.exc + R.peoff, R.pnF, rmask);
           }
         }
-        const float wb = main ? tbv * ahi : 0.f;
+        // (unc_only: the interval terms of uncertain positions only, O20)
+        const float wb = (main && (!A.unc_only || (pmf & (PM_EF | PM_EG)))) ? tbv * ahi : 0.f;
 #pragma unroll
         for (int c = 0; c < 3; ++c) ahc[c] = fmaf(wb, R.chi[c], ahc[c]);
         // lower: T_lo over before(q) (E_G(q) empty) or deferred to max E_G(q)
-        if (main && !(pmf & PM_EG)) {
+        if (main && !(pmf & PM_EG) && (!A.unc_only || (pmf & PM_EF))) {
           const float wl = Tl * alo;
 #pragma unroll
           for (int c = 0; c < 3; ++c) alc[c] = fmaf(wl, R.clo[c], alc[c]);
@@ -768,6 +769,10 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A)
         for (int c = 0; c < 3; ++c) {
           float l = fminf(fmaxf(alc[c] - A.ntau, 0.f), 1.f);
           float h = fminf(fmaxf(ahc[c] + A.ntau, 0.f), 1.f);
+          if (A.unc_only) {
+            l = alc[c];
+            h = ahc[c];
+          }
           if (!in_img) l = h = 0.f;
           if (A.first) {
             A.lo[o + c] = l;
@@ -1410,10 +1415,12 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
                          window_prod2(rf, R.ph, qpos, A.exc + R.peoff, R.pnF, rmask));
           }
         }
-        const float2 wb = main ? mul2(tbv, ahi) : f2(0.f, 0.f);
+        // (unc_only: the interval terms of uncertain positions only, O20)
+        const float2 wb = (main && (!A.unc_only || (pmf & (PM_EF | PM_EG)))) ? mul2(tbv, ahi)
+                                                                            : f2(0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < 3; ++c) ahc[c] = __ffma2_rn(wb, bc(R.chi[c]), ahc[c]);
-        if (main && !(pmf & PM_EG)) {
+        if (main && !(pmf & PM_EG) && (!A.unc_only || (pmf & PM_EF))) {
           const float2 wl = mul2(Tl, alo);
 #pragma unroll
           for (int c = 0; c < 3; ++c) alc[c] = __ffma2_rn(wl, bc(R.clo[c]), alc[c]);
@@ -1485,6 +1492,10 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
           for (int c = 0; c < 3; ++c) {
             float l = fminf(fmaxf(lc[c] - A.ntau, 0.f), 1.f);
             float h = fminf(fmaxf(hc[c] + A.ntau, 0.f), 1.f);
+            if (A.unc_only) {
+              l = lc[c];
+              h = hc[c];
+            }
             if (!in) l = h = 0.f;
             if (A.first) {
               A.lo[o + c] = l;
@@ -1519,7 +1530,8 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
 // finalised (+- N tau, clamp) and intersected with the interval bounds already in img.
 template <int NV>
 __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tiles, int n_tiles,
-                                                 float* img_lo, float* img_hi) {
+                                                 float* img_lo, float* img_hi,
+                                                 const float* unc_lo, const float* unc_hi) {
   constexpr int SBX = 8, SBP = 64, C = NV + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ts = A.ts, nsb = ts / SBX, nsub = nsb * nsb;
@@ -1561,6 +1573,7 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
       const bool skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
       if (part == NPART - 1) {
         S.flags = H->flags | (skip ? F_SKIP : 0);
+        S.pmf = A.pm ? A.pm[tb + b0 + j].x : 0;  // uncertain partners (O20)
         S.r2 = H->r2;
         S.o[0] = H->o[0];
         S.o[1] = H->o[1];
@@ -1620,15 +1633,17 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
           for (int k = 0; k < C; ++k) al[k] = 0.f;
         }
       }
-      float tal[C], tah[C];
-      form_mul<NV>(Tl, Th, al, ah, tal, tah);
+      if (!(R.pmf & (PM_EF | PM_EG))) {  // certain position: Mul(T, a) c (uncertain: unc_*)
+        float tal[C], tah[C];
+        form_mul<NV>(Tl, Th, al, ah, tal, tah);
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int k = 0; k < C; ++k) {
-          pl[c][k] = fmaf(R.clo[c], tal[k], pl[c][k]);
-          ph[c][k] = fmaf(R.chi[c], tah[k], ph[c][k]);
-        }
+          for (int k = 0; k < C; ++k) {
+            pl[c][k] = fmaf(R.clo[c], tal[k], pl[c][k]);
+            ph[c][k] = fmaf(R.chi[c], tah[k], ph[c][k]);
+          }
+      }
       float oml[C], omh[C];  // 1 - a
 #pragma unroll
       for (int k = 0; k < C; ++k) {
@@ -1656,6 +1671,10 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
       l -= fabsf(pl[c][k]);
       h += fabsf(ph[c][k]);
     }
+    if (unc_lo) {  // the uncertain positions' interval terms (raw sums, O20)
+      l += unc_lo[o + c];
+      h += unc_hi[o + c];
+    }
     l = fminf(fmaxf(l - A.ntau, 0.f), 1.f);
     h = fminf(fmaxf(h + A.ntau, 0.f), 1.f);
     img_lo[o + c] = fmaxf(img_lo[o + c], l);
@@ -1663,11 +1682,6 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
   }
 }
 
-// tiles whose list has an uncertain pair (their bounds keep the interval blend)
-__global__ void k_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < M && (pm[p].x & (PM_EF | PM_EG))) unc[keys[p]] = 1;
-}
 // union of one sub-box image into the result (step 22): copy for the first sub-box
 __global__ void k_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n,
                         int first) {
@@ -1723,6 +1737,10 @@ __global__ void k_merge(TileArgs A) {
     for (int c = 0; c < 3; ++c) {
       float lv = fminf(fmaxf(l[c] - A.ntau, 0.f), 1.f);
       float hv = fminf(fmaxf(h[c] + A.ntau, 0.f), 1.f);
+      if (A.unc_only) {
+        lv = l[c];
+        hv = h[c];
+      }
       if (!inside) lv = hv = 0.f;
       if (A.first) {
         A.lo[o + c] = lv;
@@ -1855,23 +1873,22 @@ static size_t smem_lin(int bs) {
   return (size_t)bs * (sizeof(SRec<NV>) + 2 * 8 * sizeof(double));
 }
 void launch_tile_lin(int nv, const TileArgs& a, const int32_t* tiles, int n_tiles, float* lo,
-                     float* hi, cudaStream_t st) {
+                     float* hi, const float* unc_lo, const float* unc_hi, cudaStream_t st) {
   const int grid = n_tiles * (a.ts / 8) * (a.ts / 8);
   if (grid <= 0) return;
   switch (nv) {
-#define CASE(K)                                                                         \
-  case K:                                                                               \
-    k_tile_lin<K><<<grid, 64, smem_lin<K>(a.bs), st>>>(a, tiles, n_tiles, lo, hi);      \
+#define CASE(K)                                                                              \
+  case K:                                                                                    \
+    cudaFuncSetAttribute(k_tile_lin<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                         200 * 1024);                                                        \
+    k_tile_lin<K><<<grid, 64, smem_lin<K>(a.bs), st>>>(a, tiles, n_tiles, lo, hi, unc_lo,     \
+                                                       unc_hi);                              \
     break;
-    CASE(0) CASE(1) CASE(2) CASE(3)
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
     default:
       break;
   }
-}
-void launch_tile_unc(const int4* pm, const uint32_t* keys, int64_t M, int32_t* unc,
-                     cudaStream_t st) {
-  if (M > 0) k_tile_unc<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(pm, keys, M, unc);
 }
 void launch_union(const float* slo, const float* shi, float* lo, float* hi, int64_t n, bool first,
                   cudaStream_t st) {
