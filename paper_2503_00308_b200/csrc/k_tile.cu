@@ -25,6 +25,7 @@
 // H3); the lower contribution of a position with later uncertain partners is deferred and
 // finalised at g = max E_G, when all of E_G's (1 - a_hi) are known.
 #include <algorithm>
+#include <cfloat>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -1139,8 +1140,6 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
     const int64_t tb = A.tbegin[tile];
     const double ucx = ox + 0.5 * B2, ucy = oy + 0.5 * B2;
     const bool iexc = has_exc && (iflags & IT_EXC);
-    const bool inA = (ox + lx < A.W) && (oy + ly < A.H);
-    const bool inB = (ox + lx < A.W) && (oy + ly + 4 < A.H);
     const double bx0 = ox + 0.5, bx1 = fmin((double)(ox + B2), (double)A.W) - 0.5;
     const double by0 = oy + 0.5, by1 = fmin((double)(oy + B2), (double)A.H) - 0.5;
     const bool block_live = ox < A.W && oy < A.H;
@@ -1215,7 +1214,10 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         S.nT = 0;
         S.pmf = pmf;
         S.flags = H->flags | (skip ? F_SKIP : 0);
-        S.r2 = r2;
+        // finite radius: an infinite cull-table entry (pixel outside the image) then always
+        // fails the walk's test, which needs no per-pixel in-image flag (r2 = inf or NaN keeps
+        // every in-image pixel either way)
+        S.r2 = fmin(r2, DBL_MAX);
         S.o[0] = H->o[0];
         S.o[1] = H->o[1];
 #pragma unroll
@@ -1228,10 +1230,10 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
           for (int l = 0; l < B2; ++l) {
             const double x = ox + l + 0.5;
             const double dx = fmax(0.0, fmax(__dsub_rn(mxl, x), __dsub_rn(x, mxh)));
-            cx2[j * B2 + l] = __dmul_rn(dx, dx);
+            cx2[j * B2 + l] = ox + l < A.W ? __dmul_rn(dx, dx) : (double)INFINITY;
             const double y = oy + l + 0.5;
             const double dy = fmax(0.0, fmax(__dsub_rn(myl, y), __dsub_rn(y, myh)));
-            cy2[j * B2 + l] = __dmul_rn(dy, dy);
+            cy2[j * B2 + l] = oy + l < A.H ? __dmul_rn(dy, dy) : (double)INFINITY;
           }
         }
       }
@@ -1340,12 +1342,20 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         }
         if ((flags & F_SKIP) && pmf == 0) continue;
         const bool main = qpos >= pbeg && qpos < pend;
+        // the first finalisation record's deferred term, loaded before the opacity so its
+        // latency hides behind it (slot qq is not rewritten before the use: qpos - qq < R)
+        const int fr0 = R.pfb - F0;
+        float2 tl0 = f2(0.f, 0.f);
+        if (fr0 < R.pfe - F0 && fr0 < FB) {
+          const int q0 = fins[fr0].qq;
+          if (q0 >= 0) tl0 = rf[RS2(q0, 3, rmask)];
+        }
         float2 alo = f2(0.f, 0.f), ahi = f2(0.f, 0.f);
         bool kA = false, kB = false;
         if (!(flags & F_SKIP)) {
           const double cx = cx2[j * B2 + lx];
-          kA = inA && !(__dadd_rn(cx, cy2[j * B2 + ly]) > R.r2);
-          kB = inB && !(__dadd_rn(cx, cy2[j * B2 + ly + 4]) > R.r2);
+          kA = !(__dadd_rn(cx, cy2[j * B2 + ly]) > R.r2);
+          kB = !(__dadd_rn(cx, cy2[j * B2 + ly + 4]) > R.r2);
           if (__any_sync(FULLM, kA || kB)) {
             if (flags & F_FAIL) {
               ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
@@ -1435,7 +1445,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
             if (F.qq < 0) continue;
             DCHECK(qpos - F.qq > 0 && qpos - F.qq <= rmask && F.qq >= scan0);
             clo = F.clo;
-            tl = rf[RS2(F.qq, 3, rmask)];
+            tl = f == fr0 ? tl0 : rf[RS2(F.qq, 3, rmask)];
             if (tl.x == 0.f && tl.y == 0.f) continue;
             if (F.n >= 0) {
               tl = mul2(tl, f2(1.f - ahi.x, 1.f - ahi.y));
@@ -1476,7 +1486,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int py = oy + ly + 4 * e, px = ox + lx;
-      const bool in = e ? inB : inA;
+      const bool in = (px < A.W) && (py < A.H);
       const float hc[3] = {e ? ahc[0].y : ahc[0].x, e ? ahc[1].y : ahc[1].x, e ? ahc[2].y : ahc[2].x};
       const float lc[3] = {e ? alc[0].y : alc[0].x, e ? alc[1].y : alc[1].x, e ? alc[2].y : alc[2].x};
       if (iflags & IT_SINGLE) {
