@@ -108,15 +108,20 @@ typedef struct {
   double ms_pose, ms_setup, ms_bin, ms_pairs, ms_tile, ms_total;
   double tile_kernel_ms;   /* sum of k_tile durations */
   size_t device_bytes;     /* bytes currently held by the context */
-  int32_t n_items;         /* (tile, chunk) work items of the last sub-box */
+  int32_t n_items;         /* (tile, chunk) work items (max over sub-boxes) */
   int32_t grid;            /* persistent CTAs of the tile kernel (last sub-box) */
-  int32_t ring_len;        /* exception ring length R (last sub-box; 1 = no exceptions) */
+  int32_t ring_len;        /* exception ring length R allocated (last sub-box; 1 = none) */
   int32_t max_window;      /* longest exception window, positions (max over sub-boxes) */
   double ms_gather;        /* multi-GPU: the collective (all-gather of bound tiles or
                               all-reduce min/max of sub-box unions) and the untile */
   int32_t world;           /* ranks of the context's communicator (1 = single GPU) */
   int32_t n_owned;         /* tiles this rank rendered (tile sharding), else n_tiles */
   size_t peak_bytes;       /* device bytes held by the context at its largest */
+  int32_t host_syncs;      /* blocking device-to-host reads inside the render pipeline: 0 when
+                              it ran sync-free (sizes remembered from an earlier render of the
+                              same tile / batch / box dimension, checked once at the end) */
+  int32_t resized;         /* 1: the sync-free attempt outgrew the remembered sizes and the
+                              render was repeated reading each size back (result unaffected) */
 } as_stats;
 
 /* Flags */

@@ -64,7 +64,8 @@ struct as_ctx {
   DevBuf img_lo, img_hi, counters, conc_g, untile_map;
   size_t bytes = 0, peak_bytes = 0;
   int64_t launches = 0;
-  int last_items = 0, last_grid = 0, last_R = 1, max_window = 0, last_wmax = 0;
+  int last_items = 0, last_grid = 0, last_R = 1, last_wmax = 0;
+  int host_syncs = 0;  // blocking device -> host reads inside the current render
   cudaEvent_t ev[8] = {};
   bool events = false;
   // explicit partition (as_set_subboxes): host copy [n][9][2] and its device mirror
@@ -88,9 +89,22 @@ struct as_ctx {
   int last_out_tiles = 0;  // tile-major output capacity (checked build bounds)
   int last_n_owned = 0;
   bool last_has_exc = false;
-  int64_t last_M = 0;
   DevBuf tmp_lo, tmp_hi, lin_tiles, unc_lo, unc_hi;
   bool last_unc = false;  // unc_lo / unc_hi hold the last sub-box's uncertain terms
+  // Sync-free renders: the sizes a render would otherwise read back mid-pipeline (pairs,
+  // exception-list length, ring length, work items), remembered from the last probed render
+  // with the same tile / batch / box dimension.  spec_on: this render sizes from `spec`
+  // (buffers padded, kernels skip padding) and is verified once at its end; `probe`
+  // collects the maxima while a probing render reads them.
+  struct Sizes {
+    bool valid = false, exc = false;
+    int ts = 0, bs = 0, nv = -1, R = 1;
+    int64_t M = 0, nexc = 0, items = 0;
+  } spec, probe;
+  bool spec_on = false;
+  int64_t spec_redo = 0;  // renders repeated after a failed verification (stats)
+  // per sub-box phase events (collected after the render's single synchronisation)
+  std::vector<cudaEvent_t> sbev;
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
   as_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -278,11 +292,6 @@ struct Geometry {
 };
 
 // ---------------------------------------------------------------- per sub-box pipeline
-struct SubResult {
-  int64_t pairs = 0;
-  int kmax = 0;
-};
-
 void run_setup(as_ctx* ctx, const BoxInfo& bi, int s) {
   SetupArgs a{};
   a.mean = P<float>(ctx->mean);
@@ -382,15 +391,50 @@ __global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned
 }
 
 // counters layout (unsigned long long[16])
-enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6, C_UNC = 8,
-       C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_SCENE = 12, C_NCOUNTERS = 16 };
+enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_PAIRS = 3, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6,
+       C_MMAX = 7, C_UNC = 8, C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_SCENE = 12,
+       C_NEXCMAX = 13, C_ITEMSMAX = 14, C_WMAXALL = 15, C_OVF = 16, C_NCOUNTERS = 24 };
 
-int64_t read_i64(as_ctx* ctx, const int64_t* dptr) {
-  int64_t v = 0;
+// sizes the render needs on the device only: max (and sum) over the render's sub-boxes
+__global__ void k_note(const int64_t* v, unsigned long long* mx, unsigned long long* sum) {
+  const unsigned long long x = (unsigned long long)(*v > 0 ? *v : 0);
+  if (mx) atomicMax(mx, x);
+  if (sum) atomicAdd(sum, x);
+}
+__global__ void k_note32(const unsigned* v, unsigned long long* mx) {
+  atomicMax(mx, (unsigned long long)*v);
+}
+// padding of a buffer sized from remembered capacities: positions [*n, cap) get a tile id
+// past the last tile (sorted last, skipped by every later kernel)
+__global__ void k_pad_pairs(uint32_t* keys, int32_t* vals, const int64_t* n, int64_t cap,
+                            uint32_t sentinel) {
+  for (int64_t p = *n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cap;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    keys[p] = sentinel;
+    vals[p] = 0;
+  }
+}
+// work items [*n, cap): empty (tile -1), sorted last
+__global__ void k_pad_items(int4* items, int4* items2, uint32_t* key, const int64_t* n,
+                            int64_t cap) {
+  for (int64_t j = *n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cap;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    items[j] = make_int4(-1, 0, 0, 0);
+    items2[j] = make_int4(0, 0, 0, 0);
+    key[j] = 0;
+  }
+}
+
+// a blocking read of a device value (a host synchronisation inside the pipeline)
+template <typename T>
+T read_dev(as_ctx* ctx, const T* dptr) {
+  T v{};
   CK(cudaMemcpyAsync(&v, dptr, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ++ctx->host_syncs;
   return v;
 }
+int64_t read_i64(as_ctx* ctx, const int64_t* dptr) { return read_dev(ctx, dptr); }
 
 struct PhaseTimes {
   double setup = 0, bin = 0, pairs = 0, tile = 0;
@@ -398,11 +442,23 @@ struct PhaseTimes {
 
 // Render one sub-box (rows a2-a10) into row-major (tslot == nullptr) or compact tile-major
 // outputs.  tlist: device list of n_list tiles to render; owner: device owner map or null.
+// Sizes: a probing render reads each size back when it is known (a host synchronisation);
+// a sync-free one (ctx->spec_on) takes the remembered capacity, pads up to it on the device and
+// leaves the check to the end of the render (verify_sizes).  The kernels compute the same
+// chunks and results either way.
+int64_t size_or_cap(as_ctx* ctx, const int64_t* dptr, int64_t cap, int64_t& probe_max) {
+  if (ctx->spec_on) return cap;
+  const int64_t v = read_i64(ctx, dptr);
+  probe_max = std::max(probe_max, v);
+  return v;
+}
+
+// ev: 6 events of this sub-box for the phase times (nullptr: none)
 void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const Geometry& G,
                    int bs, const int32_t* owner, int rank, const int32_t* tlist, int n_list,
-                   const int32_t* tslot, float* lo, float* hi, bool first, int64_t& pairs_out,
-                   PhaseTimes* pt) {
+                   const int32_t* tslot, float* lo, float* hi, bool first, cudaEvent_t* ev) {
   cudaStream_t st = ctx->stream;
+  const bool spec = ctx->spec_on;
   ctx->last_has_exc = false;
   const int64_t N = ctx->N;
   const int nv = bi.n_vars;
@@ -410,12 +466,12 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   // BS is a performance knob: clamp it to what fits in shared memory at this n, and to 128
   // (k_tile's 256-position skip ring covers a batch plus the 128 positions before it)
   bs = tile_batch(nv, G.ts, bs);
-  if (pt) CK(cudaEventRecord(ctx->ev[1], st));
+  if (ev) CK(cudaEventRecord(ev[0], st));
   if (do_setup) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
     run_setup(ctx, bi, s);
   }
-  if (pt) CK(cudaEventRecord(ctx->ev[2], st));
+  if (ev) CK(cudaEventRecord(ev[1], st));
   // ---- a6: depth order (stable radix sort by kappa: ties keep ascending index, G6)
   cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
                   P<int32_t>(ctx->kval), P<int32_t>(ctx->order), N, 64);
@@ -439,17 +495,25 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   launch_count(ba, st);
   LAUNCHED(ctx, 1);
   cub_exclusive_sum(ctx, ba.counts, P<int64_t>(ctx->offsets), N + 1);
-  const int64_t M = read_i64(ctx, P<int64_t>(ctx->offsets) + N);
-  pairs_out = M;
+  const int64_t* Mdev = P<int64_t>(ctx->offsets) + N;
+  k_note<<<1, 1, 0, st>>>(Mdev, ctr + C_MMAX, ctr + C_PAIRS);
+  LAUNCHED(ctx, 1);
+  const int64_t M = size_or_cap(ctx, Mdev, ctx->spec.M, ctx->probe.M);
   ensure(ctx, ctx->keys, sizeof(uint32_t) * (M + 1));
   ensure(ctx, ctx->keys2, sizeof(uint32_t) * (M + 1));
   ensure(ctx, ctx->vals, sizeof(int32_t) * (M + 1));
   ensure(ctx, ctx->vals2, sizeof(int32_t) * (M + 1));
   ba.keys = P<uint32_t>(ctx->keys);
   ba.vals = P<int32_t>(ctx->vals);
+  ba.cap = M;
   launch_emit(ba, st);
   LAUNCHED(ctx, 1);
-  // stable sort by tile id: within a tile the depth order of emission is kept
+  if (spec && M > 0) {
+    k_pad_pairs<<<148, 256, 0, st>>>(ba.keys, ba.vals, Mdev, M, (uint32_t)G.ntiles);
+    LAUNCHED(ctx, 1);
+  }
+  // stable sort by tile id: within a tile the depth order of emission is kept (padding ids
+  // = ntiles fit the sorted bits and go last)
   if (M > 0)
     cub_sort_keys32(ctx, P<uint32_t>(ctx->keys), P<uint32_t>(ctx->keys2), P<int32_t>(ctx->vals),
                     P<int32_t>(ctx->vals2), M, bits_for(G.ntiles), false);
@@ -460,7 +524,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   k_tile_max<<<(G.ntiles + 255) / 256, 256, 0, st>>>(P<int64_t>(ctx->tbegin),
                                                      P<int64_t>(ctx->tend), G.ntiles, ctr + C_KMAX);
   LAUNCHED(ctx, 1);
-  if (pt) CK(cudaEventRecord(ctx->ev[3], st));
+  if (ev) CK(cudaEventRecord(ev[2], st));
   // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
   TileArgs ta{};
   bool has_exc = false;
@@ -482,6 +546,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     pa.tbegin = P<int64_t>(ctx->tbegin);
     pa.tend = P<int64_t>(ctx->tend);
     pa.M = M;
+    pa.nexc_cap = 0;
     pa.pair = ctx->pair.p;
     pa.nv = nv;
     pa.pose = P<PoseDev>(ctx->pose) + s;
@@ -517,15 +582,21 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     LAUNCHED(ctx, 2);
     launch_pairs_count(pa, st);  // one classification pass: counts, h, g, 128-bit masks
     LAUNCHED(ctx, 1);
-    unsigned long long sub_unc = 0;
-    CK(cudaMemcpyAsync(&sub_unc, pa.subunc, sizeof sub_unc, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (sub_unc > 0) {
+    bool any_unc = ctx->spec.exc;  // sync-free: the remembered answer (checked at the end)
+    if (!spec) {
+      any_unc = read_dev(ctx, pa.subunc) > 0;
+      ctx->probe.exc = ctx->probe.exc || any_unc;
+    }
+    if (any_unc) {
       // explicit lists only for positions with a partner more than 128 positions away
       cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
-      const int64_t nexc = read_i64(ctx, P<int64_t>(ctx->eoff) + M);
+      k_note<<<1, 1, 0, st>>>(P<int64_t>(ctx->eoff) + M, ctr + C_NEXCMAX, nullptr);
+      LAUNCHED(ctx, 1);
+      const int64_t nexc = size_or_cap(ctx, P<int64_t>(ctx->eoff) + M, ctx->spec.nexc,
+                                       ctx->probe.nexc);
       ctx->last_nexc = nexc;
       pa.off = P<int64_t>(ctx->eoff);
+      pa.nexc_cap = nexc;
       ensure(ctx, ctx->exc, sizeof(int32_t) * std::max<int64_t>(nexc, 1));
       pa.exc = P<int32_t>(ctx->exc);
       if (nexc > 0) {
@@ -566,12 +637,16 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ta.finstart = P<int32_t>(ctx->finstart);
       ta.fin_rec = P<FinRec>(ctx->finrec);
       ta.mF = P<ulonglong2>(ctx->maskF);
-      unsigned int hw = 0;
-      CK(cudaMemcpyAsync(&hw, wmax, sizeof hw, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      while (R <= (int)hw) R <<= 1;
-      ctx->max_window = std::max(ctx->max_window, (int)hw);
-      ctx->last_wmax = (int)hw;
+      k_note32<<<1, 1, 0, st>>>(wmax, ctr + C_WMAXALL);
+      LAUNCHED(ctx, 1);
+      if (spec) {
+        R = ctx->spec.R;
+      } else {
+        const unsigned hw = read_dev(ctx, wmax);
+        while (R <= (int)hw) R <<= 1;
+        ctx->probe.R = std::max(ctx->probe.R, R);
+        ctx->last_wmax = (int)hw;
+      }
       has_exc = true;
       ctx->last_has_exc = true;
       ta.pm = P<int4>(ctx->pflag);
@@ -580,9 +655,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ta.exc = P<int32_t>(ctx->exc);
     }
   }
-  if (pt) CK(cudaEventRecord(ctx->ev[4], st));
+  if (ev) CK(cudaEventRecord(ev[3], st));
   // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
-  int grid = tile_grid(nv, G.ts, bs);
+  const int grid0 = tile_grid(nv, G.ts, bs);
+  int grid = grid0;
   if (grid <= 0) {
     (void)cudaGetLastError();
     set_err(ctx, "tile kernel: shared-memory opt-in / occupancy query failed (n=%d, TS=%d, BS=%d)",
@@ -596,22 +672,28 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     if ((size_t)grid * per > budget) grid = std::max<int>(1, (int)(budget / per));
     ensure(ctx, ctx->scratch, (size_t)grid * per);
   }
-  // automatic: about six chunks per CTA; with windows beyond the 128-position masks (long
-  // exception lists, per-position cost growing with the window) six times more, so the few
-  // expensive tiles split finely enough to balance (C5: 14.4 -> 5.3 ms)
-  int64_t auto_target = M * tile_subblocks(G.ts) / ((int64_t)grid * 6) + 1;
-  auto_target = has_exc && ctx->last_wmax > 128 ? std::max<int64_t>(bs, auto_target / 6)
-                                                 : std::max<int64_t>(2 * bs, auto_target);
-  const int target = ctx->chunk_target > 0 ? std::max(ctx->chunk_target, bs) : (int)auto_target;
+  // automatic chunk length (about six chunks per CTA; with windows beyond the 128-position
+  // masks six times more, so the few expensive tiles split finely enough to balance, C5:
+  // 14.4 -> 5.3 ms), decided on the device from this sub-box's pair count and longest window
+  ChunkTarget tg;
+  tg.M = Mdev;
+  tg.wmax = has_exc ? reinterpret_cast<const unsigned*>(ctr + C_WMAX) : nullptr;
+  tg.nsub = tile_subblocks(G.ts);
+  tg.grid = grid0;
+  tg.bs = bs;
+  tg.over = ctx->chunk_target;
   int64_t* caps = P<int64_t>(ctx->ntot);  // reuse: int64 [ntiles+1]
   ensure(ctx, ctx->ntot, sizeof(int64_t) * (std::max<int64_t>(M, G.ntiles) + 1));
   caps = P<int64_t>(ctx->ntot);
   ensure(ctx, ctx->item_off, sizeof(int64_t) * (G.ntiles + 1));
-  launch_item_caps(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), G.ntiles, target, caps, st);
+  launch_item_caps(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), G.ntiles, tg, caps, st);
   LAUNCHED(ctx, 1);
   CK(cudaMemsetAsync(caps + G.ntiles, 0, sizeof(int64_t), st));
   cub_exclusive_sum(ctx, caps, P<int64_t>(ctx->item_off), G.ntiles + 1);
-  const int64_t n_items = read_i64(ctx, P<int64_t>(ctx->item_off) + G.ntiles);
+  const int64_t* NIdev = P<int64_t>(ctx->item_off) + G.ntiles;
+  k_note<<<1, 1, 0, st>>>(NIdev, ctr + C_ITEMSMAX, nullptr);
+  LAUNCHED(ctx, 1);
+  const int64_t n_items = size_or_cap(ctx, NIdev, ctx->spec.items, ctx->probe.items);
   ensure(ctx, ctx->items, sizeof(int4) * n_items);
   ensure(ctx, ctx->items2, sizeof(int4) * n_items);
   ensure(ctx, ctx->item_key, sizeof(uint32_t) * n_items);
@@ -622,10 +704,15 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ensure(ctx, ctx->partial, sizeof(float) * 8 * npix * n_items);
   ensure(ctx, ctx->chunk_stats, sizeof(int4) * n_items);
   launch_chunks(P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), has_exc ? P<int4>(ctx->pflag) : nullptr,
-                P<int64_t>(ctx->item_off), G.ntiles, n_items, target, owner, rank,
+                P<int64_t>(ctx->item_off), G.ntiles, n_items, tg, R, owner, rank,
                 P<int4>(ctx->chunk_stats), P<int4>(ctx->items), P<int4>(ctx->items2),
-                P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), st);
+                P<int32_t>(ctx->item_cnt), P<uint32_t>(ctx->item_key), ctr + C_OVF, st);
   LAUNCHED(ctx, 2);
+  if (spec && n_items > 0) {
+    k_pad_items<<<148, 256, 0, st>>>(P<int4>(ctx->items), P<int4>(ctx->items2),
+                                     P<uint32_t>(ctx->item_key), NIdev, n_items);
+    LAUNCHED(ctx, 1);
+  }
   k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
   LAUNCHED(ctx, 1);
   cub_sort_keys32(ctx, P<uint32_t>(ctx->item_key), P<uint32_t>(ctx->item_key2),
@@ -668,10 +755,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ctx->last_items = (int)n_items;
   ctx->last_grid = grid;
   ctx->last_R = R;
-  if (pt) CK(cudaEventRecord(ctx->ev[7], st));
+  if (ev) CK(cudaEventRecord(ev[4], st));
   launch_tile(nv, ta, grid, st);
   LAUNCHED(ctx, 1);
-  if (pt) CK(cudaEventRecord(ctx->ev[5], st));
+  if (ev) CK(cudaEventRecord(ev[5], st));
   launch_merge(ta, st);
   LAUNCHED(ctx, 1);
   // NEXT-1 (O20): the uncertain positions' interval terms as raw per-pixel sums, for the
@@ -696,16 +783,29 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   }
   (void)tlist;
   (void)n_list;
-  if (pt) {
-    CK(cudaEventSynchronize(ctx->ev[5]));
-    float a = 0, b = 0, c = 0, d = 0, e = 0;
-    CK(cudaEventElapsedTime(&a, ctx->ev[1], ctx->ev[2]));
-    CK(cudaEventElapsedTime(&b, ctx->ev[2], ctx->ev[3]));
-    CK(cudaEventElapsedTime(&c, ctx->ev[3], ctx->ev[4]));
-    CK(cudaEventElapsedTime(&e, ctx->ev[4], ctx->ev[7]));
-    CK(cudaEventElapsedTime(&d, ctx->ev[7], ctx->ev[5]));
+}
+
+// the 6 phase events of the k-th sub-box of a render (pooled)
+cudaEvent_t* sub_events(as_ctx* ctx, int k) {
+  while ((int)ctx->sbev.size() < 6 * (k + 1)) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->sbev.push_back(e);
+  }
+  return ctx->sbev.data() + 6 * k;
+}
+// phase times of n sub-boxes (after the render's synchronisation)
+void collect_phases(as_ctx* ctx, int n, PhaseTimes* pt) {
+  for (int k = 0; k < n; ++k) {
+    cudaEvent_t* e = ctx->sbev.data() + 6 * k;
+    float a = 0, b = 0, c = 0, d = 0, f = 0;
+    CK(cudaEventElapsedTime(&a, e[0], e[1]));
+    CK(cudaEventElapsedTime(&b, e[1], e[2]));
+    CK(cudaEventElapsedTime(&c, e[2], e[3]));
+    CK(cudaEventElapsedTime(&f, e[3], e[4]));
+    CK(cudaEventElapsedTime(&d, e[4], e[5]));
     pt->setup += a;
-    pt->bin += b + e;
+    pt->bin += b + f;
     pt->pairs += c;
     pt->tile += d;
   }
@@ -780,13 +880,18 @@ Geometry geometry(const as_ctx* ctx, int tile) {
   return G;
 }
 
-void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_rendered,
-                int64_t pairs, const PhaseTimes& pt, double total_ms, as_stats* out) {
-  unsigned long long h[C_NCOUNTERS];
-  CK(cudaMemcpyAsync(h, ctx->counters.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+void read_counters(as_ctx* ctx, unsigned long long* h) {
+  CK(cudaMemcpyAsync(h, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
+                     cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+}
+
+void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_rendered,
+                const PhaseTimes& pt, double total_ms, as_stats* out) {
+  unsigned long long h[C_NCOUNTERS];
+  read_counters(ctx, h);
   std::memset(out, 0, sizeof *out);
-  out->pairs = pairs;
+  out->pairs = (int64_t)h[C_PAIRS];
   out->active_pairs = (int64_t)h[C_ACTIVE];
   out->uncertain_pairs = (int64_t)h[C_UNC];
   out->fails = (int64_t)h[C_FAIL];
@@ -805,10 +910,11 @@ void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_r
   out->tile_kernel_ms = pt.tile;
   out->ms_total = total_ms;
   out->device_bytes = ctx->bytes;
-  out->n_items = ctx->last_items;
+  out->n_items = (int32_t)h[C_ITEMSMAX];
   out->grid = ctx->last_grid;
   out->ring_len = ctx->last_R;
-  out->max_window = ctx->max_window;
+  out->max_window = (int32_t)h[C_WMAXALL];
+  out->host_syncs = ctx->host_syncs;
   out->ms_gather = ctx->last_gather_ms;
   out->world = ctx->world;
   out->n_owned = n_tiles_rendered;
@@ -1095,6 +1201,7 @@ as_status as_destroy(as_ctx* ctx) {
   if (ctx->comm && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)ctx->comm);
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+  for (cudaEvent_t e : ctx->sbev) cudaEventDestroy(e);
   delete ctx;
   return AS_OK;
 }
@@ -1540,6 +1647,7 @@ void linear_pass(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int batch, f
   CK(cudaMemcpyAsync(tb.data(), ctx->tbegin.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(te.data(), ctx->tend.p, sizeof(int64_t) * G.ntiles, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  ++ctx->host_syncs;
   std::vector<int32_t> list;
   for (int t = 0; t < G.ntiles; ++t)
     if (te[t] > tb[t]) list.push_back(t);
@@ -1607,7 +1715,7 @@ namespace {
 // union over the sub-boxes [b, e) on this GPU into device images dlo / dhi (identities for an
 // empty range); the single-GPU body of a render
 void render_local(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int32_t batch, int b, int e,
-                  float* dlo, float* dhi, PhaseTimes* pt, int64_t& pairs) {
+                  float* dlo, float* dhi, bool timed) {
   cudaStream_t s = ctx->stream;
   const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
   k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tlist), G.ntiles);
@@ -1622,21 +1730,19 @@ void render_local(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int32_t bat
     ensure(ctx, ctx->tmp_hi, sizeof(float) * img);
   }
   for (int sb = b; sb < e; ++sb) {
-    int64_t M = 0;
+    cudaEvent_t* ev = timed ? sub_events(ctx, sb - b) : nullptr;
     if (!linear) {
       render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                    nullptr, dlo, dhi, sb == b, M, pt);
+                    nullptr, dlo, dhi, sb == b, ev);
     } else {  // intersection per sub-box, then the union (step 22)
       float* tl = P<float>(ctx->tmp_lo);
       float* th = P<float>(ctx->tmp_hi);
       render_subbox(ctx, bi, sb, true, G, batch, nullptr, 0, P<int32_t>(ctx->tlist), G.ntiles,
-                    nullptr, tl, th, true, M, pt);
-      ctx->last_M = M;
+                    nullptr, tl, th, true, ev);
       linear_pass(ctx, bi, G, batch, tl, th);
       launch_union(tl, th, dlo, dhi, (int64_t)img, sb == b, s);
       LAUNCHED(ctx, 1);
     }
-    pairs += M;
   }
 }
 
@@ -1678,72 +1784,104 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
     const Geometry G = geometry(ctx, tile);
-    ctx->launches = 0;
-    ctx->max_window = 0;
-    ctx->last_gather_ms = 0.0;
-    ctx->last_n_owned = G.ntiles;
-    if (stats) CK(cudaEventRecord(ctx->ev[0], s));
-    prepare_common(ctx, bi, G);
+    // Sync-free when this shape's sizes are remembered (single GPU, interval blend, a call
+    // that synchronises at its end anyway): no host read inside the pipeline, one check of
+    // the sizes at the end; if they outgrew the remembered ones the render runs again,
+    // probing (reading each size back), and the new sizes are remembered.
+    as_ctx::Sizes& sp = ctx->spec;
+    const bool can_spec = axis == 0 && ctx->blend_mode == 0 && !(flags & AS_ASYNC);
+    bool spec = can_spec && sp.valid && sp.ts == tile && sp.bs == batch && sp.nv == bi.n_vars;
+    bool resized = false;
     const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
     float *dlo = lo, *dhi = hi;
-    if (!(flags & AS_PTR_DEVICE)) {
-      ensure(ctx, ctx->img_lo, sizeof(float) * img);
-      ensure(ctx, ctx->img_hi, sizeof(float) * img);
-      dlo = P<float>(ctx->img_lo);
-      dhi = P<float>(ctx->img_hi);
-    }
-    PhaseTimes pt;
-    int64_t pairs = 0;
-    int n_done = s1 > s0 ? s1 - s0 : 0;  // sub-boxes rendered by this rank
-    if (axis == 2) {
-      // rank r: contiguous balanced range of [s0, s1); an empty range gives the identities
-      const int ns = s1 - s0, q = ns / world, rm = ns % world;
-      const int b = s0 + rank * q + std::min(rank, rm), e = b + q + (rank < rm ? 1 : 0);
-      n_done = e - b;
-      render_local(ctx, bi, G, batch, b, e, dlo, dhi, stats ? &pt : nullptr, pairs);
-      CK(cudaEventRecord(ctx->ev[3], s));
-      NCK(nccl_api().allReduce(dlo, dlo, img, ncclFloat, ncclMin, (ncclComm_t)ctx->comm, s));
-      NCK(nccl_api().allReduce(dhi, dhi, img, ncclFloat, ncclMax, (ncclComm_t)ctx->comm, s));
-      CK(cudaEventRecord(ctx->ev[4], s));
-    } else if (axis == 1) {
-      // every rank: setup + per-tile costs, the same device LPT owner map, its own tiles
-      // into a compact tile-major buffer, ONE all-gather, the untile on the device
-      const int per = (G.ntiles + world - 1) / world;
-      const int cap = per + std::max(1, per / 4);
-      tile_costs_dev(ctx, bi, G, s0, s1);
-      device_lpt(ctx, G, world, cap);
-      ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
-      k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
-          P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
-          P<int32_t>(ctx->tslot), P<int32_t>(ctx->untile_map));
-      LAUNCHED(ctx, 1);
-      const size_t tm = (size_t)cap * tile * tile * 3;
-      ensure(ctx, ctx->gsend, sizeof(float) * 2 * tm);
-      ensure(ctx, ctx->grecv, sizeof(float) * 2 * tm * world);
-      float* slo = P<float>(ctx->gsend);
-      float* shi = slo + tm;
-      // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
-      k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
-      LAUNCHED(ctx, 1);
-      ctx->last_out_tiles = cap;
-      for (int sb = s0; sb < s1; ++sb) {
-        int64_t M = 0;
-        render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
-                      P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0, M,
-                      stats ? &pt : nullptr);
-        pairs += M;
+    int n_done = 0, n_timed = 0;
+    for (;;) {
+      ctx->spec_on = spec;
+      ctx->probe = as_ctx::Sizes{};
+      ctx->host_syncs = 0;
+      ctx->launches = 0;
+      ctx->last_gather_ms = 0.0;
+      ctx->last_n_owned = G.ntiles;
+      if (stats) CK(cudaEventRecord(ctx->ev[0], s));
+      prepare_common(ctx, bi, G);
+      if (!(flags & AS_PTR_DEVICE)) {
+        ensure(ctx, ctx->img_lo, sizeof(float) * img);
+        ensure(ctx, ctx->img_hi, sizeof(float) * img);
+        dlo = P<float>(ctx->img_lo);
+        dhi = P<float>(ctx->img_hi);
       }
-      CK(cudaEventRecord(ctx->ev[3], s));
-      NCK(nccl_api().allGather(slo, P<float>(ctx->grecv), 2 * tm, ncclFloat,
-                               (ncclComm_t)ctx->comm, s));
-      const float* rl = P<float>(ctx->grecv);
-      launch_untile(rl, rl + tm, P<int32_t>(ctx->untile_map), tile, G.ntx, G.nty, ctx->cam.W,
-                    ctx->cam.H, dlo, dhi, s);
-      LAUNCHED(ctx, 1);
-      CK(cudaEventRecord(ctx->ev[4], s));
-    } else {
-      render_local(ctx, bi, G, batch, s0, s1, dlo, dhi, stats ? &pt : nullptr, pairs);
+      n_done = s1 > s0 ? s1 - s0 : 0;  // sub-boxes rendered by this rank
+      n_timed = n_done;
+      if (axis == 2) {
+        // rank r: contiguous balanced range of [s0, s1); an empty range gives the identities
+        const int ns = s1 - s0, q = ns / world, rm = ns % world;
+        const int b = s0 + rank * q + std::min(rank, rm), e = b + q + (rank < rm ? 1 : 0);
+        n_done = n_timed = e - b;
+        render_local(ctx, bi, G, batch, b, e, dlo, dhi, stats != nullptr);
+        CK(cudaEventRecord(ctx->ev[3], s));
+        NCK(nccl_api().allReduce(dlo, dlo, img, ncclFloat, ncclMin, (ncclComm_t)ctx->comm, s));
+        NCK(nccl_api().allReduce(dhi, dhi, img, ncclFloat, ncclMax, (ncclComm_t)ctx->comm, s));
+        CK(cudaEventRecord(ctx->ev[4], s));
+      } else if (axis == 1) {
+        // every rank: setup + per-tile costs, the same device LPT owner map, its own tiles
+        // into a compact tile-major buffer, ONE all-gather, the untile on the device
+        const int per = (G.ntiles + world - 1) / world;
+        const int cap = per + std::max(1, per / 4);
+        tile_costs_dev(ctx, bi, G, s0, s1);
+        device_lpt(ctx, G, world, cap);
+        ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
+        k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
+            P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
+            P<int32_t>(ctx->tslot), P<int32_t>(ctx->untile_map));
+        LAUNCHED(ctx, 1);
+        const size_t tm = (size_t)cap * tile * tile * 3;
+        ensure(ctx, ctx->gsend, sizeof(float) * 2 * tm);
+        ensure(ctx, ctx->grecv, sizeof(float) * 2 * tm * world);
+        float* slo = P<float>(ctx->gsend);
+        float* shi = slo + tm;
+        // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
+        k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
+        LAUNCHED(ctx, 1);
+        ctx->last_out_tiles = cap;
+        for (int sb = s0; sb < s1; ++sb)
+          render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
+                        P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0,
+                        stats ? sub_events(ctx, sb - s0) : nullptr);
+        CK(cudaEventRecord(ctx->ev[3], s));
+        NCK(nccl_api().allGather(slo, P<float>(ctx->grecv), 2 * tm, ncclFloat,
+                                 (ncclComm_t)ctx->comm, s));
+        const float* rl = P<float>(ctx->grecv);
+        launch_untile(rl, rl + tm, P<int32_t>(ctx->untile_map), tile, G.ntx, G.nty, ctx->cam.W,
+                      ctx->cam.H, dlo, dhi, s);
+        LAUNCHED(ctx, 1);
+        CK(cudaEventRecord(ctx->ev[4], s));
+      } else {
+        render_local(ctx, bi, G, batch, s0, s1, dlo, dhi, stats != nullptr);
+      }
+      if (spec) {  // the one check of a sync-free render
+        unsigned long long h[C_NCOUNTERS];
+        read_counters(ctx, h);
+        const bool fits = h[C_OVF] == 0 && (int64_t)h[C_MMAX] <= sp.M &&
+                          (h[C_UNC] == 0 || sp.exc) && (int64_t)h[C_NEXCMAX] <= sp.nexc &&
+                          (int64_t)h[C_WMAXALL] < sp.R && (int64_t)h[C_ITEMSMAX] <= sp.items;
+        if (!fits) {
+          sp.valid = false;
+          spec = false;
+          resized = true;
+          ++ctx->spec_redo;
+          continue;
+        }
+        if (2 * (int64_t)h[C_MMAX] < sp.M) sp.valid = false;  // far smaller: re-probe next time
+      } else if (can_spec) {
+        sp = ctx->probe;
+        sp.valid = true;
+        sp.ts = tile;
+        sp.bs = batch;
+        sp.nv = bi.n_vars;
+      }
+      break;
     }
+    ctx->spec_on = false;
     if (!(flags & AS_PTR_DEVICE)) {
       CK(cudaMemcpyAsync(lo, dlo, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(hi, dhi, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
@@ -1763,13 +1901,17 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
         CK(cudaMemcpy(&no, P<int32_t>(ctx->nown) + rank, sizeof no, cudaMemcpyDeviceToHost));
         ctx->last_n_owned = no;
       }
+      PhaseTimes pt;
+      collect_phases(ctx, n_timed, &pt);
       BoxInfo br = bi;
       br.n_sub = n_done;
-      fill_stats(ctx, br, G, ctx->last_n_owned, pairs, pt, tot, stats);
+      fill_stats(ctx, br, G, ctx->last_n_owned, pt, tot, stats);
+      stats->resized = resized ? 1 : 0;
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;
   } catch (const Err& e) {
+    ctx->spec_on = false;
     return e.st;
   }
 }
@@ -1842,7 +1984,8 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       return AS_E_ARG;
     }
     ctx->launches = 0;
-    ctx->max_window = 0;
+    ctx->host_syncs = 0;
+    ctx->spec_on = false;  // probing: this entry point reads every size back
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
     // ---- owner map (identical on every rank): LPT over per-tile pair counts, on the device
@@ -1868,16 +2011,12 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       dlo = P<float>(ctx->img_lo);
       dhi = P<float>(ctx->img_hi);
     }
-    PhaseTimes pt;
-    int64_t pairs = 0;
     ctx->last_out_tiles = max_tiles;
     for (int sb = 0; sb < bi.n_sub; ++sb) {
-      int64_t M = 0;
       const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0
       render_subbox(ctx, bi, sb, need_setup, G, batch, P<int32_t>(ctx->owner), rank,
-                    P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0, M,
-                    stats ? &pt : nullptr);
-      pairs += M;
+                    P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0,
+                    stats ? sub_events(ctx, sb) : nullptr);
     }
     // the owned tile ids (host output): the owner map comes back once the render is queued
     std::vector<int32_t> own(G.ntiles);
@@ -1903,7 +2042,9 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       CK(cudaEventSynchronize(ctx->ev[6]));
       float tot = 0;
       CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
-      fill_stats(ctx, bi, G, nm, pairs, pt, tot, stats);
+      PhaseTimes pt;
+      collect_phases(ctx, bi.n_sub, &pt);
+      fill_stats(ctx, bi, G, nm, pt, tot, stats);
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;

@@ -270,18 +270,22 @@ struct BinArgs {
   uint32_t* keys;        // [M] tile id
   int32_t* vals;         // [M] Gaussian index
   unsigned long long* tile_cost;  // [ntiles] or nullptr
+  int64_t cap;           // room in keys / vals: pairs beyond it are not written (the caller
+                         // detects the overflow from offsets[N] and renders again)
 };
 void launch_count(const BinArgs& a, cudaStream_t st);
 void launch_emit(const BinArgs& a, cudaStream_t st);
+// keys >= ntiles are padding (sorted last) and ignored
 void launch_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin, int64_t* end,
                    cudaStream_t st);
 
 struct PairArgs {
-  const uint32_t* keys;   // [M] sorted tile ids
+  const uint32_t* keys;   // [M] sorted tile ids; ids >= ntiles are padding positions (empty)
   const int32_t* vals;    // [M] Gaussian ids
   const int64_t* tbegin;  // [ntiles]
   const int64_t* tend;
-  int64_t M;
+  int64_t M;              // positions, padding included (row stride of posD)
+  int64_t nexc_cap;       // room in exc: lists past it are not written (caller re-renders)
   const void* pair;       // PairRec<NV>[N]
   int nv;
   // slope-aware window (a7): per tile the depth slope model m(kappa) = g0 + kappa h_T
@@ -325,12 +329,24 @@ void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut,
 void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
                    const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
 void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st);
-void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
+// chunk length, decided on the device from the sub-box's own pair count and longest window
+// (so a render sized from remembered capacities cuts exactly the chunks a probed one does):
+// `over` > 0 is as_set_chunk_target's value; otherwise about six chunks per CTA of `grid`,
+// six times finer when a window passes the 128-position masks
+struct ChunkTarget {
+  const int64_t* M;        // device: pairs of this sub-box
+  const unsigned* wmax;    // device: longest exception window, or nullptr (no exceptions)
+  int nsub, grid, bs, over;
+};
+void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, ChunkTarget tg,
                       int64_t* caps, cudaStream_t st);
+// items beyond n_items (room) are not written and a ring longer than R is clamped: both set
+// *ovf, and the caller renders again with larger buffers
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                   const int64_t* item_off, int ntiles, int64_t n_items, int target,
+                   const int64_t* item_off, int ntiles, int64_t n_items, ChunkTarget tg, int R,
                    const int32_t* owner, int rank, int4* stats, int4* items, int4* items2,
-                   int32_t* item_cnt, uint32_t* item_key, cudaStream_t st);
+                   int32_t* item_cnt, uint32_t* item_key, unsigned long long* ovf,
+                   cudaStream_t st);
 
 struct TileArgs {
   const void* hot;            // HotRec<NV>[N]

@@ -74,8 +74,10 @@ __global__ void k_bin(BinArgs A) {
           continue;
         }
         if (EMIT) {
-          A.keys[out] = (uint32_t)tile;
-          A.vals[out] = g;
+          if (out < A.cap) {
+            A.keys[out] = (uint32_t)tile;
+            A.vals[out] = g;
+          }
           ++out;
         } else if (A.tile_cost) {
           atomicAdd(&A.tile_cost[tile], 1ull);
@@ -113,10 +115,12 @@ void launch_emit(const BinArgs& a, cudaStream_t st) {
   NV_SWITCH(a.nv, (k_bin<NVc, true><<<blocks, 128, 0, st>>>(a)));
 }
 
-__global__ void k_ranges(const uint32_t* keys, int64_t M, int64_t* begin, int64_t* end) {
+__global__ void k_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin,
+                         int64_t* end) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= M) return;
   const uint32_t t = keys[p];
+  if (t >= (uint32_t)ntiles) return;  // padding
   if (p == 0 || keys[p - 1] != t) begin[t] = p;
   if (p == M - 1 || keys[p + 1] != t) end[t] = p + 1;
 }
@@ -125,7 +129,7 @@ void launch_ranges(const uint32_t* keys, int64_t M, int ntiles, int64_t* begin, 
   cudaMemsetAsync(begin, 0, sizeof(int64_t) * ntiles, st);
   cudaMemsetAsync(end, 0, sizeof(int64_t) * ntiles, st);
   if (M <= 0) return;
-  k_ranges<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(keys, M, begin, end);
+  k_ranges<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(keys, M, ntiles, begin, end);
 }
 
 // ------------------------------------------------------------------------- pairs (a7)
@@ -232,11 +236,12 @@ __device__ __forceinline__ void warp_max_u32(unsigned* dst, unsigned v) {
 template <int NV>
 __global__ void k_pairs_prep(PairArgs A) {
   const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = p0 < A.M;
-  const int64_t p = live ? p0 : A.M - 1;  // dead lanes mirror the last position (no writes)
+  const int64_t p = p0 < A.M ? p0 : A.M - 1;  // dead lanes mirror the last position (no writes)
   const uint32_t t = A.keys[p];
+  const bool pad = t >= (uint32_t)A.ntiles;  // padding position: arithmetic on tile 0, no writes
+  const bool live = p0 < A.M && !pad;
   const PairRec<NV> Pi = load_pair<NV>(A.pair, A.vals[p]);
-  const double* h = A.tileh + (size_t)t * (NVMAX + 1);
+  const double* h = A.tileh + (size_t)(pad ? 0u : t) * (NVMAX + 1);
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -311,8 +316,21 @@ __global__ void k_pairs(PairArgs A) {
     if (A.ntot[p] == 0) return;  // not an overflow position
     off = A.off[p];
     nFt = A.nF[p];
+    if (off + A.ntot[p] > A.nexc_cap) return;  // no room: the caller renders again
   }
   const uint32_t t = A.keys[p];
+  if (t >= (uint32_t)A.ntiles) {  // padding position: no partners
+    if (PASS == 0) {
+      A.nF[p] = 0;
+      A.nG[p] = 0;
+      A.hpos[p] = 0;
+      A.gpos[p] = 0;
+      A.ntot[p] = 0;
+      A.mF[p] = make_ulonglong2(0ull, 0ull);
+      A.mG[p] = make_ulonglong2(0ull, 0ull);
+    }
+    return;
+  }
   const int64_t b = A.tbegin[t], e = A.tend[t];
   const int32_t gi = A.vals[p];
   const DForm<NV> Pi = load_posd<NV>(A.posD, A.M, p);
@@ -434,6 +452,12 @@ __global__ void k_meta(PairArgs A, const int32_t* cstore, const int32_t* ccut,
                        int32_t* finval) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
+  if (A.keys[p] >= (uint32_t)A.ntiles) {  // padding position
+    pm[p] = make_int4(0, 0, 0, 0);
+    finkey[p] = (uint32_t)A.M;
+    finval[p] = (int32_t)p;
+    return;
+  }
   const int nF = A.nF[p], nG = A.nG[p];
   const int64_t b = A.tbegin[A.keys[p]];
   const int loc = (int)(p - b);
@@ -519,25 +543,34 @@ void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t 
 // [A_k, L_k) for any chunk length).  One warp per tile.
 //   items[i]  = {tile, s, e, flags | log2(ring length) << 8}
 //   items2[i] = {A, L, A_next, 0}
-__global__ void k_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
-                            int64_t* caps) {
+__device__ __forceinline__ int chunk_target(const ChunkTarget& g) {
+  if (g.over > 0) return max(g.over, g.bs);
+  const int64_t t = *g.M * g.nsub / ((int64_t)g.grid * 6) + 1;
+  if (g.wmax && *g.wmax > 128u) return (int)(t / 6 > g.bs ? t / 6 : (int64_t)g.bs);
+  const int64_t u = t > 2 * (int64_t)g.bs ? t : 2 * (int64_t)g.bs;
+  return (int)(u < (1 << 30) ? u : (1 << 30));
+}
+__global__ void k_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles,
+                            ChunkTarget tg, int64_t* caps) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
+  const int target = chunk_target(tg);
   const int64_t K = tend[t] - tbegin[t];
   caps[t] = K > 0 ? (K + target - 1) / target : 1;
 }
-void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, int target,
+void launch_item_caps(const int64_t* tbegin, const int64_t* tend, int ntiles, ChunkTarget tg,
                       int64_t* caps, cudaStream_t st) {
-  k_item_caps<<<(ntiles + 255) / 256, 256, 0, st>>>(tbegin, tend, ntiles, target, caps);
+  k_item_caps<<<(ntiles + 255) / 256, 256, 0, st>>>(tbegin, tend, ntiles, tg, caps);
 }
 // Chunk statistics in parallel (warp per work item): the lookback / lookahead margins a, l
 // of the chunk's exception windows, its longest window and whether it has any exception.
 __global__ void k_chunk_stats(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                              const int64_t* item_off, int ntiles, int64_t n_items, int target,
-                              const int32_t* owner, int rank, int4* stats) {
+                              const int64_t* item_off, int ntiles, int64_t n_items,
+                              ChunkTarget tg, const int32_t* owner, int rank, int4* stats) {
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= n_items) return;
+  const int target = chunk_target(tg);
   int lo = 0, hi = ntiles - 1;  // tile t with item_off[t] <= j < item_off[t + 1]
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -573,16 +606,23 @@ __global__ void k_chunk_stats(const int64_t* tbegin, const int64_t* tend, const 
 }
 // per tile, back to front (A_next known, scan starts non-decreasing): the work items
 __global__ void k_chunk_items(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                              const int64_t* item_off, int ntiles, int target,
-                              const int32_t* owner, int rank, const int4* stats, int4* items,
-                              int4* items2, int32_t* item_cnt, uint32_t* item_key) {
+                              const int64_t* item_off, int ntiles, int64_t n_items,
+                              ChunkTarget tg, int R, const int32_t* owner, int rank,
+                              const int4* stats, int4* items, int4* items2, int32_t* item_cnt,
+                              uint32_t* item_key, unsigned long long* ovf) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
+  const int target = chunk_target(tg);
   const int K = (int)(tend[t] - tbegin[t]);
   const int64_t o = item_off[t];
   const int64_t cap = item_off[t + 1] - o;
   const bool mine = owner == nullptr || owner[t] == rank;
   const int n = mine ? (K > 0 ? (K + target - 1) / target : 1) : 0;
+  if (o + (cap > n ? cap : (int64_t)n) > n_items) {  // no room for this tile's items
+    atomicOr(ovf, 1ull);
+    item_cnt[t] = 0;
+    return;
+  }
   int prevA = 0;
   for (int k = n - 1; k >= 0; --k) {
     const int s = k * target, e = min(K, s + target);
@@ -591,6 +631,11 @@ __global__ void k_chunk_items(const int64_t* tbegin, const int64_t* tend, const 
     const int L = max(e, st.y);
     int lr = 0;
     while ((1 << lr) <= st.z) ++lr;
+    if ((1 << lr) > R) {  // window longer than the ring: clamped, the caller renders again
+      atomicOr(ovf, 2ull);
+      lr = 0;
+      while ((2 << lr) <= R) ++lr;
+    }
     const int Anext = (k == n - 1) ? e : prevA;
     if (k < n - 1) A = min(A, prevA);
     const int fl = ((pm && st.w) ? IT_EXC : 0) | (n == 1 ? IT_SINGLE : 0) | (lr << 8);
@@ -607,15 +652,16 @@ __global__ void k_chunk_items(const int64_t* tbegin, const int64_t* tend, const 
   item_cnt[t] = n;
 }
 void launch_chunks(const int64_t* tbegin, const int64_t* tend, const int4* pm,
-                   const int64_t* item_off, int ntiles, int64_t n_items, int target,
+                   const int64_t* item_off, int ntiles, int64_t n_items, ChunkTarget tg, int R,
                    const int32_t* owner, int rank, int4* stats, int4* items, int4* items2,
-                   int32_t* item_cnt, uint32_t* item_key, cudaStream_t st) {
+                   int32_t* item_cnt, uint32_t* item_key, unsigned long long* ovf,
+                   cudaStream_t st) {
   if (n_items > 0)
     k_chunk_stats<<<(unsigned)((n_items + 3) / 4), 128, 0, st>>>(
-        tbegin, tend, pm, item_off, ntiles, n_items, target, owner, rank, stats);
-  k_chunk_items<<<(ntiles + 127) / 128, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, target,
-                                                      owner, rank, stats, items, items2, item_cnt,
-                                                      item_key);
+        tbegin, tend, pm, item_off, ntiles, n_items, tg, owner, rank, stats);
+  k_chunk_items<<<(ntiles + 127) / 128, 128, 0, st>>>(tbegin, tend, pm, item_off, ntiles, n_items,
+                                                      tg, R, owner, rank, stats, items, items2,
+                                                      item_cnt, item_key, ovf);
 }
 
 // ------------------------------------------------------------------------- untile (a11)

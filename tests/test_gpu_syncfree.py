@@ -1,0 +1,126 @@
+"""Sync-free renders: a render of a shape whose sizes are remembered
+(tile, batch, box dimension) runs without any blocking host read inside the pipeline — the
+pair count, exception-list length, ring length and work-item count come from the last probed
+render, the buffers are padded on the device and the kernels skip the padding — and checks
+the real sizes once at its end.  These tests pin that:
+
+* the second render of a workload reports host_syncs == 0 and is bit-identical to the first
+  (probed) one and to a fresh context's;
+* a workload that outgrows the remembered sizes (more pairs, longer windows, exceptions where
+  there were none, more work items) is detected, repeated with probing (resized == 1) and
+  still matches the fp64 oracle at 1e-4;
+* multi-sub-box renders (C3 shape) go sync-free too."""
+import numpy as np
+import pytest
+
+from workloads import make_config, stacked_config
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def Context():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_00308_b200 import Context
+    return Context
+
+
+def render(ctx, w, tile=None, batch=None):
+    ctx.load_workload(w)
+    lo, hi, st = ctx.as_render_bounds(tile=tile or w.tile, batch=batch or w.batch)
+    return lo.cpu().numpy(), hi.cpu().numpy(), st
+
+
+def fresh(Context, w, tile=None, batch=None):
+    c = Context(0)
+    try:
+        return render(c, w, tile, batch)
+    finally:
+        c.close()
+
+
+def parity(oracle, w, lo, hi, st, tile=None):
+    olo, ohi, ost = oracle.render_bounds(w, tile=tile or w.tile)
+    err = max(np.abs(lo - olo).max(), np.abs(hi - ohi).max())
+    assert err <= TOL, err
+    for k in ("pairs", "active_pairs", "uncertain_pairs"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
+
+
+@pytest.mark.parametrize("tile,batch", [(16, 24), (8, 32)])
+def test_second_render_is_sync_free_and_identical(Context, oracle, tile, batch):
+    w = stacked_config(N=300, rot_deg=0.5, axis_frac=0.5)
+    ctx = Context(0)
+    try:
+        lo1, hi1, s1 = render(ctx, w, tile, batch)
+        lo2, hi2, s2 = render(ctx, w, tile, batch)
+    finally:
+        ctx.close()
+    assert s1["host_syncs"] > 0 and s1["resized"] == 0
+    assert s2["host_syncs"] == 0 and s2["resized"] == 0
+    assert s2["uncertain_pairs"] > 0
+    assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
+    for k in ("pairs", "active_pairs", "uncertain_pairs", "n_items", "max_window"):
+        assert s1[k] == s2[k], k
+    lo3, hi3, _ = fresh(Context, w, tile, batch)
+    assert np.array_equal(lo2, lo3) and np.array_equal(hi2, hi3)
+    parity(oracle, w, lo2, hi2, s2, tile)
+
+
+def test_growth_is_detected_and_repeated(Context, oracle):
+    small = stacked_config(N=100, rot_deg=0.2)
+    big = stacked_config(N=400, rot_deg=1.0, axis_frac=0.5)  # same box dimension
+    ctx = Context(0)
+    try:
+        render(ctx, small)
+        _, _, s = render(ctx, small)
+        assert s["host_syncs"] == 0
+        lo, hi, sb = render(ctx, big)
+        assert sb["resized"] == 1 and sb["host_syncs"] > 0
+        assert sb["pairs"] > s["pairs"] and sb["max_window"] > s["max_window"]
+        parity(oracle, big, lo, hi, sb)
+        lo2, hi2, sb2 = render(ctx, big)  # remembered now
+        assert sb2["host_syncs"] == 0 and sb2["resized"] == 0
+        assert np.array_equal(lo, lo2) and np.array_equal(hi, hi2)
+        # and back to the smaller workload: fits the remembered sizes (padded buffers)
+        lo3, hi3, s3 = render(ctx, stacked_config(N=300, rot_deg=0.7))
+        assert s3["resized"] == 0
+    finally:
+        ctx.close()
+    w3 = stacked_config(N=300, rot_deg=0.7)
+    flo, fhi, fs = fresh(Context, w3)
+    assert np.array_equal(lo3, flo) and np.array_equal(hi3, fhi)
+    parity(oracle, w3, lo3, hi3, s3)
+
+
+def test_exceptions_appearing_after_an_exception_free_render(Context, oracle):
+    calm = stacked_config(N=200, rot_deg=1e-7, depth_spread=1.0)  # depths far apart: certain
+    ctx = Context(0)
+    try:
+        render(ctx, calm)
+        _, _, s = render(ctx, calm)
+        assert s["host_syncs"] == 0 and s["uncertain_pairs"] == 0 and s["ring_len"] == 1
+        w = stacked_config(N=200, rot_deg=1.0)
+        lo, hi, st = render(ctx, w)
+    finally:
+        ctx.close()
+    assert st["resized"] == 1 and st["uncertain_pairs"] > 0
+    parity(oracle, w, lo, hi, st)
+
+
+def test_multi_subbox_render_is_sync_free(Context, oracle):
+    w = make_config("C3", N=5000, res=56)
+    ctx = Context(0)
+    try:
+        lo1, hi1, s1 = render(ctx, w)
+        lo2, hi2, s2 = render(ctx, w)
+    finally:
+        ctx.close()
+    assert s1["n_sub"] > 1
+    assert s2["host_syncs"] == 0 and s2["resized"] == 0
+    assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
+    assert s2["ms_tile"] > 0 and s2["ms_setup"] > 0
+    parity(oracle, w, lo2, hi2, s2)
