@@ -497,7 +497,7 @@ def run_ours(args):
                                             "straddles", "dropped", "kmax", "ms_setup", "ms_bin",
                                             "ms_pairs", "ms_tile", "device_bytes", "n_items",
                                             "grid", "ring_len", "max_window", "ms_gather",
-                                            "host_syncs", "resized",
+                                            "host_syncs", "resized", "graph_replay", "ms_total",
                                             "world", "n_owned", "peak_bytes")}}
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -122,6 +122,9 @@ typedef struct {
                               same tile / batch / box dimension, checked once at the end) */
   int32_t resized;         /* 1: the sync-free attempt outgrew the remembered sizes and the
                               render was repeated reading each size back (result unaffected) */
+  int32_t graph_replay;    /* 1: the sync-free pipeline ran as one replay of the CUDA graph
+                              captured from an identical earlier render (same sizes, tile, batch,
+                              outputs; no state-changing call in between) */
 } as_stats;
 
 /* Flags */

@@ -103,6 +103,34 @@ struct as_ctx {
   } spec, probe;
   bool spec_on = false;
   int64_t spec_redo = 0;  // renders repeated after a failed verification (stats)
+  // CUDA graph of the sync-free pipeline: captured on the render after a sync-free one that
+  // allocated nothing, replayed while the key holds.  gen counts every state-changing API
+  // call, alloc_gen every (re)allocation; both are part of the key.
+  struct GraphKey {
+    int tile = 0, batch = 0, s0 = 0, s1 = 0;
+    const float* lo = nullptr;
+    const float* hi = nullptr;
+    bool timed = false, exc = false;
+    uint64_t gen = 0, alloc_gen = 0;
+    int64_t M = 0, nexc = 0, items = 0;
+    int R = 0;
+    bool operator==(const GraphKey& o) const {
+      return tile == o.tile && batch == o.batch && s0 == o.s0 && s1 == o.s1 && lo == o.lo &&
+             hi == o.hi && timed == o.timed && exc == o.exc && gen == o.gen &&
+             alloc_gen == o.alloc_gen && M == o.M && nexc == o.nexc && items == o.items &&
+             R == o.R;
+    }
+  } gkey, gready;
+  bool gready_ok = false;
+  cudaGraphExec_t gexec = nullptr;
+  // graphs are captured on / launched into a private non-blocking stream (the caller's may be
+  // the legacy default stream, which cannot be captured), ordered after and before the
+  // caller's stream by two events
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  int64_t glaunches = 0;
+  uint64_t gen = 0, alloc_gen = 0;
+  bool use_graphs = true;
   // per sub-box phase events (collected after the render's single synchronisation)
   std::vector<cudaEvent_t> sbev;
   as_alloc_fn alloc_fn = nullptr;  // as_set_allocator hook (nullptr = cudaMalloc)
@@ -144,6 +172,7 @@ void set_err(as_ctx* c, const char* fmt, ...) {
 
 void free_buf(as_ctx* ctx, DevBuf& b) {
   if (!b.p) return;
+  ++ctx->alloc_gen;
   if (b.free_fn)
     b.free_fn(b.user, b.p, b.cap, ctx->stream);
   else
@@ -171,6 +200,7 @@ void ensure(as_ctx* ctx, DevBuf& b, size_t bytes) {
     CK(cudaMalloc(&b.p, want));
   }
   b.cap = want;
+  ++ctx->alloc_gen;
   ctx->bytes += want;
   ctx->peak_bytes = std::max(ctx->peak_bytes, ctx->bytes);
 }
@@ -401,6 +431,11 @@ __global__ void k_note(const int64_t* v, unsigned long long* mx, unsigned long l
   if (mx) atomicMax(mx, x);
   if (sum) atomicAdd(sum, x);
 }
+// a size past its remembered capacity: flag it (the tile kernels then skip their work)
+__global__ void k_cap_check(const int64_t* v, int64_t cap, unsigned long long* ovf,
+                            unsigned long long bit) {
+  if (*v > cap) atomicOr(ovf, bit);
+}
 __global__ void k_note32(const unsigned* v, unsigned long long* mx) {
   atomicMax(mx, (unsigned long long)*v);
 }
@@ -423,6 +458,17 @@ __global__ void k_pad_items(int4* items, int4* items2, uint32_t* key, const int6
     items2[j] = make_int4(0, 0, 0, 0);
     key[j] = 0;
   }
+}
+
+// a timing event: recorded for real inside a captured graph too (an event record node; a
+// plain record would only mark a capture dependency)
+cudaError_t timing_record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const cudaError_t r = cudaStreamIsCapturing(st, &cs);
+  if (r != cudaSuccess) return r;
+  return cs == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+             : cudaEventRecord(e, st);
 }
 
 // a blocking read of a device value (a host synchronisation inside the pipeline)
@@ -466,12 +512,12 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   // BS is a performance knob: clamp it to what fits in shared memory at this n, and to 128
   // (k_tile's 256-position skip ring covers a batch plus the 128 positions before it)
   bs = tile_batch(nv, G.ts, bs);
-  if (ev) CK(cudaEventRecord(ev[0], st));
+  if (ev) CK(timing_record(ev[0], st));
   if (do_setup) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
     run_setup(ctx, bi, s);
   }
-  if (ev) CK(cudaEventRecord(ev[1], st));
+  if (ev) CK(timing_record(ev[1], st));
   // ---- a6: depth order (stable radix sort by kappa: ties keep ascending index, G6)
   cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
                   P<int32_t>(ctx->kval), P<int32_t>(ctx->order), N, 64);
@@ -499,6 +545,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   k_note<<<1, 1, 0, st>>>(Mdev, ctr + C_MMAX, ctr + C_PAIRS);
   LAUNCHED(ctx, 1);
   const int64_t M = size_or_cap(ctx, Mdev, ctx->spec.M, ctx->probe.M);
+  if (spec) {
+    k_cap_check<<<1, 1, 0, st>>>(Mdev, M, ctr + C_OVF, 4ull);
+    LAUNCHED(ctx, 1);
+  }
   ensure(ctx, ctx->keys, sizeof(uint32_t) * (M + 1));
   ensure(ctx, ctx->keys2, sizeof(uint32_t) * (M + 1));
   ensure(ctx, ctx->vals, sizeof(int32_t) * (M + 1));
@@ -524,7 +574,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   k_tile_max<<<(G.ntiles + 255) / 256, 256, 0, st>>>(P<int64_t>(ctx->tbegin),
                                                      P<int64_t>(ctx->tend), G.ntiles, ctr + C_KMAX);
   LAUNCHED(ctx, 1);
-  if (ev) CK(cudaEventRecord(ev[2], st));
+  if (ev) CK(timing_record(ev[2], st));
   // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
   TileArgs ta{};
   bool has_exc = false;
@@ -594,6 +644,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       LAUNCHED(ctx, 1);
       const int64_t nexc = size_or_cap(ctx, P<int64_t>(ctx->eoff) + M, ctx->spec.nexc,
                                        ctx->probe.nexc);
+      if (spec) {
+        k_cap_check<<<1, 1, 0, st>>>(P<int64_t>(ctx->eoff) + M, nexc, ctr + C_OVF, 8ull);
+        LAUNCHED(ctx, 1);
+      }
       ctx->last_nexc = nexc;
       pa.off = P<int64_t>(ctx->eoff);
       pa.nexc_cap = nexc;
@@ -655,7 +709,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       ta.exc = P<int32_t>(ctx->exc);
     }
   }
-  if (ev) CK(cudaEventRecord(ev[3], st));
+  if (ev) CK(timing_record(ev[3], st));
   // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
   const int grid0 = tile_grid(nv, G.ts, bs);
   int grid = grid0;
@@ -747,6 +801,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ta.hi = hi;
   ta.active = ctr + C_ACTIVE;
   ta.dbg = ctx->debug ? P<unsigned long long>(ctx->dbg) : nullptr;
+  ta.ovf = spec ? ctr + C_OVF : nullptr;
   ta.kver = tile_kernel_version(G.ts);
   ta.M = M;
   ta.nexc = has_exc ? ctx->last_nexc : 0;
@@ -755,10 +810,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ctx->last_items = (int)n_items;
   ctx->last_grid = grid;
   ctx->last_R = R;
-  if (ev) CK(cudaEventRecord(ev[4], st));
+  if (ev) CK(timing_record(ev[4], st));
   launch_tile(nv, ta, grid, st);
   LAUNCHED(ctx, 1);
-  if (ev) CK(cudaEventRecord(ev[5], st));
+  if (ev) CK(timing_record(ev[5], st));
   launch_merge(ta, st);
   LAUNCHED(ctx, 1);
   // NEXT-1 (O20): the uncertain positions' interval terms as raw per-pixel sums, for the
@@ -886,10 +941,15 @@ void read_counters(as_ctx* ctx, unsigned long long* h) {
   CK(cudaStreamSynchronize(ctx->stream));
 }
 
+// hc: the counters when already read after the render (nullptr: read them here)
 void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_rendered,
-                const PhaseTimes& pt, double total_ms, as_stats* out) {
+                const PhaseTimes& pt, double total_ms, as_stats* out,
+                const unsigned long long* hc = nullptr) {
   unsigned long long h[C_NCOUNTERS];
-  read_counters(ctx, h);
+  if (hc)
+    std::memcpy(h, hc, sizeof h);
+  else
+    read_counters(ctx, h);
   std::memset(out, 0, sizeof *out);
   out->pairs = (int64_t)h[C_PAIRS];
   out->active_pairs = (int64_t)h[C_ACTIVE];
@@ -1202,6 +1262,10 @@ as_status as_destroy(as_ctx* ctx) {
   for (int k = 0; k < 8; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   for (cudaEvent_t e : ctx->sbev) cudaEventDestroy(e);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->gev_in) cudaEventDestroy(ctx->gev_in);
+  if (ctx->gev_out) cudaEventDestroy(ctx->gev_out);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   delete ctx;
   return AS_OK;
 }
@@ -1218,6 +1282,7 @@ as_status as_nccl_id(uint8_t id[128]) {
 }
 
 as_status as_comm_init(as_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (!id || world < 1 || world > 128 || rank < 0 || rank >= world) {
     set_err(ctx, "as_comm_init: bad arguments (rank %d, world %d)", rank, world);
@@ -1250,6 +1315,7 @@ as_status as_comm_init(as_ctx* ctx, int32_t rank, int32_t world, const uint8_t i
 }
 
 as_status as_set_shard_axis(as_ctx* ctx, int32_t axis) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (axis < 0 || axis > 2) {
     set_err(ctx, "as_set_shard_axis: axis must be 0 (auto), 1 (tiles) or 2 (sub-boxes)");
@@ -1260,6 +1326,7 @@ as_status as_set_shard_axis(as_ctx* ctx, int32_t axis) {
 }
 
 as_status as_debug_counters(as_ctx* ctx, int32_t enable, uint64_t* out) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   try {
     cudaSetDevice(ctx->device);
@@ -1279,6 +1346,7 @@ as_status as_debug_counters(as_ctx* ctx, int32_t enable, uint64_t* out) {
 }
 
 as_status as_set_allocator(as_ctx* ctx, as_alloc_fn alloc, as_free_fn free_fn, void* user) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if ((alloc == nullptr) != (free_fn == nullptr)) {
     set_err(ctx, "as_set_allocator: alloc and free must both be set or both be NULL");
@@ -1313,6 +1381,7 @@ __global__ void k_validate(int64_t N, const float* m, const float* c, const floa
 
 as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* chol,
                         const float* opacity, const float* color, int32_t flags) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (N < 0 || (N > 0 && (!mean || !chol || !opacity || !color))) {
     set_err(ctx, "as_load_scene: bad arguments");
@@ -1378,6 +1447,7 @@ as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* 
 }
 
 as_status as_set_camera(as_ctx* ctx, const as_camera* cam) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (!cam || cam->W <= 0 || cam->H <= 0 || cam->W > 65536 || cam->H > 65536 ||
       !(cam->fx > 0) || !(cam->fy > 0) || !std::isfinite(cam->cx) || !std::isfinite(cam->cy)) {
@@ -1395,6 +1465,7 @@ as_status as_set_camera(as_ctx* ctx, const as_camera* cam) {
 }
 
 as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (n < 0 || (n > 0 && !bounds) || n > 1000000) {
     set_err(ctx, "as_set_subboxes: bad arguments (n = %d)", n);
@@ -1427,6 +1498,7 @@ as_status as_set_subboxes(as_ctx* ctx, int32_t n, const double* bounds) {
 }
 
 as_status as_set_blend(as_ctx* ctx, int32_t mode) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (mode != 0 && mode != 1) {
     set_err(ctx, "as_set_blend: mode 0 (interval) or 1 (interval + linear)");
@@ -1437,6 +1509,7 @@ as_status as_set_blend(as_ctx* ctx, int32_t mode) {
 }
 
 as_status as_set_chunk_target(as_ctx* ctx, int32_t target) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (target < 0) {
     set_err(ctx, "as_set_chunk_target: target >= 0 (0 = automatic), got %d", target);
@@ -1447,6 +1520,7 @@ as_status as_set_chunk_target(as_ctx* ctx, int32_t target) {
 }
 
 as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (backward != 0 && backward != 1) {
     set_err(ctx, "as_set_inverse_mode: 0 (forward) or 1 (back-substitution)");
@@ -1461,6 +1535,7 @@ as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward) {
 }
 
 as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (!std::isfinite(k_tol) || (k_tol > 0 && (k_max < 8 || k_max > 64))) {
     set_err(ctx, "as_set_matrixinv: k_tol finite, k_max in [8, 64] (got %g, %d)", k_tol, k_max);
@@ -1476,6 +1551,7 @@ as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max) {
 }
 
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   BoxInfo bi;
@@ -1504,6 +1580,7 @@ as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails) {
 }
 
 as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (!box) {
     set_err(ctx, "as_set_pose_box: NULL");
@@ -1533,6 +1610,7 @@ as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box) {
 }
 
 as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   if (!ctx) return AS_E_ARG;
   if (ctx->N < 0) {
     set_err(ctx, "as_set_scene_box before as_load_scene");
@@ -1795,72 +1873,173 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
     const size_t img = (size_t)ctx->cam.W * ctx->cam.H * 3;
     float *dlo = lo, *dhi = hi;
     int n_done = 0, n_timed = 0;
+    if (!(flags & AS_PTR_DEVICE)) {
+      ensure(ctx, ctx->img_lo, sizeof(float) * img);
+      ensure(ctx, ctx->img_hi, sizeof(float) * img);
+      dlo = P<float>(ctx->img_lo);
+      dhi = P<float>(ctx->img_hi);
+    }
+    bool replayed = false;
+    unsigned long long hfinal[C_NCOUNTERS];
+    bool have_h = false;
     for (;;) {
+      have_h = false;
       ctx->spec_on = spec;
       ctx->probe = as_ctx::Sizes{};
       ctx->host_syncs = 0;
       ctx->launches = 0;
       ctx->last_gather_ms = 0.0;
       ctx->last_n_owned = G.ntiles;
-      if (stats) CK(cudaEventRecord(ctx->ev[0], s));
-      prepare_common(ctx, bi, G);
-      if (!(flags & AS_PTR_DEVICE)) {
-        ensure(ctx, ctx->img_lo, sizeof(float) * img);
-        ensure(ctx, ctx->img_hi, sizeof(float) * img);
-        dlo = P<float>(ctx->img_lo);
-        dhi = P<float>(ctx->img_hi);
+      // the whole pipeline, enqueued on the stream (captured into a graph when sync-free)
+      auto enqueue = [&]() {
+        if (stats) CK(timing_record(ctx->ev[0], s));
+        prepare_common(ctx, bi, G);
+        n_done = s1 > s0 ? s1 - s0 : 0;  // sub-boxes rendered by this rank
+        n_timed = n_done;
+        if (axis == 2) {
+          // rank r: contiguous balanced range of [s0, s1); an empty range gives the identities
+          const int ns = s1 - s0, q = ns / world, rm = ns % world;
+          const int b = s0 + rank * q + std::min(rank, rm), e = b + q + (rank < rm ? 1 : 0);
+          n_done = n_timed = e - b;
+          render_local(ctx, bi, G, batch, b, e, dlo, dhi, stats != nullptr);
+          CK(timing_record(ctx->ev[3], s));
+          NCK(nccl_api().allReduce(dlo, dlo, img, ncclFloat, ncclMin, (ncclComm_t)ctx->comm, s));
+          NCK(nccl_api().allReduce(dhi, dhi, img, ncclFloat, ncclMax, (ncclComm_t)ctx->comm, s));
+          CK(timing_record(ctx->ev[4], s));
+        } else if (axis == 1) {
+          // every rank: setup + per-tile costs, the same device LPT owner map, its own tiles
+          // into a compact tile-major buffer, ONE all-gather, the untile on the device
+          const int per = (G.ntiles + world - 1) / world;
+          const int cap = per + std::max(1, per / 4);
+          tile_costs_dev(ctx, bi, G, s0, s1);
+          device_lpt(ctx, G, world, cap);
+          ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
+          k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
+              P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
+              P<int32_t>(ctx->tslot), P<int32_t>(ctx->untile_map));
+          LAUNCHED(ctx, 1);
+          const size_t tm = (size_t)cap * tile * tile * 3;
+          ensure(ctx, ctx->gsend, sizeof(float) * 2 * tm);
+          ensure(ctx, ctx->grecv, sizeof(float) * 2 * tm * world);
+          float* slo = P<float>(ctx->gsend);
+          float* shi = slo + tm;
+          // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
+          k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
+          LAUNCHED(ctx, 1);
+          ctx->last_out_tiles = cap;
+          for (int sb = s0; sb < s1; ++sb)
+            render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
+                          P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0,
+                          stats ? sub_events(ctx, sb - s0) : nullptr);
+          CK(timing_record(ctx->ev[3], s));
+          NCK(nccl_api().allGather(slo, P<float>(ctx->grecv), 2 * tm, ncclFloat,
+                                   (ncclComm_t)ctx->comm, s));
+          const float* rl = P<float>(ctx->grecv);
+          launch_untile(rl, rl + tm, P<int32_t>(ctx->untile_map), tile, G.ntx, G.nty, ctx->cam.W,
+                        ctx->cam.H, dlo, dhi, s);
+          LAUNCHED(ctx, 1);
+          CK(timing_record(ctx->ev[4], s));
+        } else {
+          render_local(ctx, bi, G, batch, s0, s1, dlo, dhi, stats != nullptr);
+        }
+      };
+      auto key = [&]() {
+        as_ctx::GraphKey k;
+        k.tile = tile;
+        k.batch = batch;
+        k.s0 = s0;
+        k.s1 = s1;
+        k.lo = dlo;
+        k.hi = dhi;
+        k.timed = stats != nullptr;
+        k.exc = sp.exc;
+        k.gen = ctx->gen;
+        k.alloc_gen = ctx->alloc_gen;
+        k.M = sp.M;
+        k.nexc = sp.nexc;
+        k.items = sp.items;
+        k.R = sp.R;
+        return k;
+      };
+      bool done = false;
+      replayed = false;
+      if (spec && ctx->use_graphs) {
+        const as_ctx::GraphKey k = key();
+        auto launch_graph = [&]() {  // the graph between two events of the caller's stream
+          CK(cudaEventRecord(ctx->gev_in, s));
+          CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev_in, 0));
+          CK(cudaGraphLaunch(ctx->gexec, ctx->gstream));
+          CK(cudaEventRecord(ctx->gev_out, ctx->gstream));
+          CK(cudaStreamWaitEvent(s, ctx->gev_out, 0));
+        };
+        if (ctx->gexec && ctx->gkey == k) {  // replay
+          n_done = n_timed = s1 > s0 ? s1 - s0 : 0;
+          launch_graph();
+          ctx->launches = ctx->glaunches;
+          done = replayed = true;
+        } else if (ctx->gready_ok && ctx->gready == k) {
+          // the last render of this key ran sync-free and allocated nothing: capture it
+          if (ctx->gexec) {
+            cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+          }
+          if (!ctx->gstream) {
+            CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ctx->gev_in, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->gev_out, cudaEventDisableTiming));
+          }
+          cudaGraph_t g = nullptr;
+          const cudaStream_t user = s;
+          s = ctx->stream = ctx->gstream;  // everything below enqueues on the capture stream
+          try {
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+            try {
+              enqueue();
+            } catch (...) {
+              cudaStreamEndCapture(s, &g);
+              if (g) cudaGraphDestroy(g);
+              throw;
+            }
+            CK(cudaStreamEndCapture(s, &g));
+          } catch (...) {
+            s = ctx->stream = user;
+            throw;
+          }
+          s = ctx->stream = user;
+          if (ctx->alloc_gen == k.alloc_gen &&
+              cudaGraphInstantiate(&ctx->gexec, g, 0ull) != cudaSuccess) {
+            (void)cudaGetLastError();
+            ctx->gexec = nullptr;
+          }
+          cudaGraphDestroy(g);
+          ctx->gready_ok = false;
+          if (ctx->gexec) {
+            ctx->gkey = k;
+            ctx->glaunches = ctx->launches;
+            launch_graph();
+            done = replayed = true;
+          } else {  // not capturable this time: plain sync-free launches
+            ctx->launches = 0;
+            enqueue();
+            done = true;
+          }
+        }
       }
-      n_done = s1 > s0 ? s1 - s0 : 0;  // sub-boxes rendered by this rank
-      n_timed = n_done;
-      if (axis == 2) {
-        // rank r: contiguous balanced range of [s0, s1); an empty range gives the identities
-        const int ns = s1 - s0, q = ns / world, rm = ns % world;
-        const int b = s0 + rank * q + std::min(rank, rm), e = b + q + (rank < rm ? 1 : 0);
-        n_done = n_timed = e - b;
-        render_local(ctx, bi, G, batch, b, e, dlo, dhi, stats != nullptr);
-        CK(cudaEventRecord(ctx->ev[3], s));
-        NCK(nccl_api().allReduce(dlo, dlo, img, ncclFloat, ncclMin, (ncclComm_t)ctx->comm, s));
-        NCK(nccl_api().allReduce(dhi, dhi, img, ncclFloat, ncclMax, (ncclComm_t)ctx->comm, s));
-        CK(cudaEventRecord(ctx->ev[4], s));
-      } else if (axis == 1) {
-        // every rank: setup + per-tile costs, the same device LPT owner map, its own tiles
-        // into a compact tile-major buffer, ONE all-gather, the untile on the device
-        const int per = (G.ntiles + world - 1) / world;
-        const int cap = per + std::max(1, per / 4);
-        tile_costs_dev(ctx, bi, G, s0, s1);
-        device_lpt(ctx, G, world, cap);
-        ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
-        k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
-            P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
-            P<int32_t>(ctx->tslot), P<int32_t>(ctx->untile_map));
-        LAUNCHED(ctx, 1);
-        const size_t tm = (size_t)cap * tile * tile * 3;
-        ensure(ctx, ctx->gsend, sizeof(float) * 2 * tm);
-        ensure(ctx, ctx->grecv, sizeof(float) * 2 * tm * world);
-        float* slo = P<float>(ctx->gsend);
-        float* shi = slo + tm;
-        // tiles a rank owns but that no Gaussian touches are never written by the tile kernel
-        k_fill2<<<(unsigned)((2 * tm + 255) / 256), 256, 0, s>>>(slo, 0.f, shi, 0.f, (int64_t)tm);
-        LAUNCHED(ctx, 1);
-        ctx->last_out_tiles = cap;
-        for (int sb = s0; sb < s1; ++sb)
-          render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
-                        P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0,
-                        stats ? sub_events(ctx, sb - s0) : nullptr);
-        CK(cudaEventRecord(ctx->ev[3], s));
-        NCK(nccl_api().allGather(slo, P<float>(ctx->grecv), 2 * tm, ncclFloat,
-                                 (ncclComm_t)ctx->comm, s));
-        const float* rl = P<float>(ctx->grecv);
-        launch_untile(rl, rl + tm, P<int32_t>(ctx->untile_map), tile, G.ntx, G.nty, ctx->cam.W,
-                      ctx->cam.H, dlo, dhi, s);
-        LAUNCHED(ctx, 1);
-        CK(cudaEventRecord(ctx->ev[4], s));
-      } else {
-        render_local(ctx, bi, G, batch, s0, s1, dlo, dhi, stats != nullptr);
+      if (!done) {
+        const uint64_t ag = ctx->alloc_gen;
+        enqueue();
+        ctx->gready_ok = spec && ctx->alloc_gen == ag;
+        if (ctx->gready_ok) ctx->gready = key();
       }
+      if (!(flags & AS_PTR_DEVICE)) {  // queued before the check: one synchronisation for both
+        CK(cudaMemcpyAsync(lo, dlo, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hi, dhi, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
+      }
+      if (stats) CK(cudaEventRecord(ctx->ev[6], s));
       if (spec) {  // the one check of a sync-free render
-        unsigned long long h[C_NCOUNTERS];
+        unsigned long long* h = hfinal;
         read_counters(ctx, h);
+        have_h = true;
         const bool fits = h[C_OVF] == 0 && (int64_t)h[C_MMAX] <= sp.M &&
                           (h[C_UNC] == 0 || sp.exc) && (int64_t)h[C_NEXCMAX] <= sp.nexc &&
                           (int64_t)h[C_WMAXALL] < sp.R && (int64_t)h[C_ITEMSMAX] <= sp.items;
@@ -1882,12 +2061,7 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       break;
     }
     ctx->spec_on = false;
-    if (!(flags & AS_PTR_DEVICE)) {
-      CK(cudaMemcpyAsync(lo, dlo, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(hi, dhi, sizeof(float) * img, cudaMemcpyDeviceToHost, s));
-    }
     if (stats) {
-      CK(cudaEventRecord(ctx->ev[6], s));
       CK(cudaEventSynchronize(ctx->ev[6]));
       float tot = 0;
       CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
@@ -1905,8 +2079,9 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
       collect_phases(ctx, n_timed, &pt);
       BoxInfo br = bi;
       br.n_sub = n_done;
-      fill_stats(ctx, br, G, ctx->last_n_owned, pt, tot, stats);
+      fill_stats(ctx, br, G, ctx->last_n_owned, pt, tot, stats, have_h ? hfinal : nullptr);
       stats->resized = resized ? 1 : 0;
+      stats->graph_replay = replayed ? 1 : 0;
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;
@@ -1927,6 +2102,7 @@ as_status as_lpt_assign(int32_t n_tiles, const int64_t* costs, int32_t world, in
 
 as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_tiles,
                          int32_t* owner, int64_t* costs) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   BoxInfo bi;
@@ -1962,6 +2138,7 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
 as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank, int32_t world,
                           float* lo_tm, float* hi_tm, int32_t max_tiles, int32_t* owned,
                           int32_t* n_owned, int32_t flags, as_stats* stats) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   BoxInfo bi;
@@ -2056,6 +2233,7 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
 as_status as_untile(as_ctx* ctx, int32_t W, int32_t H, int32_t tile, int32_t world,
                     int32_t max_tiles, const int32_t* owned, const int32_t* n_owned,
                     const float* lo_tm, const float* hi_tm, float* lo, float* hi, int32_t flags) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   const bool dev = flags & AS_PTR_DEVICE;
   if (dev && !ctx) return AS_E_ARG;
   if ((tile != 8 && tile != 16 && tile != 32) || W <= 0 || H <= 0 || world < 1 ||
@@ -2118,6 +2296,7 @@ as_status as_untile(as_ctx* ctx, int32_t W, int32_t H, int32_t tile, int32_t wor
 }
 
 as_status as_render_concrete(as_ctx* ctx, const double* xi, float* img, int32_t flags) {
+  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   BoxInfo bi;

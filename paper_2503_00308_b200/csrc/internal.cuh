@@ -391,6 +391,9 @@ struct TileArgs {
   // NEXT-1 (reading O20): 1 = sum the interval terms of the uncertain positions only (E_F or
   // E_G non-empty) and write the raw sums (no +- N tau, no clamp) -- the linear blend adds them
   int unc_only;
+  // sync-free renders: set on the device when a size outgrew its remembered capacity; the
+  // tile kernels and the merge then do nothing (the render is repeated) -- nullptr: never
+  const unsigned long long* ovf;
 };
 // rare-path counters of the tile kernel (as_debug_counters): evidence that every slow path
 // of the exception machinery runs in some parity case

@@ -620,6 +620,11 @@ __global__ void k_chunk_items(const int64_t* tbegin, const int64_t* tend, const 
   const int n = mine ? (K > 0 ? (K + target - 1) / target : 1) : 0;
   if (o + (cap > n ? cap : (int64_t)n) > n_items) {  // no room for this tile's items
     atomicOr(ovf, 1ull);
+    for (int64_t j = o; j < n_items; ++j) {  // its slots inside the buffer: empty
+      items[j] = make_int4(-1, 0, 0, 0);
+      items2[j] = make_int4(0, 0, 0, 0);
+      item_key[j] = 0;
+    }
     item_cnt[t] = 0;
     return;
   }

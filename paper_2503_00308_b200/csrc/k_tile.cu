@@ -379,6 +379,7 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
 
 template <int NV, int BX>
 __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A) {
+  if (A.ovf && *A.ovf) return;  // sizes outgrown: the render is repeated
   constexpr int SBX = BX;         // block width
   constexpr int SBP = SBX * SBY;  // threads per CTA = pixels per work item
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1086,6 +1087,7 @@ __device__ __forceinline__ float2 ring_prod2(const float2* rf, unsigned long lon
 
 template <int NV>
 __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
+  if (A.ovf && *A.ovf) return;  // sizes outgrown: the render is repeated
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_work;
   __shared__ unsigned s_skip[8];
@@ -1704,6 +1706,7 @@ __global__ void k_union(const float* slo, const float* shi, float* lo, float* hi
 // front-to-back composition of a tile's chunks: pc = sum_k P(<A_k) S_k with
 // P(<A_{k+1}) = P(<A_k) R_k (R_k = chunk k's running product at A_{k+1})
 __global__ void k_merge(TileArgs A) {
+  if (A.ovf && *A.ovf) return;
   const int tile = blockIdx.x;
   const int n = A.item_cnt[tile];
   if (n <= 1) return;

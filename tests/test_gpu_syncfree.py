@@ -124,3 +124,40 @@ def test_multi_subbox_render_is_sync_free(Context, oracle):
     assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
     assert s2["ms_tile"] > 0 and s2["ms_setup"] > 0
     parity(oracle, w, lo2, hi2, s2)
+
+
+def test_graph_replay_and_invalidation(Context, oracle):
+    """Third render on: the sync-free pipeline is one CUDA-graph replay (captured from the
+    second); any state-changing call (here a new camera) retires the graph."""
+    import copy
+    import torch
+    w = stacked_config(N=300, rot_deg=0.5, axis_frac=0.5)
+    ctx = Context(0)
+    try:
+        ctx.load_workload(w)
+        lo = torch.empty((w.camera["H"], w.camera["W"], 3), dtype=torch.float32, device="cuda:0")
+        hi = torch.empty_like(lo)
+        out = []
+        for _ in range(4):
+            _, _, st = ctx.as_render_bounds(w.tile, w.batch, lo, hi)
+            out.append((lo.cpu().numpy().copy(), hi.cpu().numpy().copy(), st))
+        assert [o[2]["graph_replay"] for o in out] == [0, 0, 1, 1]
+        assert [o[2]["host_syncs"] for o in out][1:] == [0, 0, 0]
+        for o in out[1:]:
+            assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[1], out[0][1])
+            for k in ("pairs", "active_pairs", "uncertain_pairs", "n_items"):
+                assert o[2][k] == out[0][2][k], k
+        assert out[3][2]["launches"] == out[1][2]["launches"] > 0
+        assert out[3][2]["ms_tile"] > 0 and out[3][2]["ms_setup"] > 0
+        # a moved camera: same shapes, new state -> no replay of the old graph
+        w2 = copy.deepcopy(w)
+        w2.camera["t"] = [0.01, -0.005, 0.0]
+        ctx.load_workload(w2)
+        _, _, st = ctx.as_render_bounds(w2.tile, w2.batch, lo, hi)
+        lo2, hi2 = lo.cpu().numpy(), hi.cpu().numpy()
+        assert st["graph_replay"] == 0
+    finally:
+        ctx.close()
+    flo, fhi, _ = fresh(Context, w2)
+    assert np.array_equal(lo2, flo) and np.array_equal(hi2, fhi)
+    parity(oracle, w2, lo2, hi2, st)
