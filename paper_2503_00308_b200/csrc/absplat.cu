@@ -727,8 +727,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     ensure(ctx, ctx->scratch, (size_t)grid * per);
   }
   // automatic chunk length (about six chunks per CTA; with windows beyond the 128-position
-  // masks six times more, so the few expensive tiles split finely enough to balance, C5:
-  // 14.4 -> 5.3 ms), decided on the device from this sub-box's pair count and longest window
+  // masks six times more but at least two batches, so the few expensive tiles split finely
+  // enough to balance without rescanning long lookbacks too often: C5 14.4 -> 5.3 ms in round
+  // 1, 2.17 -> 1.82 ms with the two-batch floor), decided on the device from this sub-box's
+  // pair count and longest window
   ChunkTarget tg;
   tg.M = Mdev;
   tg.wmax = has_exc ? reinterpret_cast<const unsigned*>(ctr + C_WMAX) : nullptr;

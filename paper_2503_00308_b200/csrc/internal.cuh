@@ -332,7 +332,7 @@ void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t 
 // chunk length, decided on the device from the sub-box's own pair count and longest window
 // (so a render sized from remembered capacities cuts exactly the chunks a probed one does):
 // `over` > 0 is as_set_chunk_target's value; otherwise about six chunks per CTA of `grid`,
-// six times finer when a window passes the 128-position masks
+// six times finer (but at least two batches) when a window passes the 128-position masks
 struct ChunkTarget {
   const int64_t* M;        // device: pairs of this sub-box
   const unsigned* wmax;    // device: longest exception window, or nullptr (no exceptions)
