@@ -377,8 +377,11 @@ __device__ __forceinline__ float ring_prod(const float* rf, unsigned long long m
   return prod;
 }
 
+#ifndef KT1_MINB8
+#define KT1_MINB8 8  // 8x8 blocks: 8 CTAs per SM bound (C5 1.80 -> ~1.72 ms; 9 spilled)
+#endif
 template <int NV, int BX>
-__global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : 9) k_tile(TileArgs A) {
+__global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : KT1_MINB8) k_tile(TileArgs A) {
   if (A.ovf && *A.ovf) return;  // sizes outgrown: the render is repeated
   constexpr int SBX = BX;         // block width
   constexpr int SBP = SBX * SBY;  // threads per CTA = pixels per work item
