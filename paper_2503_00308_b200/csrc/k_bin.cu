@@ -511,18 +511,23 @@ void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, c
 }
 
 // CSR of the finalisation lists over ALL positions: fin_rec[fs[p] .. fs[p+1]) are the
-// records finalised at p (fs[p] = lower bound of p in the sorted keys; no-fin keys are M and
-// sort last).  Thread i fills fs over the key gap (key[i-1], key[i]].
+// records finalised at p.  fs[p] = lower bound of p in the sorted keys (no-fin keys are >= M
+// and sort last): one binary search per position (a per-gap fill left one thread writing the
+// whole tail after the last finalising position, 0.24 ms on C5).
 __global__ void k_fin_start(const uint32_t* key, int64_t M, int32_t* fs) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > M) return;
-  auto K = [&](int64_t j) -> int64_t {
-    const uint32_t k = key[j];
-    return k >= (uint64_t)M ? M : (int64_t)k;
-  };
-  const int64_t lo = i == 0 ? -1 : K(i - 1);
-  const int64_t hi = i == M ? M : K(i);
-  for (int64_t p = lo + 1; p <= hi; ++p) fs[p] = (int32_t)i;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > M) return;
+  int64_t lo = 0, hi = M;  // first j with min(key[j], M) >= p
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const uint32_t k = key[mid];
+    const int64_t kk = k >= (uint64_t)M ? M : (int64_t)k;
+    if (kk < p)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  fs[p] = (int32_t)lo;
 }
 void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st) {
   if (M <= 0) {
