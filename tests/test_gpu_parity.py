@@ -57,8 +57,11 @@ def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
     base_lo, base_hi, _ = gpu_render(ctx, w, 16, 64)
     for tile, batch in ((8, 1), (8, 256), (16, 7), (32, 32), (32, 128)):
         lo, hi, _ = gpu_render(ctx, w, tile, batch)
-        # tile-centred fp32 forms round differently per tile size; within the parity budget
-        assert np.abs(lo - base_lo).max() <= TOL and np.abs(hi - base_hi).max() <= TOL
+        # block-centred fp32 forms round differently per block size (TS 8 uses 8x8 blocks,
+        # TS 16 / 32 16x16): measured max 1.1e-5 (C4, TS 8 vs 16) and 2.4e-7 between 16x16
+        # layouts (tools/measure_tolerances.py on a B200); twice the measured bound
+        tol = 2e-5 if tile == 8 else 1e-6
+        assert np.abs(lo - base_lo).max() <= tol and np.abs(hi - base_hi).max() <= tol, (tile, batch)
 
 
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
@@ -130,7 +133,7 @@ def test_gpu_bounds_contain_concrete_renders(ctx, oracle, name):
     for trial in range(24):
         xi = rng.uniform(-1, 1, len(var)) if trial else np.ones(len(var))
         img = ctx.as_render_concrete(xi).cpu().numpy().astype(np.float64)
-        if trial < 2:  # the GPU concrete renderer against the fp64 oracle renderer
+        if trial < 8:  # the GPU concrete renderer against the fp64 oracle renderer (8 poses)
             p = np.array([(lo_ + hi_) / 2 for lo_, hi_ in ax])
             for k, x in zip(var, xi):
                 p[k] = (ax[k][0] + ax[k][1]) / 2 + x * (ax[k][1] - ax[k][0]) / 2
@@ -138,7 +141,7 @@ def test_gpu_bounds_contain_concrete_renders(ctx, oracle, name):
             ref = oracle.render_concrete(w, euler=e, t=t, shifts=shifts)
             assert np.abs(img - ref).max() <= 1e-5
         worst = max(worst, (lo - img).max(), (img - hi).max())
-    assert worst <= 2e-5, worst
+    assert worst <= 1e-6, worst  # H5 (measured: 0 on C2 / C4 / C5 over 64 poses)
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
