@@ -154,7 +154,13 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sbox);
  * Gaussians staged in shared memory per step (1..256).  TS and BS are performance knobs
  * only (reading O1): the bounds do not depend on them.  lo/hi: caller-owned float32
  * [H][W][3], host pointers unless AS_PTR_DEVICE.  Returns once lo/hi are written unless
- * AS_ASYNC (device outputs only).  stats may be NULL. */
+ * AS_ASYNC (device outputs only).  stats may be NULL.
+ * Single-GPU interval renders after the first of a (tile, batch, box dimension) shape run
+ * sync-free: no blocking host read inside the pipeline, buffer sizes remembered from an
+ * earlier render and checked once at the end (a render that outgrows them is repeated
+ * reading each size back: stats->resized); once such a render allocated nothing, the next
+ * identical call is captured into a CUDA graph and later ones replay it (stats->graph_replay)
+ * until any as_set_* / as_load_* call.  Results are bit-identical either way. */
 as_status as_render_bounds(as_ctx* ctx, int32_t tile, int32_t batch, float* lo, float* hi,
                            int32_t flags, as_stats* stats);
 
@@ -192,7 +198,8 @@ as_status as_set_matrixinv(as_ctx* ctx, double k_tol, int32_t k_max);
 /* MatrixInv conic bounds: backward = 0 (default) concretises the
  * forward forms of Xp = X0 + X0 sum_i P^i (reading G3); backward = 1 bounds each conic entry
  * by back-substitution (CROWN-style) through P^i = P^{i-1} E with the same
- * McCormick planes down to E = I - X X0 (reading O17); tighter (Example 1: 0.7588 -> 0.7371).
+ * McCormick planes down to E = I - X X0, the intermediate P^i bounds back-substituted too
+ * (reading O17); tighter (Example 1: 0.7588 -> 0.6875 at k = 8; the paper prints 0.70).
  * With back-substitution the adaptive order is limited to k_max <= 32. */
 as_status as_set_inverse_mode(as_ctx* ctx, int32_t backward);
 as_status as_subbox_fails(as_ctx* ctx, int32_t n, int64_t* fails);
