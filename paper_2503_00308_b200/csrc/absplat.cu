@@ -630,8 +630,8 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     CK(cudaMemsetAsync(pa.subunc, 0, sizeof(unsigned long long), st));
     launch_pairs_prep(pa, st);
     LAUNCHED(ctx, 2);
-    launch_pairs_count(pa, st);  // one classification pass: counts, h, g, 128-bit masks
-    LAUNCHED(ctx, 1);
+    launch_pairs_count(pa, st);  // forward-only classification + completion: counts, h, g, masks
+    LAUNCHED(ctx, 2);
     bool any_unc = ctx->spec.exc;  // sync-free: the remembered answer (checked at the end)
     if (!spec) {
       any_unc = read_dev(ctx, pa.subunc) > 0;

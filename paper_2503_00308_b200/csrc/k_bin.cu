@@ -250,6 +250,11 @@ __global__ void k_pairs_prep(PairArgs A) {
     s2 += fabs(Pi.du[k] - m);
   }
   const double ws = 0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2);
+  if (p0 < A.M) {  // E_F accumulators of the forward-only classification (k_pairs PASS 0)
+    A.mF[p] = make_ulonglong2(0ull, 0ull);
+    A.nF[p] = 0;
+    A.hpos[p] = 0x7fffffff;
+  }
   if (live) {
     A.wsP[p] = ws;
     A.kapP[p] = Pi.kappa;
@@ -301,32 +306,34 @@ __device__ __forceinline__ void shr128(unsigned long long& m0, unsigned long lon
   }
 }
 
-// PASS 0 (every position): classify the window once; write |E_F|, |E_G|, h = min E_F,
-// g = max E_G (tile-local; the position itself when empty), the 128-bit masks E_F over
-// [h, h + 128) and E_G over (p, p + 128], and ntot = |E_F| + |E_G| only for positions whose
-// partners are more than 128 positions away (PM_OVF: they keep explicit CSR lists).
-// PASS 1 (PM_OVF positions only): fill those lists.
+// PASS 0 (every position p): classify the forward window once.  Ind is antisymmetric
+// (ind_class_d(q, p) = 1 - ind_class_d(p, q) on certain pairs, '?' on both sides together:
+// dl and du swap and negate exactly), so each unordered pair is classified by its earlier
+// position only: E_G(p) is kept in registers (bits over (p, p + 128], its count and last
+// partner), and p enters E_F(q) of the later partner through one atomic per uncertain pair
+// (a bit of q's mask over [q - 128, q), or, further than 128 positions, a far count and the
+// far minimum).  k_pairs_post then derives |E_F|, h = min E_F, the masks relative to h and the
+// overflow flags.  PASS 1 (PM_OVF positions only: a partner more than 128 positions away)
+// fills their explicit E_F / E_G lists by scanning both directions.
 template <int NV, int PASS>
 __global__ void k_pairs(PairArgs A) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.M) return;
-  int64_t off = 0;
+  int64_t off = 0, ntp = 0;
   int nFt = 0;
   if (PASS == 1) {
-    if (A.ntot[p] == 0) return;  // not an overflow position
+    ntp = A.ntot[p];
+    if (ntp == 0) return;  // not an overflow position
     off = A.off[p];
     nFt = A.nF[p];
-    if (off + A.ntot[p] > A.nexc_cap) return;  // no room: the caller renders again
+    if (off + ntp > A.nexc_cap) return;  // no room: the caller renders again
   }
   const uint32_t t = A.keys[p];
   if (t >= (uint32_t)A.ntiles) {  // padding position: no partners
     if (PASS == 0) {
-      A.nF[p] = 0;
       A.nG[p] = 0;
-      A.hpos[p] = 0;
       A.gpos[p] = 0;
       A.ntot[p] = 0;
-      A.mF[p] = make_ulonglong2(0ull, 0ull);
       A.mG[p] = make_ulonglong2(0ull, 0ull);
     }
     return;
@@ -338,65 +345,89 @@ __global__ void k_pairs(PairArgs A) {
   const double M = __longlong_as_double((long long)A.tilemax[t]);
   const double factor = A.tileh[(size_t)t * (NVMAX + 1) + NVMAX];
   const double wsi = A.wsP[p];
-  int nF = 0, nG = 0, viol = 0;
-  int hmin = (int)(p - b), gmax = (int)(p - b);
-  unsigned long long f0 = 0, f1 = 0, g0 = 0, g1 = 0;  // E_F rel. p - 128, E_G rel. p + 1
-  bool ovf = false;
-  // backward: earlier positions (expected Ind in {1, ?})
-  for (int64_t q = p - 1; q >= b; --q) {
-    const double kj = A.kapP[q];
-    if (beyond(ki - kj, factor, wsi, M, ki, kj)) break;
-    const int32_t gj = A.vals[q];
-    const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, A.M, q), gj, A.ns);
-    if (c == -1 || c == 0) {  // c == 0 contradicts the order: counted, treated as '?'
-      if (c == 0) ++viol;
-      if (PASS == 1) A.exc[off + nFt - 1 - nF] = (int32_t)(q - b);
-      if (PASS == 0) {
-        if (p - q <= 128)
-          set_bit128(f0, f1, (int)(q - p + 128));
-        else
-          ovf = true;
-      }
-      hmin = (int)(q - b);
-      ++nF;
+  if (PASS == 1) {
+    // backward: earlier positions (expected Ind in {1, ?}), E_F in ascending order
+    int nF = 0;
+    for (int64_t q = p - 1; q >= b; --q) {
+      const double kj = A.kapP[q];
+      if (beyond(ki - kj, factor, wsi, M, ki, kj)) break;
+      const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, A.M, q), A.vals[q], A.ns);
+      if ((c == -1 || c == 0) && nF < nFt) A.exc[off + nFt - 1 - nF++] = (int32_t)(q - b);
     }
   }
   // forward: later positions (expected Ind in {0, ?})
+  int nG = 0, viol = 0;
+  int gmax = (int)(p - b);
+  unsigned long long g0 = 0, g1 = 0;  // E_G rel. p + 1
+  bool far = false;
   for (int64_t q = p + 1; q < e; ++q) {
     const double kj = A.kapP[q];
     if (beyond(kj - ki, factor, wsi, M, ki, kj)) break;
     const int32_t gj = A.vals[q];
     const int c = ind_class_d<NV>(Pi, gi, load_posd<NV>(A.posD, A.M, q), gj, A.ns);
-    if (c == -1 || c == 1) {
-      if (c == 1) ++viol;
-      if (PASS == 1) A.exc[off + nFt + nG] = (int32_t)(q - b);
+    if (c == -1 || c == 1) {  // c == 1 contradicts the order: counted, treated as '?'
+      if (PASS == 1 && nFt + nG < ntp) A.exc[off + nFt + nG] = (int32_t)(q - b);
       if (PASS == 0) {
-        if (q - p <= 128)
-          set_bit128(g0, g1, (int)(q - p - 1));
-        else
-          ovf = true;
+        if (c == 1) ++viol;
+        const int d = (int)(q - p);
+        if (d <= 128) {
+          set_bit128(g0, g1, d - 1);
+          const int k = 128 - d;  // p as a bit of q's E_F mask over [q - 128, q)
+          if (k < 64)
+            atomicOr(&A.mF[q].x, 1ull << k);
+          else
+            atomicOr(&A.mF[q].y, 1ull << (k - 64));
+        } else {
+          far = true;
+          atomicAdd(&A.nF[q], 1);
+          atomicMin(&A.hpos[q], (int)(p - b));
+        }
       }
       gmax = (int)(q - b);
       ++nG;
     }
   }
   if (PASS == 0) {
-    A.nF[p] = nF;
     A.nG[p] = nG;
-    A.hpos[p] = hmin;
     A.gpos[p] = gmax;
-    A.ntot[p] = ovf ? nF + nG : 0;
-    if (ovf) {
-      f0 = f1 = g0 = g1 = 0;
-    } else {  // E_F relative to h: shift by h - (p - 128)
-      shr128(f0, f1, (int)(hmin - (p - b) + 128));
-    }
-    A.mF[p] = make_ulonglong2(f0, f1);
+    A.ntot[p] = far ? 1 : 0;  // provisional: E_G past 128 (k_pairs_post completes it)
     A.mG[p] = make_ulonglong2(g0, g1);
     warp_add(&A.counters[0], (unsigned)nG);
     warp_add(&A.counters[1], (unsigned)viol);
-    warp_add(A.subunc, (unsigned)(nF + nG));
+    warp_add(A.subunc, (unsigned)nG);
   }
+}
+
+// Completes PASS 0 per position: |E_F| = mask bits + far count, h = min E_F (the far minimum
+// when there is one, else the lowest mask bit, else p itself), PM_OVF positions (a partner
+// more than 128 positions away on either side) get ntot = |E_F| + |E_G| and no masks, the
+// others their E_F mask shifted to start at h.
+__global__ void k_pairs_post(PairArgs A) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.M) return;
+  const uint32_t t = A.keys[p];
+  if (t >= (uint32_t)A.ntiles) {  // padding: prep zeroed nF / mF; h is unused
+    A.hpos[p] = 0;
+    return;
+  }
+  const int loc = (int)(p - A.tbegin[t]);
+  unsigned long long f0 = A.mF[p].x, f1 = A.mF[p].y;
+  const int nfar = A.nF[p];
+  const int nF = __popcll(f0) + __popcll(f1) + nfar;
+  int h = loc;
+  if (nfar > 0) {
+    h = A.hpos[p];
+  } else if (f0 | f1) {
+    const int kmin = f0 ? __ffsll((long long)f0) - 1 : 64 + __ffsll((long long)f1) - 1;
+    h = loc - 128 + kmin;
+    shr128(f0, f1, kmin);
+  }
+  const bool ovf = nfar > 0 || A.ntot[p] != 0;
+  A.nF[p] = nF;
+  A.hpos[p] = h;
+  A.ntot[p] = ovf ? nF + A.nG[p] : 0;
+  A.mF[p] = ovf ? make_ulonglong2(0ull, 0ull) : make_ulonglong2(f0, f1);
+  if (ovf) A.mG[p] = make_ulonglong2(0ull, 0ull);
 }
 
 void launch_pairs_prep(const PairArgs& a, cudaStream_t st) {
@@ -410,6 +441,7 @@ void launch_pairs_count(const PairArgs& a, cudaStream_t st) {
   if (a.M <= 0) return;
   const unsigned blocks = (unsigned)((a.M + 127) / 128);
   NV_SWITCH(a.nv, (k_pairs<NVc, 0><<<blocks, 128, 0, st>>>(a)));
+  k_pairs_post<<<(unsigned)((a.M + 255) / 256), 256, 0, st>>>(a);
 }
 void launch_pairs_fill(const PairArgs& a, cudaStream_t st) {
   if (a.M <= 0) return;
