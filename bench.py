@@ -498,6 +498,7 @@ def run_ours(args):
                                             "ms_pairs", "ms_tile", "device_bytes", "n_items",
                                             "grid", "ring_len", "max_window", "ms_gather",
                                             "host_syncs", "resized", "graph_replay", "ms_total",
+                                            "ms_sort", "ms_merge", "kmean",
                                             "world", "n_owned", "peak_bytes")}}
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -125,6 +125,10 @@ typedef struct {
   int32_t graph_replay;    /* 1: the sync-free pipeline ran as one replay of the CUDA graph
                               captured from an identical earlier render (same sizes, tile, batch,
                               outputs; no state-changing call in between) */
+  double ms_sort;          /* radix sorts of the binning (kappa order, pairs by tile), inside ms_bin */
+  double ms_merge;         /* front-to-back composition of split tiles and its write of lo / hi
+                              (the union over sub-boxes is fused into these writes: min / max) */
+  double kmean;            /* mean |L_T| over non-empty (sub-box, tile) lists */
 } as_stats;
 
 /* Flags */

@@ -49,7 +49,8 @@ class AsStats(C.Structure):
                 ("device_bytes", C.c_size_t), ("n_items", C.c_int32), ("grid", C.c_int32),
                 ("ring_len", C.c_int32), ("max_window", C.c_int32), ("ms_gather", C.c_double),
                 ("world", C.c_int32), ("n_owned", C.c_int32), ("peak_bytes", C.c_size_t),
-                ("host_syncs", C.c_int32), ("resized", C.c_int32), ("graph_replay", C.c_int32)]
+                ("host_syncs", C.c_int32), ("resized", C.c_int32), ("graph_replay", C.c_int32),
+                ("ms_sort", C.c_double), ("ms_merge", C.c_double), ("kmean", C.c_double)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

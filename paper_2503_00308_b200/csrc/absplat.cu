@@ -412,18 +412,24 @@ __global__ void k_seq(int32_t* v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = i;
 }
-__global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned long long* out) {
+// longest tile list (out[0]) and the number of non-empty tiles (nonempty)
+__global__ void k_tile_max(const int64_t* tb, const int64_t* te, int n, unsigned long long* out,
+                           unsigned long long* nonempty) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const int64_t k = te[i] - tb[i];
-    if (k > 0) atomicMax(out, (unsigned long long)k);
+    if (k > 0) {
+      atomicMax(out, (unsigned long long)k);
+      atomicAdd(nonempty, 1ull);
+    }
   }
 }
 
 // counters layout (unsigned long long[16])
 enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_PAIRS = 3, C_WSMAX = 4, C_KMAX = 5, C_ACTIVE = 6,
        C_MMAX = 7, C_UNC = 8, C_VIOL = 9, C_WMAX = 10, C_SUBUNC = 11, C_SCENE = 12,
-       C_NEXCMAX = 13, C_ITEMSMAX = 14, C_WMAXALL = 15, C_OVF = 16, C_NCOUNTERS = 24 };
+       C_NEXCMAX = 13, C_ITEMSMAX = 14, C_WMAXALL = 15, C_OVF = 16, C_NONEMPTY = 17,
+       C_NCOUNTERS = 24 };
 
 // sizes the render needs on the device only: max (and sum) over the render's sub-boxes
 __global__ void k_note(const int64_t* v, unsigned long long* mx, unsigned long long* sum) {
@@ -483,7 +489,7 @@ T read_dev(as_ctx* ctx, const T* dptr) {
 int64_t read_i64(as_ctx* ctx, const int64_t* dptr) { return read_dev(ctx, dptr); }
 
 struct PhaseTimes {
-  double setup = 0, bin = 0, pairs = 0, tile = 0;
+  double setup = 0, bin = 0, pairs = 0, tile = 0, sort = 0, merge = 0;
 };
 
 // Render one sub-box (rows a2-a10) into row-major (tslot == nullptr) or compact tile-major
@@ -499,7 +505,7 @@ int64_t size_or_cap(as_ctx* ctx, const int64_t* dptr, int64_t cap, int64_t& prob
   return v;
 }
 
-// ev: 6 events of this sub-box for the phase times (nullptr: none)
+// ev: SUB_EVENTS events of this sub-box for the phase times (nullptr: none)
 void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const Geometry& G,
                    int bs, const int32_t* owner, int rank, const int32_t* tlist, int n_list,
                    const int32_t* tslot, float* lo, float* hi, bool first, cudaEvent_t* ev) {
@@ -519,8 +525,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   }
   if (ev) CK(timing_record(ev[1], st));
   // ---- a6: depth order (stable radix sort by kappa: ties keep ascending index, G6)
+  if (ev) CK(timing_record(ev[6], st));
   cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
                   P<int32_t>(ctx->kval), P<int32_t>(ctx->order), N, 64);
+  if (ev) CK(timing_record(ev[7], st));
   // ---- a6: count overlapped tiles per Gaussian, scan, emit in depth order
   BinArgs ba{};
   ba.order = P<int32_t>(ctx->order);
@@ -564,15 +572,18 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   }
   // stable sort by tile id: within a tile the depth order of emission is kept (padding ids
   // = ntiles fit the sorted bits and go last)
+  if (ev) CK(timing_record(ev[8], st));
   if (M > 0)
     cub_sort_keys32(ctx, P<uint32_t>(ctx->keys), P<uint32_t>(ctx->keys2), P<int32_t>(ctx->vals),
                     P<int32_t>(ctx->vals2), M, bits_for(G.ntiles), false);
+  if (ev) CK(timing_record(ev[9], st));
   const uint32_t* skeys = P<uint32_t>(ctx->keys2);
   const int32_t* svals = P<int32_t>(ctx->vals2);
   launch_ranges(skeys, M, G.ntiles, P<int64_t>(ctx->tbegin), P<int64_t>(ctx->tend), st);
   LAUNCHED(ctx, 1);
   k_tile_max<<<(G.ntiles + 255) / 256, 256, 0, st>>>(P<int64_t>(ctx->tbegin),
-                                                     P<int64_t>(ctx->tend), G.ntiles, ctr + C_KMAX);
+                                                     P<int64_t>(ctx->tend), G.ntiles, ctr + C_KMAX,
+                                                     ctr + C_NONEMPTY);
   LAUNCHED(ctx, 1);
   if (ev) CK(timing_record(ev[2], st));
   // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
@@ -818,6 +829,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   if (ev) CK(timing_record(ev[5], st));
   launch_merge(ta, st);
   LAUNCHED(ctx, 1);
+  if (ev) CK(timing_record(ev[10], st));
   // NEXT-1 (O20): the uncertain positions' interval terms as raw per-pixel sums, for the
   // linear blend that follows (full-image renders only)
   ctx->last_unc = false;
@@ -842,29 +854,37 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   (void)n_list;
 }
 
-// the 6 phase events of the k-th sub-box of a render (pooled)
+// the phase events of the k-th sub-box of a render (pooled): [0] start, [1] after setup,
+// [2] after binning, [3] after pair classification, [4] before / [5] after the tile kernel,
+// [6]/[7] around the kappa sort, [8]/[9] around the pair sort, [10] after the chunk merge
+constexpr int SUB_EVENTS = 11;
 cudaEvent_t* sub_events(as_ctx* ctx, int k) {
-  while ((int)ctx->sbev.size() < 6 * (k + 1)) {
+  while ((int)ctx->sbev.size() < SUB_EVENTS * (k + 1)) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     ctx->sbev.push_back(e);
   }
-  return ctx->sbev.data() + 6 * k;
+  return ctx->sbev.data() + SUB_EVENTS * k;
 }
 // phase times of n sub-boxes (after the render's synchronisation)
 void collect_phases(as_ctx* ctx, int n, PhaseTimes* pt) {
   for (int k = 0; k < n; ++k) {
-    cudaEvent_t* e = ctx->sbev.data() + 6 * k;
-    float a = 0, b = 0, c = 0, d = 0, f = 0;
+    cudaEvent_t* e = ctx->sbev.data() + SUB_EVENTS * k;
+    float a = 0, b = 0, c = 0, d = 0, f = 0, s1 = 0, s2 = 0, m = 0;
     CK(cudaEventElapsedTime(&a, e[0], e[1]));
     CK(cudaEventElapsedTime(&b, e[1], e[2]));
     CK(cudaEventElapsedTime(&c, e[2], e[3]));
     CK(cudaEventElapsedTime(&f, e[3], e[4]));
     CK(cudaEventElapsedTime(&d, e[4], e[5]));
+    CK(cudaEventElapsedTime(&s1, e[6], e[7]));
+    CK(cudaEventElapsedTime(&s2, e[8], e[9]));
+    CK(cudaEventElapsedTime(&m, e[5], e[10]));
     pt->setup += a;
     pt->bin += b + f;
     pt->pairs += c;
     pt->tile += d;
+    pt->sort += s1 + s2;
+    pt->merge += m;
   }
 }
 
@@ -977,6 +997,9 @@ void fill_stats(as_ctx* ctx, const BoxInfo& bi, const Geometry& G, int n_tiles_r
   out->ring_len = ctx->last_R;
   out->max_window = (int32_t)h[C_WMAXALL];
   out->host_syncs = ctx->host_syncs;
+  out->ms_sort = pt.sort;
+  out->ms_merge = pt.merge;
+  out->kmean = h[C_NONEMPTY] ? (double)h[C_PAIRS] / (double)h[C_NONEMPTY] : 0.0;
   out->ms_gather = ctx->last_gather_ms;
   out->world = ctx->world;
   out->n_owned = n_tiles_rendered;

@@ -123,6 +123,13 @@ def test_multi_subbox_render_is_sync_free(Context, oracle):
     assert s2["host_syncs"] == 0 and s2["resized"] == 0
     assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
     assert s2["ms_tile"] > 0 and s2["ms_setup"] > 0
+    # stats of the boundary: sorts inside the binning phase, the chunk merge,
+    # the mean list length over non-empty (sub-box, tile) lists
+    for st in (s1, s2):
+        assert 0 < st["ms_sort"] <= st["ms_bin"] and st["ms_merge"] > 0
+        nonempty = st["pairs"] / st["kmean"]
+        assert abs(nonempty - round(nonempty)) < 1e-6 * nonempty
+        assert round(nonempty) <= st["n_sub"] * st["n_tiles"] and st["kmean"] <= st["kmax"]
     parity(oracle, w, lo2, hi2, s2)
 
 
