@@ -151,7 +151,10 @@ as_status as_load_scene(as_ctx* ctx, int64_t N, const float* mean, const float* 
                         const float* opacity, const float* color, int32_t flags);
 as_status as_set_camera(as_ctx* ctx, const as_camera* cam);
 as_status as_set_pose_box(as_ctx* ctx, const as_pose_box* box);
-/* Optional scene box (NULL clears).  Must be called after as_load_scene (uses N). */
+/* Optional scene box (NULL clears).  Must be called after as_load_scene (uses N).  Host
+ * arrays, copied; validated on the device (group ids in [-1, n_groups), colour / opacity
+ * intervals inside [0,1] with lo <= hi, private-mean intervals finite with lo <= hi): on a bad
+ * entry the scene box is cleared and AS_E_ARG (group id) or AS_E_SCENE is returned. */
 as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sbox);
 
 /* Abstract render of the whole image.  tile = TS in {8, 16, 32}; batch = BS, the number of

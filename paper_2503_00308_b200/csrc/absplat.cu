@@ -1387,6 +1387,32 @@ namespace {
 // scene validation on the device: the smallest invalid Gaussian index and its reason
 // (1 mean / colour not finite or colour outside [0,1], 2 chol not finite, 3 chol diagonal
 // <= 0, 4 opacity outside [0,1]) packed as index * 8 + reason into an atomicMin
+// scene box (as_set_scene_box), on the device: lowest bad index * 8 + reason into *bad
+__global__ void k_validate_sbox(int64_t N, const int32_t* group_of, int n_groups,
+                                const float* col_lo, const float* col_hi, const float* op_lo,
+                                const float* op_hi, const float* priv_lo, const float* priv_hi,
+                                unsigned long long* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int why = 0;
+  if (group_of && (group_of[i] < -1 || group_of[i] >= n_groups)) why = 1;
+  if (!why && col_lo)
+    for (int k = 0; k < 3; ++k) {
+      const float l = col_lo[3 * i + k], h = col_hi[3 * i + k];
+      if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) why = 2;
+    }
+  if (!why && op_lo) {
+    const float l = op_lo[i], h = op_hi[i];
+    if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) why = 3;
+  }
+  if (!why && priv_lo)
+    for (int k = 0; k < 3; ++k) {
+      const float l = priv_lo[3 * i + k], h = priv_hi[3 * i + k];
+      if (!isfinite(l) || !isfinite(h) || !(l <= h)) why = 4;
+    }
+  if (why) atomicMin(bad, (unsigned long long)i * 8ull + (unsigned long long)why);
+}
+
 __global__ void k_validate(int64_t N, const float* m, const float* c, const float* o,
                            const float* col, unsigned long long* bad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1665,35 +1691,6 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
       return AS_E_ARG;
     }
   }
-  for (int64_t i = 0; i < N; ++i) {
-    if (sb->n_groups > 0 && (sb->group_of[i] < -1 || sb->group_of[i] >= sb->n_groups)) {
-      set_err(ctx, "group_of[%lld] out of range", (long long)i);
-      return AS_E_ARG;
-    }
-    if (sb->col_lo)
-      for (int k = 0; k < 3; ++k) {
-        const float l = sb->col_lo[3 * i + k], h = sb->col_hi[3 * i + k];
-        if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) {
-          set_err(ctx, "colour interval of Gaussian %lld invalid", (long long)i);
-          return AS_E_SCENE;
-        }
-      }
-    if (sb->op_lo) {
-      const float l = sb->op_lo[i], h = sb->op_hi[i];
-      if (!(l >= 0.f) || !(l <= h) || !(h <= 1.f)) {
-        set_err(ctx, "opacity interval of Gaussian %lld invalid", (long long)i);
-        return AS_E_SCENE;
-      }
-    }
-    if (sb->priv_lo)
-      for (int k = 0; k < 3; ++k) {
-        const float l = sb->priv_lo[3 * i + k], h = sb->priv_hi[3 * i + k];
-        if (!std::isfinite(l) || !std::isfinite(h) || !(l <= h)) {
-          set_err(ctx, "private mean interval of Gaussian %lld invalid", (long long)i);
-          return AS_E_SCENE;
-        }
-      }
-  }
   try {
     cudaSetDevice(ctx->device);
     ctx->n_groups = sb->n_groups;
@@ -1729,7 +1726,41 @@ as_status as_set_scene_box(as_ctx* ctx, const as_scene_box* sb) {
       CK(cudaMemcpyAsync(ctx->priv_lo.p, sb->priv_lo, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
       CK(cudaMemcpyAsync(ctx->priv_hi.p, sb->priv_hi, 12 * N, cudaMemcpyHostToDevice, ctx->stream));
     }
+    // validated on the device (copies first, one check): a bad entry clears the scene box
+    unsigned long long bad = ~0ull;
+    ensure(ctx, ctx->counters, sizeof(unsigned long long) * C_NCOUNTERS);
+    unsigned long long* dbad = P<unsigned long long>(ctx->counters) + C_SCENE;
+    CK(cudaMemcpyAsync(dbad, &bad, sizeof bad, cudaMemcpyHostToDevice, ctx->stream));
+    if (N > 0) {
+      k_validate_sbox<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+          N, ctx->has_group ? P<int32_t>(ctx->group_of) : nullptr, sb->n_groups,
+          ctx->has_col ? P<float>(ctx->col_lo) : nullptr, ctx->has_col ? P<float>(ctx->col_hi) : nullptr,
+          ctx->has_op ? P<float>(ctx->op_lo) : nullptr, ctx->has_op ? P<float>(ctx->op_hi) : nullptr,
+          ctx->has_priv ? P<float>(ctx->priv_lo) : nullptr,
+          ctx->has_priv ? P<float>(ctx->priv_hi) : nullptr, dbad);
+      LAUNCHED(ctx, 1);
+    }
+    CK(cudaMemcpyAsync(&bad, dbad, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // host sources may be freed after return
+    if (bad != ~0ull) {
+      ctx->n_groups = 0;
+      ctx->has_group = ctx->has_col = ctx->has_op = ctx->has_priv = false;
+      const long long gi = (long long)(bad >> 3);
+      switch ((int)(bad & 7)) {
+        case 1:
+          set_err(ctx, "group_of[%lld] out of range", gi);
+          return AS_E_ARG;
+        case 2:
+          set_err(ctx, "colour interval of Gaussian %lld invalid", gi);
+          return AS_E_SCENE;
+        case 3:
+          set_err(ctx, "opacity interval of Gaussian %lld invalid", gi);
+          return AS_E_SCENE;
+        default:
+          set_err(ctx, "private mean interval of Gaussian %lld invalid", gi);
+          return AS_E_SCENE;
+      }
+    }
     return AS_OK;
   } catch (const Err& e) {
     return e.st;

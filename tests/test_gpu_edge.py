@@ -102,3 +102,36 @@ def test_slow_paths_run_and_match(ctx, oracle):
     print("rare-path counters over the stress cases:", fired)
     missing = [k for k, v in fired.items() if v == 0]
     assert not missing, (missing, fired)
+
+
+@pytest.mark.parametrize("field,idx,reason", [("col_hi", 7, "colour"), ("group_of", 11, "group_of"),
+                                              ("op_lo", 3, "opacity"), ("priv_hi", 5, "private")])
+def test_scene_box_validated_on_device(ctx, field, idx, reason):
+    """as_set_scene_box checks every entry on the device: the first bad
+    index is reported, the scene box is cleared, and a valid box is accepted again."""
+    from paper_2503_00308_b200.api import AbsplatError
+    from workloads import make_config
+    w = make_config("C5", N=400, res=32)
+    ctx.load_workload(w)
+    N = w.mean.shape[0]
+    sb = dict(w.scene_box)
+    sb["op_lo"] = np.full(N, 0.2, np.float32)
+    sb["op_hi"] = np.full(N, 0.9, np.float32)
+    sb["priv_lo"] = np.full((N, 3), -0.01, np.float32)
+    sb["priv_hi"] = np.full((N, 3), 0.01, np.float32)
+    bad = {k: (np.array(v, copy=True) if isinstance(v, np.ndarray) else v) for k, v in sb.items()}
+    arr = bad[field]
+    if field == "group_of":
+        arr[idx] = 3  # >= n_groups
+    elif field == "col_hi":
+        arr[idx, 0] = 1.5
+    elif field == "op_lo":
+        arr[idx] = 0.95  # above op_hi
+    else:
+        arr[idx, 1] = np.inf
+    with pytest.raises(AbsplatError) as e:
+        ctx.as_set_scene_box(bad)
+    assert reason in str(e.value) and str(idx) in str(e.value)
+    ctx.as_set_scene_box(sb)  # valid: accepted
+    lo, hi, _ = ctx.as_render_bounds(tile=8, batch=32)
+    assert np.all(lo.cpu().numpy() <= hi.cpu().numpy())
