@@ -1122,6 +1122,9 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   const float2 DU1 = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
+#ifdef KT2_PROF
+  long long pr_bar = 0, pr_mbar = 0, pr_stage = 0, pr_walk = 0, pr_t = 0;
+#endif
 
   for (;;) {
     if (tid == 0) s_work = atomicAdd(A.counter, 1);
@@ -1175,9 +1178,19 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
       // the next batch's Gaussian ids, loaded now so the copies can be issued right after
       // this batch's records are staged
       const int32_t gnext = tid < nbn ? A.vals[tb + b0 + nb + tid] : 0;
+#ifdef KT2_PROF
+      // profiling order: the bulk-copy wait first (per thread), then the barrier
+      pr_t = clock64();
+      mbar_wait(&s_bar, phase);
+      { const long long t = clock64(); pr_mbar += t - pr_t; pr_t = t; }
+      __syncthreads();
+      { volatile int dep = s_work; (void)dep; const long long t = clock64(); pr_bar += t - pr_t; pr_t = t; }
+      phase ^= 1u;
+#else
       __syncthreads();
       mbar_wait(&s_bar, phase);  // this batch's raw records have landed
       phase ^= 1u;
+#endif
       // ---- phase A: metadata + cull tables (one thread per Gaussian, highest ids) and
       //      staging (NPART threads per Gaussian), as in k_tile
       for (int j = T2 - 1 - tid; j < nb; j += T2) {
@@ -1335,6 +1348,9 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         F.n = (short)n;
       }
       __syncthreads();
+#ifdef KT2_PROF
+      { const long long t = clock64(); pr_stage += t - pr_t; pr_t = t; }
+#endif
       // ---- walk the batch in (kappa, index) order, two pixels per thread
       for (int j = 0; j < nb; ++j) {
         const SRec2<NV>& R = srec[j];
@@ -1486,6 +1502,9 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
           for (int c = 0; c < 3; ++c) alc[c] = __ffma2_rn(tl, bc(clo[c]), alc[c]);
         }
       }
+#ifdef KT2_PROF
+      { const long long t = clock64(); pr_walk += t - pr_t; pr_t = t; }
+#endif
     }
     // ---- epilogue (both pixels)
 #pragma unroll
@@ -1531,6 +1550,14 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
       }
     }
   }
+#ifdef KT2_PROF
+  if ((tid & 31) == 0 && A.dbg) {
+    atomicAdd(A.dbg + 0, (unsigned long long)pr_bar);
+    atomicAdd(A.dbg + 1, (unsigned long long)pr_mbar);
+    atomicAdd(A.dbg + 2, (unsigned long long)pr_stage);
+    atomicAdd(A.dbg + 3, (unsigned long long)pr_walk);
+  }
+#endif
   unsigned v = active;
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULLM, v, s);
