@@ -431,6 +431,12 @@ enum { C_FAIL = 0, C_STRAD = 1, C_DROP = 2, C_PAIRS = 3, C_WSMAX = 4, C_KMAX = 5
        C_NEXCMAX = 13, C_ITEMSMAX = 14, C_WMAXALL = 15, C_OVF = 16, C_NONEMPTY = 17,
        C_NCOUNTERS = 24 };
 
+// per-position count of the finalisation records (keys >= M: none)
+__global__ void k_fin_hist(const uint32_t* key, int64_t M, int32_t* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M && key[i] < (uint64_t)M) atomicAdd(&cnt[key[i]], 1);
+}
+
 // sizes the render needs on the device only: max (and sum) over the render's sub-boxes
 __global__ void k_note(const int64_t* v, unsigned long long* mx, unsigned long long* sum) {
   const unsigned long long x = (unsigned long long)(*v > 0 ? *v : 0);
@@ -694,8 +700,13 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       LAUNCHED(ctx, 1);
       cub_sort_keys32(ctx, P<uint32_t>(ctx->finkey), P<uint32_t>(ctx->finkey2),
                       P<int32_t>(ctx->finval), P<int32_t>(ctx->finval2), M, bits_for(M), false);
-      launch_fin_start(P<uint32_t>(ctx->finkey2), M, P<int32_t>(ctx->finstart), st);
+      // CSR start of the finalisation lists over all positions: fs = exclusive scan of the
+      // per-position record counts (the keys' histogram; `cover` is free after k_meta)
+      int32_t* fcnt = P<int32_t>(ctx->cover);
+      CK(cudaMemsetAsync(fcnt, 0, sizeof(int32_t) * (M + 1), st));
+      k_fin_hist<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(P<uint32_t>(ctx->finkey2), M, fcnt);
       LAUNCHED(ctx, 1);
+      cub_exclusive_sum(ctx, fcnt, P<int32_t>(ctx->finstart), M + 1);
       launch_finrec(P<uint32_t>(ctx->finkey2), P<int32_t>(ctx->finval2), pa, P<int4>(ctx->pflag),
                     P<ulonglong2>(ctx->maskG), ctx->hot.p, P<FinRec>(ctx->finrec), st);
       LAUNCHED(ctx, 1);

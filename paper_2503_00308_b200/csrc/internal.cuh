@@ -328,7 +328,6 @@ void launch_meta(const PairArgs& a, const int32_t* cstore, const int32_t* ccut,
                  int32_t* finval, cudaStream_t st);
 void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, const int4* pm,
                    const ulonglong2* mG, const void* hot, FinRec* out, cudaStream_t st);
-void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st);
 // chunk length, decided on the device from the sub-box's own pair count and longest window
 // (so a render sized from remembered capacities cuts exactly the chunks a probed one does):
 // `over` > 0 is as_set_chunk_target's value; otherwise about six chunks per CTA of `grid`,

@@ -542,33 +542,6 @@ void launch_finrec(const uint32_t* key, const int32_t* val, const PairArgs& a, c
   NV_SWITCH(a.nv, (k_finrec<NVc><<<blocks, 256, 0, st>>>(key, val, a, pm, mG, hot, out)));
 }
 
-// CSR of the finalisation lists over ALL positions: fin_rec[fs[p] .. fs[p+1]) are the
-// records finalised at p.  fs[p] = lower bound of p in the sorted keys (no-fin keys are >= M
-// and sort last): one binary search per position (a per-gap fill left one thread writing the
-// whole tail after the last finalising position, 0.24 ms on C5).
-__global__ void k_fin_start(const uint32_t* key, int64_t M, int32_t* fs) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p > M) return;
-  int64_t lo = 0, hi = M;  // first j with min(key[j], M) >= p
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    const uint32_t k = key[mid];
-    const int64_t kk = k >= (uint64_t)M ? M : (int64_t)k;
-    if (kk < p)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  fs[p] = (int32_t)lo;
-}
-void launch_fin_start(const uint32_t* key, int64_t M, int32_t* fs, cudaStream_t st) {
-  if (M <= 0) {
-    cudaMemsetAsync(fs, 0, sizeof(int32_t), st);
-    return;
-  }
-  k_fin_start<<<(unsigned)((M + 1 + 255) / 256), 256, 0, st>>>(key, M, fs);
-}
-
 // ------------------------------------------------------------------------- work items
 // Split every tile's list into chunks of `target` positions.  A chunk [s, e) is scanned
 // over [A, L): the lookback [A, s) covers the E_F windows of its positions (A = min h_p)
