@@ -1088,7 +1088,9 @@ __device__ __forceinline__ float2 ring_prod2(const float2* rf, unsigned long lon
   return prod;
 }
 
-template <int NV>
+// EXC = false: the instantiation for renders without uncertain depth pairs (no ring, no
+// exception metadata): every exception branch of the walk folds away at compile time
+template <int NV, bool EXC>
 __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   if (A.ovf && *A.ovf) return;  // sizes outgrown: the render is repeated
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1107,7 +1109,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   // current batch is walked (one mbarrier phase per batch)
   HotRec<NV>* raw = reinterpret_cast<HotRec<NV>*>(fins + FB);     // [BS]
   __shared__ __align__(8) unsigned long long s_bar;
-  const bool has_exc = A.pm != nullptr;
+  const bool has_exc = EXC && A.pm != nullptr;
   const int tid = threadIdx.x;
   float2* rf = has_exc ? reinterpret_cast<float2*>(A.ring) + (size_t)blockIdx.x * A.R * 4 * T2 + tid
                        : nullptr;
@@ -1310,7 +1312,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         }
       }
       const int F0 = s_F[0];
-      for (int t = tid - 32; t < min(s_F[1] - F0, FB); t += T2 - 32) {
+      for (int t = tid - 32; EXC && t < min(s_F[1] - F0, FB); t += T2 - 32) {
         if (t < 0) break;
         const FinRec fr = A.fin_rec[F0 + t];
         FinS& F = fins[t];
@@ -1354,7 +1356,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
       // ---- walk the batch in (kappa, index) order, two pixels per thread
       for (int j = 0; j < nb; ++j) {
         const SRec2<NV>& R = srec[j];
-        const int flags = R.flags, pmf = R.pmf;
+        const int flags = R.flags, pmf = EXC ? R.pmf : 0;
         const int qpos = b0 + j;
         if (qpos == anext) {
           recb = Tb;
@@ -1367,7 +1369,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         // latency hides behind it (slot qq is not rewritten before the use: qpos - qq < R)
         const int fr0 = R.pfb - F0;
         float2 tl0 = f2(0.f, 0.f);
-        if (fr0 < R.pfe - F0 && fr0 < FB) {
+        if (EXC && fr0 < R.pfe - F0 && fr0 < FB) {
           const int q0 = fins[fr0].qq;
           if (q0 >= 0) tl0 = rf[RS2(q0, 3, rmask)];
         }
@@ -1458,7 +1460,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
         }
         Tb = __ffma2_rn(f2(-Tb.x, -Tb.y), alo, Tb);
         Tl = __ffma2_rn(f2(-Tl.x, -Tl.y), ahi, Tl);
-        for (int f = R.pfb - F0; f < R.pfe - F0; ++f) {
+        for (int f = R.pfb - F0; EXC && f < R.pfe - F0; ++f) {
           float2 tl;
           const float* clo;
           if (f < FB) {
@@ -1860,11 +1862,14 @@ static int grid_bx(int ts, int bs) {
 }
 template <int NV>
 static int grid_v2(int ts, int bs) {
-  if (cudaFuncSetAttribute(k_tile2<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_tile2<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tile2<NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024) != cudaSuccess)
     return 0;
   int per_sm = 0, dev = 0, nsm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile2<NV>, T2, smem_for<NV>(ts, bs));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile2<NV, true>, T2,
+                                                smem_for<NV>(ts, bs));
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   return std::max(1, per_sm) * nsm;
@@ -1889,8 +1894,10 @@ int tile_grid(int nv, int ts, int bs) {
 
 template <int NV>
 static void launch_one(const TileArgs& a, int grid, cudaStream_t st) {
-  if (a.kver == 2)
-    k_tile2<NV><<<grid, T2, smem_for<NV>(a.ts, a.bs), st>>>(a);
+  if (a.kver == 2 && a.pm)
+    k_tile2<NV, true><<<grid, T2, smem_for<NV>(a.ts, a.bs), st>>>(a);
+  else if (a.kver == 2)
+    k_tile2<NV, false><<<grid, T2, smem_for<NV>(a.ts, a.bs), st>>>(a);
   else if (block_w(a.ts) == 16)
     k_tile<NV, 16><<<grid, 16 * SBY, smem_for<NV>(a.ts, a.bs), st>>>(a);
   else
