@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -525,11 +526,14 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   // (k_tile's 256-position skip ring covers a batch plus the 128 positions before it)
   bs = tile_batch(nv, G.ts, bs);
   if (ev) CK(timing_record(ev[0], st));
+  nvtxRangePushA("absplat.setup");
   if (do_setup) {
     CK(cudaMemsetAsync(ctr + C_WSMAX, 0, sizeof(unsigned long long), st));
     run_setup(ctx, bi, s);
   }
   if (ev) CK(timing_record(ev[1], st));
+  nvtxRangePop();
+  nvtxRangePushA("absplat.bin");
   // ---- a6: depth order (stable radix sort by kappa: ties keep ascending index, G6)
   if (ev) CK(timing_record(ev[6], st));
   cub_sort_keys64(ctx, P<unsigned long long>(ctx->kkey), P<unsigned long long>(ctx->kkey2),
@@ -592,6 +596,8 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
                                                      ctr + C_NONEMPTY);
   LAUNCHED(ctx, 1);
   if (ev) CK(timing_record(ev[2], st));
+  nvtxRangePop();
+  nvtxRangePushA("absplat.pairs");
   // ---- a7: depth-order abstraction (uncertain pairs + exception windows)
   TileArgs ta{};
   bool has_exc = false;
@@ -732,6 +738,8 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     }
   }
   if (ev) CK(timing_record(ev[3], st));
+  nvtxRangePop();
+  nvtxRangePushA("absplat.items");
   // ---- work items: (tile, chunk) cut where no uncertain pair is split, longest first
   const int grid0 = tile_grid(nv, G.ts, bs);
   int grid = grid0;
@@ -835,12 +843,17 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   ctx->last_grid = grid;
   ctx->last_R = R;
   if (ev) CK(timing_record(ev[4], st));
+  nvtxRangePop();
+  nvtxRangePushA("absplat.tile");
   launch_tile(nv, ta, grid, st);
   LAUNCHED(ctx, 1);
   if (ev) CK(timing_record(ev[5], st));
+  nvtxRangePop();
+  nvtxRangePushA("absplat.merge");
   launch_merge(ta, st);
   LAUNCHED(ctx, 1);
   if (ev) CK(timing_record(ev[10], st));
+  nvtxRangePop();
   // NEXT-1 (O20): the uncertain positions' interval terms as raw per-pixel sums, for the
   // linear blend that follows (full-image renders only)
   ctx->last_unc = false;
@@ -2041,7 +2054,9 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
         };
         if (ctx->gexec && ctx->gkey == k) {  // replay
           n_done = n_timed = s1 > s0 ? s1 - s0 : 0;
+          nvtxRangePushA("absplat.graph_replay");
           launch_graph();
+          nvtxRangePop();
           ctx->launches = ctx->glaunches;
           done = replayed = true;
         } else if (ctx->gready_ok && ctx->gready == k) {
