@@ -168,3 +168,46 @@ def test_graph_replay_and_invalidation(Context, oracle):
     flo, fhi, _ = fresh(Context, w2)
     assert np.array_equal(lo2, flo) and np.array_equal(hi2, fhi)
     parity(oracle, w2, lo2, hi2, st)
+
+
+@pytest.mark.parametrize("change", ["chunk_target", "matrixinv", "inverse_mode", "pose_box"])
+def test_state_changes_retire_the_graph(Context, change):
+    """Every state-changing call bumps the context generation: the next render is not a
+    replay, and it equals a fresh context's render of the new state bit for bit."""
+    import copy
+    import torch
+    w = stacked_config(N=300, rot_deg=0.5, axis_frac=0.5)
+    ctx = Context(0)
+    try:
+        ctx.load_workload(w)
+        lo = torch.empty((w.camera["H"], w.camera["W"], 3), dtype=torch.float32, device="cuda:0")
+        hi = torch.empty_like(lo)
+        for _ in range(3):
+            st = ctx.as_render_bounds(w.tile, w.batch, lo, hi)[2]
+        assert st["graph_replay"] == 1
+        w2 = copy.deepcopy(w)
+        if change == "chunk_target":
+            ctx.as_set_chunk_target(7)
+        elif change == "matrixinv":
+            ctx.as_set_matrixinv(1e-9, 16)
+            w2.pose_box.update(k_tol=1e-9, k_max=16)
+        elif change == "inverse_mode":
+            ctx.as_set_inverse_mode(1)
+            w2.pose_box.update(inv_backward=1)
+        else:
+            w2.pose_box = dict(w.pose_box, eps_t=[0.004, 0.0, 0.0])
+            ctx.as_set_pose_box(w2.pose_box)
+        st = ctx.as_render_bounds(w.tile, w.batch, lo, hi)[2]
+        assert st["graph_replay"] == 0
+        a_lo, a_hi = lo.cpu().numpy().copy(), hi.cpu().numpy().copy()
+    finally:
+        ctx.close()
+    f = Context(0)
+    try:
+        f.load_workload(w2)
+        if change == "chunk_target":
+            f.as_set_chunk_target(7)
+        flo, fhi, _ = f.as_render_bounds(tile=w.tile, batch=w.batch)
+    finally:
+        f.close()
+    assert np.array_equal(a_lo, flo.cpu().numpy()) and np.array_equal(a_hi, fhi.cpu().numpy())
