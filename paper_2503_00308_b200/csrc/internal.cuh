@@ -297,14 +297,16 @@ struct PairArgs {
   double* wsP;            // [M] w + S' of the Gaussian at each position
   double* kapP;           // [M] kappa at each position
   double* posD;           // [2(NV+1)][M] depth form at each position (coefficient-major)
-  int32_t* nF;            // [M]
+  int32_t* nF;            // [M] |E_F| (during k_pairs PASS 0: the count of partners > 128 back)
   int32_t* nG;            // [M]
-  int64_t* ntot;          // [M+1] nF + nG (scanned into off)
+  int64_t* ntot;          // [M+1] nF + nG of PM_OVF positions, else 0 (scanned into off)
   const int64_t* off;     // [M+1] exclusive scan of nF+nG
   int32_t* exc;           // [total] tile-local positions: E_F ascending then E_G ascending
-  int32_t* hpos;          // [M] first position of E_F (tile-local) or own position
+  int32_t* hpos;          // [M] first position of E_F (tile-local) or own position (during
+                          //     PASS 0: the minimum over partners > 128 back)
   int32_t* gpos;          // [M] last position of E_G (tile-local) or own position
-  ulonglong2* mF;         // [M] E_F bits over [h, h+128) (0 for PM_OVF positions)
+  ulonglong2* mF;         // [M] E_F bits over [h, h+128) (0 for PM_OVF positions; during
+                          //     PASS 0: bits over [p-128, p), set by the earlier partners)
   ulonglong2* mG;         // [M] E_G bits over (p, p+128] (0 for PM_OVF positions)
   unsigned long long* subunc;  // uncertain (position, partner) entries of this sub-box
   int ns;                 // shared variables; slots ns.. are per-Gaussian private (NEXT-2)
