@@ -102,3 +102,50 @@ def test_checked_build_is_the_same_abi():
                          check=True).stdout
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     assert set(_abi.declared_functions()) <= exported
+
+
+def _header_struct_fields(name):
+    """(ctype, field) pairs of a typedef struct in include/absplat.h (comments stripped;
+    pointers map to c_void_p, arrays to ctype * n)."""
+    import re
+    base = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "double": ctypes.c_double,
+            "size_t": ctypes.c_size_t, "float": ctypes.c_float}
+    txt = open(_abi.HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    end = re.search(r"\}\s*" + name + ";", txt)
+    assert end, name
+    start = txt.rfind("typedef struct {", 0, end.start())
+    body = txt[start + len("typedef struct {"):end.start()]
+    out = []
+    for decl in body.split(";"):
+        decl = decl.replace("const ", "").strip()
+        if not decl:
+            continue
+        ty, rest = decl.split(None, 1)
+        ptr = ty.endswith("*")
+        ty = ty.rstrip("*")
+        for item in rest.split(","):
+            item = item.strip()
+            ptr_i = ptr or item.startswith("*")
+            item = item.lstrip("*")
+            m = re.match(r"(\w+)(?:\[(\d+)\])?$", item)
+            assert m, item
+            ct = ctypes.c_void_p if ptr_i else base[ty]
+            if m.group(2):
+                ct = ct * int(m.group(2))
+            out.append((ct, m.group(1)))
+    return out
+
+
+@pytest.mark.parametrize("cname,pyname", [("as_stats", "AsStats"), ("as_camera", "AsCamera"),
+                                           ("as_pose_box", "AsPoseBox"),
+                                           ("as_scene_box", "AsSceneBox")])
+def test_struct_mirrors_match_header(cname, pyname):
+    """The ctypes mirrors have the header's fields, in order, with the same types and size."""
+    hdr = _header_struct_fields(cname)
+    py = getattr(_abi, pyname)._fields_
+    assert [f for _, f in hdr] == [n for n, _ in py]
+    for (ct, f), (n, t) in zip(hdr, py):
+        assert ctypes.sizeof(ct) == ctypes.sizeof(t) and ctypes.alignment(ct) == ctypes.alignment(t), f
+        if not issubclass(t, ctypes.Array):
+            assert ct is t, (f, ct, t)
