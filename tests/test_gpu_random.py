@@ -56,3 +56,12 @@ def test_random_parity(ctx, oracle, seed):
     for k in ("pairs", "active_pairs", "uncertain_pairs", "fails", "dropped"):
         assert st[k] == ost[k], (seed, k, st[k], ost[k])
     assert st["order_violations"] == 0
+    # the same render again, sync-free and then as a CUDA-graph replay, into fixed device
+    # outputs: bit for bit the probed one (sizes remembered across the sweep's shapes)
+    import torch
+    dlo, dhi = torch.empty_like(torch.as_tensor(lo)).cuda(), torch.empty_like(torch.as_tensor(hi)).cuda()
+    for k in range(3):
+        _, _, s2 = ctx.as_render_bounds(tile, batch, dlo, dhi)
+        assert np.array_equal(dlo.cpu().numpy(), lo) and np.array_equal(dhi.cpu().numpy(), hi), (seed, k)
+        assert s2["pairs"] == st["pairs"] and s2["active_pairs"] == st["active_pairs"]
+    assert s2["host_syncs"] == 0 and s2["graph_replay"] == 1, (seed, s2["host_syncs"], s2["graph_replay"])
