@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -104,6 +105,10 @@ struct as_ctx {
   } spec, probe;
   bool spec_on = false;
   int64_t spec_redo = 0;  // renders repeated after a failed verification (stats)
+  // as_render_shard's remembered sizes, per (tile, batch, box dimension, world, rank): emulated
+  // ranks run in turn on one context, each with its own pair and item counts
+  std::map<uint64_t, Sizes> shard_spec;
+  Sizes* cur_spec = &spec;  // the sizes a sync-free render_subbox takes (render or shard cache)
   // CUDA graph of the sync-free pipeline: captured on the render after a sync-free one that
   // allocated nothing, replayed while the key holds.  gen counts every state-changing API
   // call, alloc_gen every (re)allocation; both are part of the key.
@@ -562,7 +567,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   const int64_t* Mdev = P<int64_t>(ctx->offsets) + N;
   k_note<<<1, 1, 0, st>>>(Mdev, ctr + C_MMAX, ctr + C_PAIRS);
   LAUNCHED(ctx, 1);
-  const int64_t M = size_or_cap(ctx, Mdev, ctx->spec.M, ctx->probe.M);
+  const int64_t M = size_or_cap(ctx, Mdev, ctx->cur_spec->M, ctx->probe.M);
   if (spec) {
     k_cap_check<<<1, 1, 0, st>>>(Mdev, M, ctr + C_OVF, 4ull);
     LAUNCHED(ctx, 1);
@@ -655,7 +660,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
     LAUNCHED(ctx, 2);
     launch_pairs_count(pa, st);  // forward-only classification + completion: counts, h, g, masks
     LAUNCHED(ctx, 2);
-    bool any_unc = ctx->spec.exc;  // sync-free: the remembered answer (checked at the end)
+    bool any_unc = ctx->cur_spec->exc;  // sync-free: the remembered answer (checked at the end)
     if (!spec) {
       any_unc = read_dev(ctx, pa.subunc) > 0;
       ctx->probe.exc = ctx->probe.exc || any_unc;
@@ -665,7 +670,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       cub_exclusive_sum(ctx, pa.ntot, P<int64_t>(ctx->eoff), M + 1);
       k_note<<<1, 1, 0, st>>>(P<int64_t>(ctx->eoff) + M, ctr + C_NEXCMAX, nullptr);
       LAUNCHED(ctx, 1);
-      const int64_t nexc = size_or_cap(ctx, P<int64_t>(ctx->eoff) + M, ctx->spec.nexc,
+      const int64_t nexc = size_or_cap(ctx, P<int64_t>(ctx->eoff) + M, ctx->cur_spec->nexc,
                                        ctx->probe.nexc);
       if (spec) {
         k_cap_check<<<1, 1, 0, st>>>(P<int64_t>(ctx->eoff) + M, nexc, ctr + C_OVF, 8ull);
@@ -722,7 +727,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
       k_note32<<<1, 1, 0, st>>>(wmax, ctr + C_WMAXALL);
       LAUNCHED(ctx, 1);
       if (spec) {
-        R = ctx->spec.R;
+        R = ctx->cur_spec->R;
       } else {
         const unsigned hw = read_dev(ctx, wmax);
         while (R <= (int)hw) R <<= 1;
@@ -779,7 +784,7 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
   const int64_t* NIdev = P<int64_t>(ctx->item_off) + G.ntiles;
   k_note<<<1, 1, 0, st>>>(NIdev, ctr + C_ITEMSMAX, nullptr);
   LAUNCHED(ctx, 1);
-  const int64_t n_items = size_or_cap(ctx, NIdev, ctx->spec.items, ctx->probe.items);
+  const int64_t n_items = size_or_cap(ctx, NIdev, ctx->cur_spec->items, ctx->probe.items);
   ensure(ctx, ctx->items, sizeof(int4) * n_items);
   ensure(ctx, ctx->items2, sizeof(int4) * n_items);
   ensure(ctx, ctx->item_key, sizeof(uint32_t) * n_items);
@@ -1965,6 +1970,7 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
     for (;;) {
       have_h = false;
       ctx->spec_on = spec;
+      ctx->cur_spec = &ctx->spec;
       ctx->probe = as_ctx::Sizes{};
       ctx->host_syncs = 0;
       ctx->launches = 0;
@@ -2242,9 +2248,22 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       set_err(ctx, "max_tiles * world < n_tiles");
       return AS_E_ARG;
     }
+    // sync-free after the first render of this (shape, world, rank): sizes remembered and
+    // checked once, with the owner map, at the end (as in render_range)
+    const uint64_t skey = ((uint64_t)tile << 52) ^ ((uint64_t)batch << 40) ^
+                          ((uint64_t)bi.n_vars << 32) ^ ((uint64_t)world << 16) ^ (uint64_t)rank;
+    as_ctx::Sizes& sp = ctx->shard_spec[skey];
+    bool spec = sp.valid && !(flags & AS_ASYNC);
+    bool resized = false;
+    std::vector<int32_t> own(G.ntiles);
+    unsigned long long hc[C_NCOUNTERS];
+    float *dlo = lo_tm, *dhi = hi_tm;
+    for (;;) {
     ctx->launches = 0;
     ctx->host_syncs = 0;
-    ctx->spec_on = false;  // probing: this entry point reads every size back
+    ctx->spec_on = spec;
+    ctx->cur_spec = &sp;
+    ctx->probe = as_ctx::Sizes{};
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
     // ---- owner map (identical on every rank): LPT over per-tile pair counts, on the device
@@ -2263,7 +2282,6 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
                                                         nullptr);
     LAUNCHED(ctx, 1);
     const size_t tmax = (size_t)max_tiles * tile * tile * 3;
-    float *dlo = lo_tm, *dhi = hi_tm;
     if (!(flags & AS_PTR_DEVICE)) {
       ensure(ctx, ctx->img_lo, sizeof(float) * tmax);
       ensure(ctx, ctx->img_hi, sizeof(float) * tmax);
@@ -2277,11 +2295,30 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
                     P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0,
                     stats ? sub_events(ctx, sb) : nullptr);
     }
-    // the owned tile ids (host output): the owner map comes back once the render is queued
-    std::vector<int32_t> own(G.ntiles);
+    // the owned tile ids (host output) and the counters come back in one synchronisation
     CK(cudaMemcpyAsync(own.data(), ctx->owner.p, sizeof(int32_t) * G.ntiles,
                        cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc, ctx->counters.p, sizeof hc, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (spec) {
+      const bool fits = hc[C_OVF] == 0 && (int64_t)hc[C_MMAX] <= sp.M &&
+                        (hc[C_UNC] == 0 || sp.exc) && (int64_t)hc[C_NEXCMAX] <= sp.nexc &&
+                        (int64_t)hc[C_WMAXALL] < sp.R && (int64_t)hc[C_ITEMSMAX] <= sp.items;
+      if (!fits) {
+        sp.valid = false;
+        spec = false;
+        resized = true;
+        ++ctx->spec_redo;
+        continue;
+      }
+      if (2 * (int64_t)hc[C_MMAX] < sp.M) sp.valid = false;
+    } else {
+      sp = ctx->probe;
+      sp.valid = true;
+    }
+    break;
+    }
+    ctx->spec_on = false;
     int nm = 0;
     for (int t = 0; t < G.ntiles; ++t)
       if (own[t] == rank) {
@@ -2303,11 +2340,13 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       CK(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
       PhaseTimes pt;
       collect_phases(ctx, bi.n_sub, &pt);
-      fill_stats(ctx, bi, G, nm, pt, tot, stats);
+      fill_stats(ctx, bi, G, nm, pt, tot, stats, hc);
+      stats->resized = resized ? 1 : 0;
     }
     if (!(flags & AS_ASYNC)) CK(cudaStreamSynchronize(s));
     return AS_OK;
   } catch (const Err& e) {
+    ctx->spec_on = false;
     return e.st;
   }
 }

@@ -211,3 +211,28 @@ def test_state_changes_retire_the_graph(Context, change):
     finally:
         f.close()
     assert np.array_equal(a_lo, flo.cpu().numpy()) and np.array_equal(a_hi, fhi.cpu().numpy())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_renders_go_sync_free_per_rank(Context, world):
+    """as_render_shard remembers sizes per (shape, world, rank): each rank's second render has
+    no host read inside the pipeline and equals its first bit for bit."""
+    w = make_config("C4", N=8000, res=96)
+    ctx = Context(0)
+    try:
+        ctx.load_workload(w)
+        nt = ctx.n_tiles(16)
+        cap = -(-nt // world) + 2
+        first = []
+        for r in range(world):
+            a, b, o, n, st = ctx.as_render_shard(16, 64, r, world, cap)
+            assert st["host_syncs"] > 0
+            first.append((a.cpu().numpy().copy(), b.cpu().numpy().copy(), list(o[:n])))
+        for r in range(world):
+            a, b, o, n, st = ctx.as_render_shard(16, 64, r, world, cap)
+            assert st["host_syncs"] == 0 and st["resized"] == 0, (r, st["host_syncs"])
+            assert list(o[:n]) == first[r][2]
+            assert np.array_equal(a.cpu().numpy()[:n], first[r][0][:n])
+            assert np.array_equal(b.cpu().numpy()[:n], first[r][1][:n])
+    finally:
+        ctx.close()
