@@ -109,6 +109,11 @@ struct as_ctx {
   // ranks run in turn on one context, each with its own pair and item counts
   std::map<uint64_t, Sizes> shard_spec;
   Sizes* cur_spec = &spec;  // the sizes a sync-free render_subbox takes (render or shard cache)
+  // as_render_shard's owner map (LPT over the cost pass's per-tile pair counts) is a function of
+  // the state: kept while gen, tile, world and the per-rank capacity are unchanged
+  bool lpt_valid = false;
+  uint64_t lpt_gen = 0;
+  int lpt_tile = 0, lpt_world = 0, lpt_cap = 0;
   // CUDA graph of the sync-free pipeline: captured on the render after a sync-free one that
   // allocated nothing, replayed while the key holds.  gen counts every state-changing API
   // call, alloc_gen every (re)allocation; both are part of the key.
@@ -1999,6 +2004,7 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
           const int cap = per + std::max(1, per / 4);
           tile_costs_dev(ctx, bi, G, s0, s1);
           device_lpt(ctx, G, world, cap);
+          ctx->lpt_valid = false;  // the shard entry point's map is overwritten
           ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
           k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
               P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
@@ -2210,6 +2216,7 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
     prepare_common(ctx, bi, G);
     tile_costs_dev(ctx, bi, G, 0, bi.n_sub);
     device_lpt(ctx, G, world, max_tiles);
+    ctx->lpt_valid = false;
     CK(cudaMemcpyAsync(owner, ctx->owner.p, sizeof(int32_t) * G.ntiles, cudaMemcpyDeviceToHost,
                        ctx->stream));
     std::vector<unsigned long long> c(G.ntiles);
@@ -2226,7 +2233,8 @@ as_status as_tile_owners(as_ctx* ctx, int32_t tile, int32_t world, int32_t max_t
 as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank, int32_t world,
                           float* lo_tm, float* hi_tm, int32_t max_tiles, int32_t* owned,
                           int32_t* n_owned, int32_t flags, as_stats* stats) {
-  if (ctx) ++ctx->gen;  // state (or buffers) may change: no stale graph replay
+  // (no generation bump: a shard render changes no state a render graph depends on; any
+  // reallocation moves alloc_gen)
   as_status st = check_ready(ctx);
   if (st != AS_OK) return st;
   BoxInfo bi;
@@ -2266,11 +2274,21 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
     ctx->probe = as_ctx::Sizes{};
     if (stats) CK(cudaEventRecord(ctx->ev[0], s));
     prepare_common(ctx, bi, G);
-    // ---- owner map (identical on every rank): LPT over per-tile pair counts, on the device
-    if (world > 1) {
+    // ---- owner map (identical on every rank): LPT over per-tile pair counts, on the device;
+    // unchanged state: the map of the previous call (no cost pass)
+    const bool reuse_lpt = world > 1 && ctx->lpt_valid && ctx->lpt_gen == ctx->gen &&
+                           ctx->lpt_tile == tile && ctx->lpt_world == world &&
+                           ctx->lpt_cap == max_tiles;
+    if (world > 1 && !reuse_lpt) {
       tile_costs_dev(ctx, bi, G, 0, bi.n_sub);
       device_lpt(ctx, G, world, max_tiles);
-    } else {
+      ctx->lpt_valid = true;
+      ctx->lpt_gen = ctx->gen;
+      ctx->lpt_tile = tile;
+      ctx->lpt_world = world;
+      ctx->lpt_cap = max_tiles;
+    } else if (world == 1) {
+      ctx->lpt_valid = false;  // the owner map is overwritten
       ensure(ctx, ctx->tslot_all, sizeof(int32_t) * G.ntiles);
       CK(cudaMemsetAsync(ctx->owner.p, 0, sizeof(int32_t) * G.ntiles, s));
       k_seq<<<(G.ntiles + 255) / 256, 256, 0, s>>>(P<int32_t>(ctx->tslot_all), G.ntiles);
@@ -2290,7 +2308,7 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
     }
     ctx->last_out_tiles = max_tiles;
     for (int sb = 0; sb < bi.n_sub; ++sb) {
-      const bool need_setup = !(world > 1 && bi.n_sub == 1);  // cost pass left sub-box 0
+      const bool need_setup = !(world > 1 && bi.n_sub == 1 && !reuse_lpt);  // cost pass left it
       render_subbox(ctx, bi, sb, need_setup, G, batch, P<int32_t>(ctx->owner), rank,
                     P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), dlo, dhi, sb == 0,
                     stats ? sub_events(ctx, sb) : nullptr);
