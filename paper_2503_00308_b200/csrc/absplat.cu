@@ -113,7 +113,7 @@ struct as_ctx {
   // the state: kept while gen, tile, world and the per-rank capacity are unchanged
   bool lpt_valid = false;
   uint64_t lpt_gen = 0;
-  int lpt_tile = 0, lpt_world = 0, lpt_cap = 0;
+  int lpt_tile = 0, lpt_world = 0, lpt_cap = 0, lpt_s0 = 0, lpt_s1 = 0;
   // CUDA graph of the sync-free pipeline: captured on the render after a sync-free one that
   // allocated nothing, replayed while the key holds.  gen counts every state-changing API
   // call, alloc_gen every (re)allocation; both are part of the key.
@@ -2002,9 +2002,22 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
           // into a compact tile-major buffer, ONE all-gather, the untile on the device
           const int per = (G.ntiles + world - 1) / world;
           const int cap = per + std::max(1, per / 4);
-          tile_costs_dev(ctx, bi, G, s0, s1);
-          device_lpt(ctx, G, world, cap);
-          ctx->lpt_valid = false;  // the shard entry point's map is overwritten
+          // the owner map of an unchanged state is kept (no cost pass on repeated renders;
+          // every rank takes the same decision: same calls, same state)
+          const bool reuse_lpt = ctx->lpt_valid && ctx->lpt_gen == ctx->gen &&
+                                 ctx->lpt_tile == tile && ctx->lpt_world == world &&
+                                 ctx->lpt_cap == cap && ctx->lpt_s0 == s0 && ctx->lpt_s1 == s1;
+          if (!reuse_lpt) {
+            tile_costs_dev(ctx, bi, G, s0, s1);
+            device_lpt(ctx, G, world, cap);
+            ctx->lpt_valid = true;
+            ctx->lpt_gen = ctx->gen;
+            ctx->lpt_tile = tile;
+            ctx->lpt_world = world;
+            ctx->lpt_cap = cap;
+            ctx->lpt_s0 = s0;
+            ctx->lpt_s1 = s1;
+          }
           ensure(ctx, ctx->untile_map, sizeof(int32_t) * G.ntiles);
           k_slot_maps<<<(G.ntiles + 255) / 256, 256, 0, s>>>(
               P<int32_t>(ctx->owner), P<int32_t>(ctx->tslot_all), G.ntiles, rank, cap,
@@ -2020,7 +2033,8 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
           LAUNCHED(ctx, 1);
           ctx->last_out_tiles = cap;
           for (int sb = s0; sb < s1; ++sb)
-            render_subbox(ctx, bi, sb, s1 - s0 != 1, G, batch, P<int32_t>(ctx->owner), rank,
+            render_subbox(ctx, bi, sb, s1 - s0 != 1 || reuse_lpt, G, batch,
+                          P<int32_t>(ctx->owner), rank,
                           P<int32_t>(ctx->tlist), 0, P<int32_t>(ctx->tslot), slo, shi, sb == s0,
                           stats ? sub_events(ctx, sb - s0) : nullptr);
           CK(timing_record(ctx->ev[3], s));
@@ -2278,7 +2292,8 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
     // unchanged state: the map of the previous call (no cost pass)
     const bool reuse_lpt = world > 1 && ctx->lpt_valid && ctx->lpt_gen == ctx->gen &&
                            ctx->lpt_tile == tile && ctx->lpt_world == world &&
-                           ctx->lpt_cap == max_tiles;
+                           ctx->lpt_cap == max_tiles && ctx->lpt_s0 == 0 &&
+                           ctx->lpt_s1 == bi.n_sub;
     if (world > 1 && !reuse_lpt) {
       tile_costs_dev(ctx, bi, G, 0, bi.n_sub);
       device_lpt(ctx, G, world, max_tiles);
@@ -2287,6 +2302,8 @@ as_status as_render_shard(as_ctx* ctx, int32_t tile, int32_t batch, int32_t rank
       ctx->lpt_tile = tile;
       ctx->lpt_world = world;
       ctx->lpt_cap = max_tiles;
+      ctx->lpt_s0 = 0;
+      ctx->lpt_s1 = bi.n_sub;
     } else if (world == 1) {
       ctx->lpt_valid = false;  // the owner map is overwritten
       ensure(ctx, ctx->tslot_all, sizeof(int32_t) * G.ntiles);

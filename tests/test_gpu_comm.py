@@ -35,6 +35,10 @@ def test_single_rank_collective_equals_plain(torch_cuda, name, kw, axis):
         lo, hi, st = c.as_render_bounds(w.tile, w.batch)
         assert torch.equal(lo, lo0) and torch.equal(hi, hi0)
         assert st["world"] == 1 and st["ms_gather"] > 0
+        # again: the tile axis keeps its owner map (no cost pass), same images
+        lo2, hi2, st2 = c.as_render_bounds(w.tile, w.batch)
+        assert torch.equal(lo2, lo0) and torch.equal(hi2, hi0)
+        assert st2["pairs"] == st["pairs"] and st2["active_pairs"] == st["active_pairs"]
         if axis == 1:
             assert st["n_owned"] == c.n_tiles(w.tile)
 
