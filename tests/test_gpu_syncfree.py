@@ -236,3 +236,53 @@ def test_shard_renders_go_sync_free_per_rank(Context, world):
             assert np.array_equal(b.cpu().numpy()[:n], first[r][1][:n])
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("seed", [5, 6, 7])
+def test_random_call_sequences_match_fresh_contexts(Context, seed):
+    """Fuzz of the caching machinery (remembered sizes, render graphs, the kept owner map):
+    a random sequence of state changes and renders on one context; every render equals a fresh
+    context's render of the same state bit for bit."""
+    import torch
+    rng = np.random.default_rng(seed)
+    shapes = [stacked_config(N=200, rot_deg=0.4), stacked_config(N=350, rot_deg=0.8, axis_frac=0.5),
+              make_config("C3", N=3000, res=48)]
+    ctx = Context(0)
+    cur = None
+    target = 0
+    outs = {}
+    try:
+        for step in range(60):
+            op = rng.integers(0, 6) if cur is not None else 0
+            if op == 0:
+                cur = int(rng.integers(0, len(shapes)))
+                ctx.load_workload(shapes[cur])
+                ctx.as_set_chunk_target(target)
+            elif op == 1:
+                target = int(rng.choice([0, 7, 40]))
+                ctx.as_set_chunk_target(target)
+            w = shapes[cur]
+            H, W = w.camera["H"], w.camera["W"]
+            key = (cur, target)
+            if key not in outs:
+                f = Context(0)
+                try:
+                    f.load_workload(w)
+                    f.as_set_chunk_target(target)
+                    a, b, _ = f.as_render_bounds(tile=w.tile, batch=w.batch)
+                    outs[key] = (a.cpu().numpy(), b.cpu().numpy())
+                finally:
+                    f.close()
+            if rng.uniform() < 0.5:  # device outputs (graph-capable) or host-side tensors
+                lo = torch.empty((H, W, 3), dtype=torch.float32, device="cuda:0")
+                hi = torch.empty_like(lo)
+                ctx.as_render_bounds(w.tile, w.batch, lo, hi, stats=bool(rng.integers(0, 2)))
+            else:
+                lo, hi, _ = ctx.as_render_bounds(tile=w.tile, batch=w.batch)
+            assert np.array_equal(lo.cpu().numpy(), outs[key][0]), (step, key)
+            assert np.array_equal(hi.cpu().numpy(), outs[key][1]), (step, key)
+            if rng.uniform() < 0.25:  # a shard render in between (owner map, shard sizes)
+                nt = ctx.n_tiles(w.tile)
+                ctx.as_render_shard(w.tile, w.batch, int(rng.integers(0, 2)), 2, -(-nt // 2) + 2)
+    finally:
+        ctx.close()
