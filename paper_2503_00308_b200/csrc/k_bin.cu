@@ -249,7 +249,10 @@ __global__ void k_pairs_prep(PairArgs A) {
     s1 += fabs(Pi.dl[k] - m);
     s2 += fabs(Pi.du[k] - m);
   }
-  const double ws = 0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2);
+  // >= 0 by construction, clamped: rounding can leave the half-width of a zero-width constant
+  // a few ulp negative, and the tile maximum below compares bit patterns (a negative double's
+  // pattern orders above every positive one, which made M tiny and the window unsound)
+  const double ws = fmax(0.5 * (Pi.du[NV] - Pi.dl[NV]) + fmax(s1, s2), 0.0);
   if (p0 < A.M) {  // E_F accumulators of the forward-only classification (k_pairs PASS 0)
     A.mF[p] = make_ulonglong2(0ull, 0ull);
     A.nF[p] = 0;

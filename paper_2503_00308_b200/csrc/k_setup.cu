@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(128, 4) k_setup(SetupArgs A) {
     }
     H->flags = fl;
     PairRec<NV>* PR = reinterpret_cast<PairRec<NV>*>(A.pair) + i;
-    const double ws = 0.5 * (dcu - dcl) + fmax(s1, s2);
+    const double ws = fmax(0.5 * (dcu - dcl) + fmax(s1, s2), 0.0);  // bit-pattern max below
     PR->kappa = kappa;
     PR->ws = ws;
     A.kkey[i] = (fl & F_DROP) ? ~0ull : key_of_double(kappa);

@@ -44,7 +44,10 @@ def _case(seed):
     return w, tile, batch
 
 
-@pytest.mark.parametrize("seed", range(40))
+# 120 sweep cases plus three that once exposed a window bug: C5 translation boxes whose depth
+# constants have zero width, where rounding left the window term a few ulp negative and the
+# bit-pattern tile maximum went wrong (the GPU then missed half of the uncertain pairs)
+@pytest.mark.parametrize("seed", list(range(120)) + [2049, 2084, 2154])
 def test_random_parity(ctx, oracle, seed):
     w, tile, batch = _case(seed)
     ctx.load_workload(w)
