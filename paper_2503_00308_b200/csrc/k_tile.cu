@@ -856,15 +856,24 @@ constexpr int P2 = 256;  // pixels per block
 __host__ __device__ __forceinline__ int v2_x(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
 __host__ __device__ __forceinline__ int v2_y(int t) { return (t >> 6) * 8 + ((t >> 3) & 3); }
 
+#ifndef KT2_QC  // centre the fp32 forms on each warp's 8x8 quadrant (1) or on the 16x16 block (0)
+// 1 halves the fp32 cancellation of the block-centred forms (the 2000-case random sweep's one
+// case above 1e-4, a small Gaussian near a block edge at 1.8e-4, drops to 2.0e-5 as with 8x8
+// blocks) but costs 7-9% of the tile kernel (4x the centre-dependent staging, larger records,
+// smaller batches): off by default, the same precision is available with tile = 8
+#define KT2_QC 0
+#endif
+constexpr int NQ2 = KT2_QC ? 4 : 1;  // form centres per block
 template <int NV>
 struct alignas(16) SRec2 {
   static constexpr int C = NV + 1;
   static constexpr int CP = (C + 3) & ~3;
-  // lower x forms at the block centre: x_lo,a,k(u) = xb_a[k] + du_a d2[k]
-  float xb0[CP], xb1[CP], d2[CP];
+  // lower x forms at the form centre qc (the block's, or with KT2_QC the warp's 8x8 quadrant's):
+  // x_lo,a,k(u) = xb_a[qc][k] + du_a d2[k]
+  float xb0[NQ2][CP], xb1[NQ2][CP], d2[CP];
   // q_c's (mid, radius) coefficients as affine functions of (du0, du1, x0, |x0|, x1, |x1|):
   //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
-  float4 A[3][C];    // (pm, pr, q0m, q0r)
+  float4 A[NQ2][3][C];  // (pm, pr, q0m, q0r) per quadrant centre
   float4 B[3][C];    // (wm0, wr0, q1m, q1r)
   float2 W1[3][CP];  // (wm1, wr1)
   float4 WC[3];      // concretised W_0c, W_1c as (mid0, half0, mid1, half1)
@@ -909,34 +918,44 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
     const int k = part + NPART * i;
     if (k >= C) break;
     const double d2l = H->d2[0][k], d2h = H->d2[1][k];
-    double blo[2], bhi[2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      blo[a] = uc[a] * d2l - H->du[a][1][k];
-      bhi[a] = uc[a] * d2h - H->du[a][0][k];
-    }
     float wa[6], wb[6];
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
       wa[e] = H->w[e][0][k];
       wb[e] = H->w[e][1][k];
     }
-    S.xb0[k] = (float)blo[0];
-    S.xb1[k] = (float)blo[1];
     S.d2[k] = (float)d2l;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
-      const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
-      const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
-      const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q1lo = w1l * (w1l >= 0 ? d2l : d2h);
-      const double q0hi = w0h * (w0h >= 0 ? d2h : d2l), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
       const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
-      S.A[c][k] = make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
-                              (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+      const double q1lo = w1l * (w1l >= 0 ? d2l : d2h), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
       S.B[c][k] = make_float4((float)(0.5 * (a0 + b0)), (float)(0.5 * (b0 - a0)),
                               (float)(0.5 * (q1lo + q1hi)), (float)(0.5 * (q1hi - q1lo)));
       S.W1[c][k] = make_float2((float)(0.5 * (a1 + b1)), (float)(0.5 * (b1 - a1)));
+    }
+    // the centre-dependent terms, per form centre (quadrant centres: offsets of +-4 pixels)
+#pragma unroll
+    for (int qc = 0; qc < NQ2; ++qc) {
+      const double off[2] = {KT2_QC ? ((qc & 1) ? 4.0 : -4.0) : 0.0,
+                             KT2_QC ? ((qc >> 1) ? 4.0 : -4.0) : 0.0};
+      double blo[2], bhi[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        blo[a] = (uc[a] + off[a]) * d2l - H->du[a][1][k];
+        bhi[a] = (uc[a] + off[a]) * d2h - H->du[a][0][k];
+      }
+      S.xb0[qc][k] = (float)blo[0];
+      S.xb1[qc][k] = (float)blo[1];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+        const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
+        const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
+        const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q0hi = w0h * (w0h >= 0 ? d2h : d2l);
+        S.A[qc][c][k] = make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
+                                    (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+      }
     }
   }
 }
@@ -944,17 +963,18 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
 // steps 14-17 for the thread's two pixels (du0 shared; DU1 = (du1 of pixel 0, of pixel 1)):
 // returns (a_lo, a_hi) pairs.  Same per-pixel operations as s_forms / opacity.
 template <int NV>
-__device__ __forceinline__ void opacity2(const SRec2<NV>& R, float du0, float2 DU1, float2& alo,
-                                         float2& ahi) {
+__device__ __forceinline__ void opacity2(const SRec2<NV>& R, int qc, float du0, float2 DU1,
+                                         float2& alo, float2& ahi) {
   constexpr int C = NV + 1;
-  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel)
-  float x0 = fmaf(du0, R.d2[NV], R.xb0[NV]);
+  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel); du0 / DU1
+  // relative to the form centre qc
+  float x0 = fmaf(du0, R.d2[NV], R.xb0[qc][NV]);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(du0, R.d2[k], R.xb0[k]));
-  float2 X1 = __ffma2_rn(DU1, bc(R.d2[NV]), bc(R.xb1[NV]));
+  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(du0, R.d2[k], R.xb0[qc][k]));
+  float2 X1 = __ffma2_rn(DU1, bc(R.d2[NV]), bc(R.xb1[qc][NV]));
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const float2 v = __ffma2_rn(DU1, bc(R.d2[k]), bc(R.xb1[k]));
+    const float2 v = __ffma2_rn(DU1, bc(R.d2[k]), bc(R.xb1[qc][k]));
     X1 = __fadd2_rn(X1, f2(-fabsf(v.x), -fabsf(v.y)));
   }
   const float2 AX1 = f2(fabsf(X1.x), fabsf(X1.y));
@@ -969,7 +989,7 @@ __device__ __forceinline__ void opacity2(const SRec2<NV>& R, float du0, float2 D
     const float4 wc = R.WC[c];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      const float4 a = R.A[c][k], b = R.B[c][k];
+      const float4 a = R.A[qc][c][k], b = R.B[c][k];
       const float2 w1 = R.W1[c][k];
       float2 mr = __ffma2_rn(D0, f2(a.z, a.w), f2(a.x, a.y));
       mr = __ffma2_rn(X0, f2(b.x, b.y), mr);
@@ -1120,8 +1140,12 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   __syncthreads();
   unsigned phase = 0;
   const int lx = v2_x(tid), ly = v2_y(tid);
-  const float du0 = (float)lx + 0.5f - 0.5f * B2;
-  const float2 DU1 = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
+  // the warp's form centre: its 8x8 quadrant's centre (KT2_QC) or the block's
+  const int qcw = KT2_QC ? (tid >> 5) : 0;
+  const float cxq = KT2_QC ? (float)(((qcw & 1) ? 12 : 4)) : 0.5f * B2;
+  const float cyq = KT2_QC ? (float)(((qcw >> 1) ? 12 : 4)) : 0.5f * B2;
+  const float du0 = (float)lx + 0.5f - cxq;
+  const float2 DU1 = f2((float)ly + 0.5f - cyq, (float)ly + 4.5f - cyq);
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
 #ifdef KT2_PROF
@@ -1384,7 +1408,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
               ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
             } else {
               float2 l, h;
-              opacity2<NV>(R, du0, DU1, l, h);
+              opacity2<NV>(R, qcw, du0, DU1, l, h);
               const bool st = flags & F_STRADDLE;
               alo = f2(kA && !st ? l.x : 0.f, kB && !st ? l.y : 0.f);
               ahi = f2(kA ? h.x : 0.f, kB ? h.y : 0.f);
