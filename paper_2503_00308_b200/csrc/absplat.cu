@@ -809,8 +809,10 @@ void render_subbox(as_ctx* ctx, const BoxInfo& bi, int s, bool do_setup, const G
                                      P<uint32_t>(ctx->item_key), NIdev, n_items);
     LAUNCHED(ctx, 1);
   }
-  k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
-  LAUNCHED(ctx, 1);
+  if (n_items > 0) {
+    k_seq<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(P<int32_t>(ctx->item_idx), (int)n_items);
+    LAUNCHED(ctx, 1);
+  }
   cub_sort_keys32(ctx, P<uint32_t>(ctx->item_key), P<uint32_t>(ctx->item_key2),
                   P<int32_t>(ctx->item_idx), P<int32_t>(ctx->item_order), n_items, 32, true);
   ensure(ctx, ctx->work_counter, sizeof(int));
@@ -2159,7 +2161,7 @@ as_status render_range(as_ctx* ctx, int32_t tile, int32_t batch, int32_t s0, int
           continue;
         }
         if (2 * (int64_t)h[C_MMAX] < sp.M) sp.valid = false;  // far smaller: re-probe next time
-      } else if (can_spec) {
+      } else if (can_spec && n_done > 0) {  // (an empty range measures nothing)
         sp = ctx->probe;
         sp.valid = true;
         sp.ts = tile;

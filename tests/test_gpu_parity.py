@@ -146,8 +146,8 @@ def test_gpu_bounds_contain_concrete_renders(ctx, oracle, name):
 
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_equals_single(ctx, world):
-    """Tiles rendered rank by rank (sequentially on one GPU) and assembled with as_untile are
-    bitwise identical to the single-GPU image (north_star tile sharding)."""
+    """Tiles rendered rank by rank (sequentially on one GPU) and assembled with as_untile equal
+    the single-GPU image up to fp32 rounding (north_star tile sharding)."""
     import torch
     w = make_config("C4", N=8000, res=96)
     ctx.load_workload(w)
@@ -165,7 +165,10 @@ def test_sharded_equals_single(ctx, world):
     glo = torch.stack(tl)
     ghi = torch.stack(th)
     ulo, uhi = ctx.as_untile(16, world, cap, np.stack(owned), np.array(nown, np.int32), glo, ghi)
-    assert torch.equal(ulo, lo) and torch.equal(uhi, hi)
+    # a rank chunks its tiles for its own share of the pairs: the composition order of a split
+    # tile may differ from the full render's, so equality is up to fp32 rounding (bit for bit
+    # in this case; tools/api_sweep.py found 1-ulp differences at TS 32)
+    assert (ulo - lo).abs().max().item() <= 1e-6 and (uhi - hi).abs().max().item() <= 1e-6
     owner, costs = ctx.as_tile_owners(16, world, cap)
     for r in range(world):
         assert sorted(np.nonzero(owner == r)[0].tolist()) == sorted(owned[r][:nown[r]].tolist())
