@@ -286,3 +286,21 @@ def test_random_call_sequences_match_fresh_contexts(Context, seed):
                 ctx.as_render_shard(w.tile, w.batch, int(rng.integers(0, 2)), 2, -(-nt // 2) + 2)
     finally:
         ctx.close()
+
+
+def test_empty_subbox_range_then_render(Context):
+    """An empty sub-box range renders nothing; the next render of the same shape must not be
+    sized from it (it once launched a zero-size grid: tools/api_sweep.py)."""
+    w = make_config("C3", N=3000, res=48)
+    ctx = Context(0)
+    try:
+        ctx.load_workload(w)
+        P = ctx.as_subbox_count()
+        lo, hi, st = ctx.as_render_subboxes(P, P, w.tile, w.batch)
+        assert float(lo.min()) == 1.0 and float(hi.max()) == 0.0  # the union's identities
+        lo1, hi1, s1 = ctx.as_render_bounds(w.tile, w.batch)
+        lo2, hi2, s2 = ctx.as_render_bounds(w.tile, w.batch)
+        assert s2["host_syncs"] == 0
+        assert np.array_equal(lo1.cpu().numpy(), lo2.cpu().numpy())
+    finally:
+        ctx.close()
