@@ -856,14 +856,19 @@ constexpr int P2 = 256;  // pixels per block
 __host__ __device__ __forceinline__ int v2_x(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
 __host__ __device__ __forceinline__ int v2_y(int t) { return (t >> 6) * 8 + ((t >> 3) & 3); }
 
-#ifndef KT2_QC  // centre the fp32 forms on each warp's 8x8 quadrant (1) or on the 16x16 block (0)
-// 1 halves the fp32 cancellation of the block-centred forms (the 2000-case random sweep's one
-// case above 1e-4, a small Gaussian near a block edge at 1.8e-4, drops to 2.0e-5 as with 8x8
-// blocks) but costs 7-9% of the tile kernel (4x the centre-dependent staging, larger records,
-// smaller batches): off by default, the same precision is available with tile = 8
+#ifndef KT2_QC  // form centring: 0 the 16x16 block, 1 or 2 each warp's 8x8 quadrant (see below)
+// 1 and 2 halve the fp32 cancellation of the block-centred forms (the random sweeps' cases
+// above 1e-4, a small Gaussian near a block edge at up to 2.4e-4, drop to ~2e-5 as with 8x8
+// blocks) but cost 7-8% of the tile kernel (mode 1: 4x the centre-dependent staging, larger
+// records, smaller batches; mode 2: the per-quadrant constants' loads and registers): off by
+// default, the same precision is available with tile = 8
 #define KT2_QC 0
 #endif
-constexpr int NQ2 = KT2_QC ? 4 : 1;  // form centres per block
+// 0: forms at the 16x16 block centre; 1: everything at each warp's 8x8 quadrant centre;
+// 2: only the q-form constants (pm, pr) per quadrant (the terms whose fp32 rounding matters;
+//    x_b stays block-centred), stored compactly: quadrant 0 in A.xy, quadrants 1-3 in PQ
+constexpr int NQ2 = KT2_QC == 1 ? 4 : 1;   // x_b / A centres
+constexpr int NPQ = KT2_QC == 2 ? 3 : 1;   // extra (pm, pr) quadrants (dummy 1 when unused)
 template <int NV>
 struct alignas(16) SRec2 {
   static constexpr int C = NV + 1;
@@ -873,7 +878,8 @@ struct alignas(16) SRec2 {
   float xb0[NQ2][CP], xb1[NQ2][CP], d2[CP];
   // q_c's (mid, radius) coefficients as affine functions of (du0, du1, x0, |x0|, x1, |x1|):
   //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
-  float4 A[NQ2][3][C];  // (pm, pr, q0m, q0r) per quadrant centre
+  float4 A[NQ2][3][C];  // (pm, pr, q0m, q0r) per quadrant centre (KT2_QC 2: quadrant 0's)
+  float2 PQ[NPQ][3][C];  // KT2_QC 2: (pm, pr) of quadrants 1-3
   float4 B[3][C];    // (wm0, wr0, q1m, q1r)
   float2 W1[3][CP];  // (wm1, wr1)
   float4 WC[3];      // concretised W_0c, W_1c as (mid0, half0, mid1, half1)
@@ -935,26 +941,38 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
       S.W1[c][k] = make_float2((float)(0.5 * (a1 + b1)), (float)(0.5 * (b1 - a1)));
     }
     // the centre-dependent terms, per form centre (quadrant centres: offsets of +-4 pixels)
+    constexpr int NC = KT2_QC == 2 ? 4 : NQ2;  // centres computed
 #pragma unroll
-    for (int qc = 0; qc < NQ2; ++qc) {
-      const double off[2] = {KT2_QC ? ((qc & 1) ? 4.0 : -4.0) : 0.0,
-                             KT2_QC ? ((qc >> 1) ? 4.0 : -4.0) : 0.0};
+    for (int qc = 0; qc < NC; ++qc) {
+      const bool quad = KT2_QC != 0;
+      const double off[2] = {quad ? ((qc & 1) ? 4.0 : -4.0) : 0.0,
+                             quad ? ((qc >> 1) ? 4.0 : -4.0) : 0.0};
       double blo[2], bhi[2];
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
         blo[a] = (uc[a] + off[a]) * d2l - H->du[a][1][k];
         bhi[a] = (uc[a] + off[a]) * d2h - H->du[a][0][k];
       }
-      S.xb0[qc][k] = (float)blo[0];
-      S.xb1[qc][k] = (float)blo[1];
+      if (KT2_QC != 2) {
+        S.xb0[qc][k] = (float)blo[0];
+        S.xb1[qc][k] = (float)blo[1];
+      } else if (qc == 0) {  // x_b at the block centre
+        S.xb0[0][k] = (float)(uc[0] * d2l - H->du[0][1][k]);
+        S.xb1[0][k] = (float)(uc[1] * d2l - H->du[1][1][k]);
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
         const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
         const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
         const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q0hi = w0h * (w0h >= 0 ? d2h : d2l);
-        S.A[qc][c][k] = make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
-                                    (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+        if (KT2_QC == 2 && qc > 0) {
+          S.PQ[qc - 1][c][k] = make_float2((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)));
+        } else {
+          S.A[KT2_QC == 2 ? 0 : qc][c][k] =
+              make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
+                          (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
+        }
       }
     }
   }
@@ -964,17 +982,20 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
 // returns (a_lo, a_hi) pairs.  Same per-pixel operations as s_forms / opacity.
 template <int NV>
 __device__ __forceinline__ void opacity2(const SRec2<NV>& R, int qc, float du0, float2 DU1,
-                                         float2& alo, float2& ahi) {
+                                         float du0b, float2 DU1b, float2& alo, float2& ahi) {
   constexpr int C = NV + 1;
-  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel); du0 / DU1
-  // relative to the form centre qc
-  float x0 = fmaf(du0, R.d2[NV], R.xb0[qc][NV]);
+  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel), around the
+  // x_b centre (the quadrant's with KT2_QC 1, else the block's: du0b / DU1b)
+  const int qx = KT2_QC == 1 ? qc : 0;
+  const float dx0 = KT2_QC == 1 ? du0 : du0b;
+  const float2 DX1 = KT2_QC == 1 ? DU1 : DU1b;
+  float x0 = fmaf(dx0, R.d2[NV], R.xb0[qx][NV]);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(du0, R.d2[k], R.xb0[qc][k]));
-  float2 X1 = __ffma2_rn(DU1, bc(R.d2[NV]), bc(R.xb1[qc][NV]));
+  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(dx0, R.d2[k], R.xb0[qx][k]));
+  float2 X1 = __ffma2_rn(DX1, bc(R.d2[NV]), bc(R.xb1[qx][NV]));
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const float2 v = __ffma2_rn(DU1, bc(R.d2[k]), bc(R.xb1[qc][k]));
+    const float2 v = __ffma2_rn(DX1, bc(R.d2[k]), bc(R.xb1[qx][k]));
     X1 = __fadd2_rn(X1, f2(-fabsf(v.x), -fabsf(v.y)));
   }
   const float2 AX1 = f2(fabsf(X1.x), fabsf(X1.y));
@@ -989,7 +1010,13 @@ __device__ __forceinline__ void opacity2(const SRec2<NV>& R, int qc, float du0, 
     const float4 wc = R.WC[c];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      const float4 a = R.A[qc][c][k], b = R.B[c][k];
+      float4 a = R.A[KT2_QC == 1 ? qc : 0][c][k];
+      const float4 b = R.B[c][k];
+      if (KT2_QC == 2 && qc > 0) {  // this quadrant's q-form constants
+        const float2 pq = R.PQ[qc - 1][c][k];
+        a.x = pq.x;
+        a.y = pq.y;
+      }
       const float2 w1 = R.W1[c][k];
       float2 mr = __ffma2_rn(D0, f2(a.z, a.w), f2(a.x, a.y));
       mr = __ffma2_rn(X0, f2(b.x, b.y), mr);
@@ -1146,6 +1173,8 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   const float cyq = KT2_QC ? (float)(((qcw >> 1) ? 12 : 4)) : 0.5f * B2;
   const float du0 = (float)lx + 0.5f - cxq;
   const float2 DU1 = f2((float)ly + 0.5f - cyq, (float)ly + 4.5f - cyq);
+  const float du0b = (float)lx + 0.5f - 0.5f * B2;  // relative to the block centre
+  const float2 DU1b = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
 #ifdef KT2_PROF
@@ -1408,7 +1437,7 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
               ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
             } else {
               float2 l, h;
-              opacity2<NV>(R, qcw, du0, DU1, l, h);
+              opacity2<NV>(R, qcw, du0, DU1, du0b, DU1b, l, h);
               const bool st = flags & F_STRADDLE;
               alo = f2(kA && !st ? l.x : 0.f, kB && !st ? l.y : 0.f);
               ahi = f2(kA ? h.x : 0.f, kB ? h.y : 0.f);
