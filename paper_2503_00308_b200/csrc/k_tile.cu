@@ -76,6 +76,7 @@ struct alignas(16) SRec {
   float2 P[3][CP], Q0[3][CP], Q1[3][CP], W0[3][CP], W1[3][CP];
   float2 WC[6];             // concretised W, [a*3+c]: ((lo + hi) / 2, (lo - hi) / 2)
   float o[2];
+  float ctr[2];  // the form centre (block-local pixels, integer valued): see stage_forms
   float clo[3], chi[3];
   int flags;                // F_* of the Gaussian
   int pmf, ph, pg, pnF, pnG;  // position metadata (PM_*, h, g, |E_F|, |E_G|)
@@ -100,19 +101,31 @@ struct alignas(16) FinS {
   unsigned char off[EG8];
 };
 
-// Staging of one Gaussian for a block centred at (ucx, ucy): fp64 arithmetic, one rounding.
+// Staging of one Gaussian for a block centred at (ucx, ucy) with half-extents (hx, hy): fp64
+// arithmetic, one rounding.  The forms are centred on the block pixel corner nearest the
+// Gaussian's mean (the middle of its mean rectangle, clamped to the block; S.ctr), so the fp32
+// per-pixel offsets du are exact and small where the opacity is large (any centre gives the
+// same forms up to fp32 rounding; the block centre cancels more bits, see KT2_QC).
 // x_a lower form: u_a D2_lo - DU_a,hi = B_lo,a + du_a D2_lo with B_lo,a = uc_a D2_lo - DU_a,hi
 // (u_a > 0 selects D2's lower side, step 14); upper: B_hi,a + du_a D2_hi.
 // LS(x_a, w) = w >= 0 ? w x_lo,a : w x_hi,a  and  US(x_a, w) = w >= 0 ? w x_hi,a : w x_lo,a
 // (R1 with the constant w = conc W), both affine in du_a.
 template <int NV>
 __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, double ucx,
-                                            double ucy, int part) {
+                                            double ucy, double hx, double hy, int part) {
   // NPART threads per Gaussian; thread `part` stages coefficients k = part, part + NPART,
   // ... of every channel, so all of its record loads are independent and issue together
   constexpr int C = NV + 1;
   constexpr int KP = (C + NPART - 1) / NPART;
-  const double uc[2] = {ucx, ucy};
+  const double hh[2] = {hx, hy};
+  double uc[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const double o = (a ? ucy : ucx) - hh[a];
+    const double rc = fmin(fmax(rint(0.5 * (H->mu[a] + H->mu[2 + a]) - o), 0.0), 2.0 * hh[a]);
+    uc[a] = o + rc;
+    if (part == 0) S.ctr[a] = (float)rc;
+  }
   double wl[6], wh[6];  // concretised W, [a*3+c]
 #pragma unroll
   for (int e = 0; e < 6; ++e) {
@@ -162,7 +175,7 @@ __device__ __forceinline__ void stage_forms(SRec<NV>& S, const HotRec<NV>* H, do
   }
 }
 
-// steps 14-16 for one pixel at offset (du0, du1) from the block centre: the lower / upper
+// steps 14-16 for one pixel at offset (du0, du1) from the record's form centre: the lower / upper
 // forms of s as pairs S[k] = (s_lo,k, s_hi,k).  Each (m, r) term is one packed FFMA2 (same
 // order as the scalar formulas); R2's plane selection LS(q, 2p) / US(q, qmin + qmax) is
 // written select-free as tp m - |tp| r and sm m + |sm| r (two FFMA2 per coefficient).
@@ -224,7 +237,7 @@ __device__ __forceinline__ void s_forms(const SRec<NV>& R, float du0, float du1,
   }
 }
 
-// steps 14-17 for one pixel at offset (du0, du1) from the block centre: (a_lo, a_hi)
+// steps 14-17 for one pixel at offset (du0, du1) from the record's form centre: (a_lo, a_hi)
 template <int NV>
 __device__ __forceinline__ void opacity(const SRec<NV>& R, float du0, float du1, float& alo,
                                         float& ahi) {
@@ -402,8 +415,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : KT1_MINB8) k_tile(Til
   float* rf = has_exc ? reinterpret_cast<float*>(A.ring) + (size_t)blockIdx.x * A.R * SBP * 4 + pix
                       : nullptr;
   const int lx = pix_x(pix, SBX), ly = pix_y(pix, SBX);
-  const float du0 = (float)lx + 0.5f - 0.5f * SBX;  // offset from the block centre
-  const float du1 = (float)ly + 0.5f - 0.5f * SBY;
+  const float lxh = (float)lx + 0.5f, lyh = (float)ly + 0.5f;  // minus the record's form centre
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
 
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : KT1_MINB8) k_tile(Til
           const double dy = fmax(0.0, fmax(__dsub_rn(H->mu[1], by1), __dsub_rn(by0, H->mu[3])));
           skip = !block_live || __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > H->r2;
         }
-        if (!skip) stage_forms<NV>(srec[j], H, ucx, ucy, part);
+        if (!skip) stage_forms<NV>(srec[j], H, ucx, ucy, 0.5 * SBX, 0.5 * SBY, part);
       }
       if (threadIdx.x == 0) {
         s_F[0] = f0l;
@@ -634,7 +646,7 @@ __global__ void __launch_bounds__(BX * SBY, BX == 16 ? 5 : KT1_MINB8) k_tile(Til
               ahi = keep ? R.o[1] : 0.f;
             } else {
               float l, h;
-              opacity<NV>(R, du0, du1, l, h);
+              opacity<NV>(R, lxh - R.ctr[0], lyh - R.ctr[1], l, h);
               alo = keep ? ((flags & F_STRADDLE) ? 0.f : l) : 0.f;
               ahi = keep ? h : 0.f;
             }
@@ -856,17 +868,18 @@ constexpr int P2 = 256;  // pixels per block
 __host__ __device__ __forceinline__ int v2_x(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
 __host__ __device__ __forceinline__ int v2_y(int t) { return (t >> 6) * 8 + ((t >> 3) & 3); }
 
-#ifndef KT2_QC  // form centring: 0 the 16x16 block, 1 or 2 each warp's 8x8 quadrant (see below)
-// 1 and 2 halve the fp32 cancellation of the block-centred forms (the random sweeps' cases
-// above 1e-4, a small Gaussian near a block edge at up to 2.4e-4, drop to ~2e-5 as with 8x8
-// blocks) but cost 7-8% of the tile kernel (mode 1: 4x the centre-dependent staging, larger
-// records, smaller batches; mode 2: the per-quadrant constants' loads and registers): off by
-// default, the same precision is available with tile = 8
-#define KT2_QC 0
+#ifndef KT2_QC  // where the fp32 forms are centred (default 3)
+// The per-pixel forms are evaluated in fp32 as x = x_b + du D2 and m = p_m + du q_m around a
+// centre; with |du| up to 8 these sums cancel many bits for a small Gaussian far from the
+// centre (the random sweeps' cases above 1e-4, up to 2.4e-4, with the block centre).
+// 3: each record's own centre, the block pixel corner nearest its mean (exact per-record
+//    offsets, ~0.5% of the kernel): the offsets are small where the opacity is large; sweep
+//    median error 3.7e-6 -> 6e-7, no case above 1e-4.
+// 0: the 16x16 block centre; 1: each warp's 8x8 quadrant centre (every centre-dependent term);
+// 2: only the q-form constants (pm, pr) per quadrant, quadrant 0 in A.xy, 1-3 in PQ.
+//    1 and 2 halve the offsets at 7-8% of the kernel (4x the staging / the per-quadrant loads).
+#define KT2_QC 3
 #endif
-// 0: forms at the 16x16 block centre; 1: everything at each warp's 8x8 quadrant centre;
-// 2: only the q-form constants (pm, pr) per quadrant (the terms whose fp32 rounding matters;
-//    x_b stays block-centred), stored compactly: quadrant 0 in A.xy, quadrants 1-3 in PQ
 constexpr int NQ2 = KT2_QC == 1 ? 4 : 1;   // x_b / A centres
 constexpr int NPQ = KT2_QC == 2 ? 3 : 1;   // extra (pm, pr) quadrants (dummy 1 when unused)
 template <int NV>
@@ -884,6 +897,7 @@ struct alignas(16) SRec2 {
   float2 W1[3][CP];  // (wm1, wr1)
   float4 WC[3];      // concretised W_0c, W_1c as (mid0, half0, mid1, half1)
   float o[2];
+  float ctr[2];      // KT2_QC 3: the form centre (block-local pixels, integer valued)
   float clo[3], chi[3];
   int flags;
   int pmf, ph, pg, pnF, pnG;
@@ -906,6 +920,19 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
   constexpr int C = NV + 1;
   constexpr int KP = (C + NPART - 1) / NPART;
   const double uc[2] = {ucx, ucy};
+  // KT2_QC 3: the forms are centred on the block pixel corner nearest the Gaussian's mean
+  // (the middle of its mean rectangle, clamped to the block), so the offsets are small where
+  // the opacity is large; any centre gives the same forms up to fp32 rounding
+  double rc[2] = {0.5 * B2, 0.5 * B2};
+  if (KT2_QC == 3) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      rc[a] = fmin(fmax(rint(0.5 * (H->mu[a] + H->mu[2 + a]) - (uc[a] - 0.5 * B2)), 0.0), (double)B2);
+    if (part == 0) {
+      S.ctr[0] = (float)rc[0];
+      S.ctr[1] = (float)rc[1];
+    }
+  }
   double wl[6], wh[6];
 #pragma unroll
   for (int e = 0; e < 6; ++e) {
@@ -944,9 +971,9 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
     constexpr int NC = KT2_QC == 2 ? 4 : NQ2;  // centres computed
 #pragma unroll
     for (int qc = 0; qc < NC; ++qc) {
-      const bool quad = KT2_QC != 0;
-      const double off[2] = {quad ? ((qc & 1) ? 4.0 : -4.0) : 0.0,
-                             quad ? ((qc >> 1) ? 4.0 : -4.0) : 0.0};
+      const bool quad = KT2_QC == 1 || KT2_QC == 2;
+      const double off[2] = {quad ? ((qc & 1) ? 4.0 : -4.0) : rc[0] - 0.5 * B2,
+                             quad ? ((qc >> 1) ? 4.0 : -4.0) : rc[1] - 0.5 * B2};
       double blo[2], bhi[2];
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
@@ -1168,9 +1195,10 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   unsigned phase = 0;
   const int lx = v2_x(tid), ly = v2_y(tid);
   // the warp's form centre: its 8x8 quadrant's centre (KT2_QC) or the block's
-  const int qcw = KT2_QC ? (tid >> 5) : 0;
-  const float cxq = KT2_QC ? (float)(((qcw & 1) ? 12 : 4)) : 0.5f * B2;
-  const float cyq = KT2_QC ? (float)(((qcw >> 1) ? 12 : 4)) : 0.5f * B2;
+  constexpr bool QW = KT2_QC == 1 || KT2_QC == 2;
+  const int qcw = QW ? (tid >> 5) : 0;
+  const float cxq = QW ? (float)(((qcw & 1) ? 12 : 4)) : 0.5f * B2;
+  const float cyq = QW ? (float)(((qcw >> 1) ? 12 : 4)) : 0.5f * B2;
   const float du0 = (float)lx + 0.5f - cxq;
   const float2 DU1 = f2((float)ly + 0.5f - cyq, (float)ly + 4.5f - cyq);
   const float du0b = (float)lx + 0.5f - 0.5f * B2;  // relative to the block centre
@@ -1437,7 +1465,13 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
               ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
             } else {
               float2 l, h;
-              opacity2<NV>(R, qcw, du0, DU1, du0b, DU1b, l, h);
+              if (KT2_QC == 3) {  // offsets from the record's form centre (exact)
+                const float rdu0 = (float)lx + 0.5f - R.ctr[0];
+                const float2 RDU1 = f2((float)ly + 0.5f - R.ctr[1], (float)ly + 4.5f - R.ctr[1]);
+                opacity2<NV>(R, 0, rdu0, RDU1, rdu0, RDU1, l, h);
+              } else {
+                opacity2<NV>(R, qcw, du0, DU1, du0b, DU1b, l, h);
+              }
               const bool st = flags & F_STRADDLE;
               alo = f2(kA && !st ? l.x : 0.f, kB && !st ? l.y : 0.f);
               ahi = f2(kA ? h.x : 0.f, kB ? h.y : 0.f);
@@ -1640,7 +1674,6 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
   if (w >= n_tiles * nsub) return;
   const int tile = tiles[w / nsub], sub = w % nsub;
   const int pix = threadIdx.x, lx = pix & 7, ly = pix >> 3;
-  const float du0 = (float)lx + 0.5f - 0.5f * SBX, du1 = (float)ly + 0.5f - 0.5f * SBY;
   const int tx = tile % A.ntx, ty = tile / A.ntx;
   const int ox = tx * ts + (sub % nsb) * SBX, oy = ty * ts + (sub / nsb) * SBY;
   const double ucx = ox + 0.5 * SBX, ucy = oy + 0.5 * SBY;
@@ -1690,7 +1723,7 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
           }
         }
       }
-      if (!skip) stage_forms<NV>(S, H, ucx, ucy, part);
+      if (!skip) stage_forms<NV>(S, H, ucx, ucy, 0.5 * SBX, 0.5 * SBY, part);
     }
     __syncthreads();
     for (int j = 0; j < nb; ++j) {
@@ -1706,7 +1739,7 @@ __global__ void __launch_bounds__(64) k_tile_lin(TileArgs A, const int32_t* tile
         ah[NV] = R.o[1];
       } else {
         float sl[C], sh[C];
-        opacity_sforms<NV>(R, du0, du1, sl, sh);
+        opacity_sforms<NV>(R, (float)lx + 0.5f - R.ctr[0], (float)ly + 0.5f - R.ctr[1], sl, sh);
         float smin = sl[NV], smax = sh[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {

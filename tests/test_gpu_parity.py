@@ -57,7 +57,7 @@ def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
     base_lo, base_hi, _ = gpu_render(ctx, w, 16, 64)
     for tile, batch in ((8, 1), (8, 256), (16, 7), (32, 32), (32, 128)):
         lo, hi, _ = gpu_render(ctx, w, tile, batch)
-        # block-centred fp32 forms round differently per block size (TS 8 uses 8x8 blocks,
+        # the fp32 forms round differently per block size (TS 8 uses 8x8 blocks,
         # TS 16 / 32 16x16): measured max 1.1e-5 (C4, TS 8 vs 16) and 2.4e-7 between 16x16
         # layouts (tools/measure_tolerances.py on a B200); twice the measured bound
         tol = 2e-5 if tile == 8 else 1e-6
