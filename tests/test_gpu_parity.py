@@ -58,9 +58,9 @@ def test_tile_and_batch_are_performance_knobs(ctx, oracle, name):
     for tile, batch in ((8, 1), (8, 256), (16, 7), (32, 32), (32, 128)):
         lo, hi, _ = gpu_render(ctx, w, tile, batch)
         # the fp32 forms round differently per block size (TS 8 uses 8x8 blocks,
-        # TS 16 / 32 16x16): measured max 1.1e-5 (C4, TS 8 vs 16) and 2.4e-7 between 16x16
-        # layouts (tools/measure_tolerances.py on a B200); twice the measured bound
-        tol = 2e-5 if tile == 8 else 1e-6
+        # TS 16 / 32 16x16): measured max 3.7e-6 (C4, TS 8 vs 16; 1.1e-5 with block-centred
+        # forms) and 2.4e-7 between 16x16 layouts (tools/measure_tolerances.py on a B200)
+        tol = 1e-5 if tile == 8 else 1e-6
         assert np.abs(lo - base_lo).max() <= tol and np.abs(hi - base_hi).max() <= tol, (tile, batch)
 
 
