@@ -120,6 +120,35 @@ def test_parity_full_sampled(ctx, oracle, name):
     assert np.all(lo <= hi) and lo.min() >= 0 and hi.max() <= 1
 
 
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_parity_full_whole_tiles(ctx, oracle, name):
+    """BASELINE.json full sizes, in the bench's launch configuration, against the oracle on
+    whole tiles (every pixel of each, all sub-boxes): the tiles with the widest GPU bounds and
+    with the most pairs' worth of gap (where the exception windows are), evenly spaced tiles,
+    and the last (ragged) tile.  The oracle renders only these tiles (or_render_tiles)."""
+    w = make_config(name)
+    lo, hi, st = gpu_render(ctx, w)
+    ts = w.tile
+    Wd, Hd = w.camera["W"], w.camera["H"]
+    ntx, nty = -(-Wd // ts), -(-Hd // ts)
+    gap = (hi - lo).sum(-1)
+    pad = np.zeros((nty * ts, ntx * ts))
+    pad[:Hd, :Wd] = gap
+    tsum = pad.reshape(nty, ts, ntx, ts).sum((1, 3)).reshape(-1)
+    tmax = pad.reshape(nty, ts, ntx, ts).max((1, 3)).reshape(-1)
+    tiles = np.unique(np.concatenate([np.argsort(tsum)[-5:], np.argsort(tmax)[-3:],
+                                      np.linspace(0, ntx * nty - 1, 6).round().astype(int),
+                                      [ntx * nty - 1]])).astype(np.int32)
+    olo, ohi, _ = oracle.render_tiles(w, tiles)
+    m = np.zeros((Hd, Wd), bool)
+    for t in tiles:
+        ty, tx = divmod(int(t), ntx)
+        m[ty * ts:(ty + 1) * ts, tx * ts:(tx + 1) * ts] = True
+    err = max(np.abs(lo[m] - olo[m]).max(), np.abs(hi[m] - ohi[m]).max())
+    assert err <= TOL, (name, err, len(tiles))
+    assert m.sum() >= 10 * min(ts * ts, Wd * Hd // (ntx * nty))
+
+
 @pytest.mark.parametrize("name", ["C2", "C4", "C5"])
 def test_gpu_bounds_contain_concrete_renders(ctx, oracle, name):
     """Theorem 1 on the GPU output: concrete renders at sampled box points (GPU concrete

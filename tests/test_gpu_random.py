@@ -84,3 +84,30 @@ def test_block_edge_precision_case(ctx, oracle):
         err = max(np.abs(lo.cpu().numpy() - olo).max(), np.abs(hi.cpu().numpy() - ohi).max())
         assert err <= tol, (ts, err)
         assert st["uncertain_pairs"] == ost["uncertain_pairs"]
+
+
+def test_depth_tie_within_rounding(ctx, oracle):
+    """Reading O21: a sweep case (seed 170189, C5, three sub-boxes) with two
+    Gaussians at the same depth to within an ulp.  The oracle's bounds of d_i - d_j for that pair
+    are +-8.9e-16, so the fp64 evaluation order of the depth forms decides whether the pair is
+    certain or '?': the GPU (FMA contraction, lane-tree sums) finds it uncertain where the oracle
+    does not.  Everything else is equal and the bounds agree within the tolerance."""
+    w, tile, batch = _case(170189)
+    # the near tie exists in the oracle's own forms (every sub-box)
+    for sub in range(3):
+        g = oracle.gaussian_forms(w, sub)
+        n, d = g["n"], g["d"]
+        lA, lb, uA, ub = d[:, :n], d[:, n], d[:, n + 1:2 * n + 1], d[:, 2 * n + 1]
+        i, j = 206, 1524
+        dl = lb[i] - ub[j] - np.abs(lA[i] - uA[j]).sum()
+        du = ub[i] - lb[j] + np.abs(uA[i] - lA[j]).sum()
+        assert abs(dl) < 1e-14 and abs(du) < 1e-14, (sub, dl, du)
+    ctx.load_workload(w)
+    lo, hi, st = ctx.as_render_bounds(tile, batch)
+    olo, ohi, ost = oracle.render_bounds(w, tile=tile)
+    err = max(np.abs(lo.cpu().numpy() - olo).max(), np.abs(hi.cpu().numpy() - ohi).max())
+    assert err <= 1e-4, err
+    for k in ("pairs", "active_pairs", "fails", "dropped", "straddles"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
+    assert 0 <= st["uncertain_pairs"] - ost["uncertain_pairs"] <= 3 * 3, (st["uncertain_pairs"],
+                                                                          ost["uncertain_pairs"])
