@@ -105,7 +105,7 @@ struct alignas(16) FinS {
 // arithmetic, one rounding.  The forms are centred on the block pixel corner nearest the
 // Gaussian's mean (the middle of its mean rectangle, clamped to the block; S.ctr), so the fp32
 // per-pixel offsets du are exact and small where the opacity is large (any centre gives the
-// same forms up to fp32 rounding; the block centre cancels more bits, see KT2_QC).
+// same forms up to fp32 rounding; the block centre cancels more bits).
 // x_a lower form: u_a D2_lo - DU_a,hi = B_lo,a + du_a D2_lo with B_lo,a = uc_a D2_lo - DU_a,hi
 // (u_a > 0 selects D2's lower side, step 14); upper: B_hi,a + du_a D2_hi.
 // LS(x_a, w) = w >= 0 ? w x_lo,a : w x_hi,a  and  US(x_a, w) = w >= 0 ? w x_hi,a : w x_lo,a
@@ -868,36 +868,28 @@ constexpr int P2 = 256;  // pixels per block
 __host__ __device__ __forceinline__ int v2_x(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
 __host__ __device__ __forceinline__ int v2_y(int t) { return (t >> 6) * 8 + ((t >> 3) & 3); }
 
-#ifndef KT2_QC  // where the fp32 forms are centred (default 3)
-// The per-pixel forms are evaluated in fp32 as x = x_b + du D2 and m = p_m + du q_m around a
-// centre; with |du| up to 8 these sums cancel many bits for a small Gaussian far from the
-// centre (the random sweeps' cases above 1e-4, up to 2.4e-4, with the block centre).
-// 3: each record's own centre, the block pixel corner nearest its mean (exact per-record
-//    offsets, ~0.5% of the kernel): the offsets are small where the opacity is large; sweep
-//    median error 3.7e-6 -> 6e-7, no case above 1e-4.
-// 0: the 16x16 block centre; 1: each warp's 8x8 quadrant centre (every centre-dependent term);
-// 2: only the q-form constants (pm, pr) per quadrant, quadrant 0 in A.xy, 1-3 in PQ.
-//    1 and 2 halve the offsets at 7-8% of the kernel (4x the staging / the per-quadrant loads).
-#define KT2_QC 3
-#endif
-constexpr int NQ2 = KT2_QC == 1 ? 4 : 1;   // x_b / A centres
-constexpr int NPQ = KT2_QC == 2 ? 3 : 1;   // extra (pm, pr) quadrants (dummy 1 when unused)
+// Form centres: the per-pixel forms are evaluated in fp32 as x = x_b + du D2 and
+// m = p_m + du q_m around a centre.  Around the 16x16 block centre (|du| up to 8) these sums
+// cancel many bits for a small Gaussian far from it (the random sweeps' cases above 1e-4, up to
+// 2.4e-4).  Each record is therefore centred on the block pixel corner nearest its mean (exact
+// per-record offsets, ~0.5% of the kernel): the offsets are small where the opacity is large
+// (sweep median error 3.7e-6 -> 6e-7, no case above 1e-4).  Measured and dropped: centring on
+// each warp's 8x8 quadrant (every centre-dependent term, or only the q-form constants), 7-8% of
+// the kernel for half the offsets.
 template <int NV>
 struct alignas(16) SRec2 {
   static constexpr int C = NV + 1;
   static constexpr int CP = (C + 3) & ~3;
-  // lower x forms at the form centre qc (the block's, or with KT2_QC the warp's 8x8 quadrant's):
-  // x_lo,a,k(u) = xb_a[qc][k] + du_a d2[k]
-  float xb0[NQ2][CP], xb1[NQ2][CP], d2[CP];
+  // lower x forms at the record's form centre ctr: x_lo,a,k(u) = xb_a[k] + du_a d2[k]
+  float xb0[CP], xb1[CP], d2[CP];
   // q_c's (mid, radius) coefficients as affine functions of (du0, du1, x0, |x0|, x1, |x1|):
   //   m = pm + du0 q0m + du1 q1m + x0 wm0 + x1 wm1,  r = pr + du0 q0r + du1 q1r + |x0| wr0 + |x1| wr1
-  float4 A[NQ2][3][C];  // (pm, pr, q0m, q0r) per quadrant centre (KT2_QC 2: quadrant 0's)
-  float2 PQ[NPQ][3][C];  // KT2_QC 2: (pm, pr) of quadrants 1-3
+  float4 A[3][C];    // (pm, pr, q0m, q0r)
   float4 B[3][C];    // (wm0, wr0, q1m, q1r)
   float2 W1[3][CP];  // (wm1, wr1)
   float4 WC[3];      // concretised W_0c, W_1c as (mid0, half0, mid1, half1)
   float o[2];
-  float ctr[2];      // KT2_QC 3: the form centre (block-local pixels, integer valued)
+  float ctr[2];      // the form centre (block-local pixels, integer valued)
   float clo[3], chi[3];
   int flags;
   int pmf, ph, pg, pnF, pnG;
@@ -920,18 +912,16 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
   constexpr int C = NV + 1;
   constexpr int KP = (C + NPART - 1) / NPART;
   const double uc[2] = {ucx, ucy};
-  // KT2_QC 3: the forms are centred on the block pixel corner nearest the Gaussian's mean
-  // (the middle of its mean rectangle, clamped to the block), so the offsets are small where
-  // the opacity is large; any centre gives the same forms up to fp32 rounding
-  double rc[2] = {0.5 * B2, 0.5 * B2};
-  if (KT2_QC == 3) {
+  // the forms are centred on the block pixel corner nearest the Gaussian's mean (the middle
+  // of its mean rectangle, clamped to the block), so the offsets are small where the opacity
+  // is large; any centre gives the same forms up to fp32 rounding
+  double ctr[2];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-      rc[a] = fmin(fmax(rint(0.5 * (H->mu[a] + H->mu[2 + a]) - (uc[a] - 0.5 * B2)), 0.0), (double)B2);
-    if (part == 0) {
-      S.ctr[0] = (float)rc[0];
-      S.ctr[1] = (float)rc[1];
-    }
+  for (int a = 0; a < 2; ++a) {
+    const double o = uc[a] - 0.5 * B2;
+    const double rc = fmin(fmax(rint(0.5 * (H->mu[a] + H->mu[2 + a]) - o), 0.0), (double)B2);
+    ctr[a] = o + rc;
+    if (part == 0) S.ctr[a] = (float)rc;
   }
   double wl[6], wh[6];
 #pragma unroll
@@ -967,62 +957,42 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
                               (float)(0.5 * (q1lo + q1hi)), (float)(0.5 * (q1hi - q1lo)));
       S.W1[c][k] = make_float2((float)(0.5 * (a1 + b1)), (float)(0.5 * (b1 - a1)));
     }
-    // the centre-dependent terms, per form centre (quadrant centres: offsets of +-4 pixels)
-    constexpr int NC = KT2_QC == 2 ? 4 : NQ2;  // centres computed
+    // the centre-dependent terms
+    double blo[2], bhi[2];
 #pragma unroll
-    for (int qc = 0; qc < NC; ++qc) {
-      const bool quad = KT2_QC == 1 || KT2_QC == 2;
-      const double off[2] = {quad ? ((qc & 1) ? 4.0 : -4.0) : rc[0] - 0.5 * B2,
-                             quad ? ((qc >> 1) ? 4.0 : -4.0) : rc[1] - 0.5 * B2};
-      double blo[2], bhi[2];
+    for (int a = 0; a < 2; ++a) {
+      blo[a] = ctr[a] * d2l - H->du[a][1][k];
+      bhi[a] = ctr[a] * d2h - H->du[a][0][k];
+    }
+    S.xb0[k] = (float)blo[0];
+    S.xb1[k] = (float)blo[1];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        blo[a] = (uc[a] + off[a]) * d2l - H->du[a][1][k];
-        bhi[a] = (uc[a] + off[a]) * d2h - H->du[a][0][k];
-      }
-      if (KT2_QC != 2) {
-        S.xb0[qc][k] = (float)blo[0];
-        S.xb1[qc][k] = (float)blo[1];
-      } else if (qc == 0) {  // x_b at the block centre
-        S.xb0[0][k] = (float)(uc[0] * d2l - H->du[0][1][k]);
-        S.xb1[0][k] = (float)(uc[1] * d2l - H->du[1][1][k]);
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
-        const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
-        const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
-        const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q0hi = w0h * (w0h >= 0 ? d2h : d2l);
-        if (KT2_QC == 2 && qc > 0) {
-          S.PQ[qc - 1][c][k] = make_float2((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)));
-        } else {
-          S.A[KT2_QC == 2 ? 0 : qc][c][k] =
-              make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
-                          (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
-        }
-      }
+    for (int c = 0; c < 3; ++c) {
+      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+      const double plo = w0l * (w0l >= 0 ? blo[0] : bhi[0]) + w1l * (w1l >= 0 ? blo[1] : bhi[1]);
+      const double phi = w0h * (w0h >= 0 ? bhi[0] : blo[0]) + w1h * (w1h >= 0 ? bhi[1] : blo[1]);
+      const double q0lo = w0l * (w0l >= 0 ? d2l : d2h), q0hi = w0h * (w0h >= 0 ? d2h : d2l);
+      S.A[c][k] = make_float4((float)(0.5 * (plo + phi)), (float)(0.5 * (phi - plo)),
+                              (float)(0.5 * (q0lo + q0hi)), (float)(0.5 * (q0hi - q0lo)));
     }
   }
 }
 
-// steps 14-17 for the thread's two pixels (du0 shared; DU1 = (du1 of pixel 0, of pixel 1)):
-// returns (a_lo, a_hi) pairs.  Same per-pixel operations as s_forms / opacity.
+// steps 14-17 for the thread's two pixels at offsets (du0, DU1) from the record's form centre
+// (du0 shared; DU1 = (du1 of pixel 0, of pixel 1)): returns (a_lo, a_hi) pairs.  Same
+// per-pixel operations as s_forms / opacity.
 template <int NV>
-__device__ __forceinline__ void opacity2(const SRec2<NV>& R, int qc, float du0, float2 DU1,
-                                         float du0b, float2 DU1b, float2& alo, float2& ahi) {
+__device__ __forceinline__ void opacity2(const SRec2<NV>& R, float du0, float2 DU1, float2& alo,
+                                         float2& ahi) {
   constexpr int C = NV + 1;
-  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel), around the
-  // x_b centre (the quadrant's with KT2_QC 1, else the block's: du0b / DU1b)
-  const int qx = KT2_QC == 1 ? qc : 0;
-  const float dx0 = KT2_QC == 1 ? du0 : du0b;
-  const float2 DX1 = KT2_QC == 1 ? DU1 : DU1b;
-  float x0 = fmaf(dx0, R.d2[NV], R.xb0[qx][NV]);
+  // 14: concretised lower bounds of x_0 (shared by the column) and x_1 (per pixel)
+  float x0 = fmaf(du0, R.d2[NV], R.xb0[NV]);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(dx0, R.d2[k], R.xb0[qx][k]));
-  float2 X1 = __ffma2_rn(DX1, bc(R.d2[NV]), bc(R.xb1[qx][NV]));
+  for (int k = 0; k < NV; ++k) x0 -= fabsf(fmaf(du0, R.d2[k], R.xb0[k]));
+  float2 X1 = __ffma2_rn(DU1, bc(R.d2[NV]), bc(R.xb1[NV]));
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const float2 v = __ffma2_rn(DX1, bc(R.d2[k]), bc(R.xb1[qx][k]));
+    const float2 v = __ffma2_rn(DU1, bc(R.d2[k]), bc(R.xb1[k]));
     X1 = __fadd2_rn(X1, f2(-fabsf(v.x), -fabsf(v.y)));
   }
   const float2 AX1 = f2(fabsf(X1.x), fabsf(X1.y));
@@ -1037,13 +1007,8 @@ __device__ __forceinline__ void opacity2(const SRec2<NV>& R, int qc, float du0, 
     const float4 wc = R.WC[c];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      float4 a = R.A[KT2_QC == 1 ? qc : 0][c][k];
+      const float4 a = R.A[c][k];
       const float4 b = R.B[c][k];
-      if (KT2_QC == 2 && qc > 0) {  // this quadrant's q-form constants
-        const float2 pq = R.PQ[qc - 1][c][k];
-        a.x = pq.x;
-        a.y = pq.y;
-      }
       const float2 w1 = R.W1[c][k];
       float2 mr = __ffma2_rn(D0, f2(a.z, a.w), f2(a.x, a.y));
       mr = __ffma2_rn(X0, f2(b.x, b.y), mr);
@@ -1194,15 +1159,9 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
   __syncthreads();
   unsigned phase = 0;
   const int lx = v2_x(tid), ly = v2_y(tid);
-  // the warp's form centre: its 8x8 quadrant's centre (KT2_QC) or the block's
-  constexpr bool QW = KT2_QC == 1 || KT2_QC == 2;
-  const int qcw = QW ? (tid >> 5) : 0;
-  const float cxq = QW ? (float)(((qcw & 1) ? 12 : 4)) : 0.5f * B2;
-  const float cyq = QW ? (float)(((qcw >> 1) ? 12 : 4)) : 0.5f * B2;
-  const float du0 = (float)lx + 0.5f - cxq;
-  const float2 DU1 = f2((float)ly + 0.5f - cyq, (float)ly + 4.5f - cyq);
-  const float du0b = (float)lx + 0.5f - 0.5f * B2;  // relative to the block centre
-  const float2 DU1b = f2((float)ly + 0.5f - 0.5f * B2, (float)ly + 4.5f - 0.5f * B2);
+  // pixel centres in the block (minus each record's form centre in the walk)
+  const float lxh = (float)lx + 0.5f;
+  const float2 LYH = f2((float)ly + 0.5f, (float)ly + 4.5f);
   unsigned active = 0;
   const int nwork = A.n_items * nsub;
 #ifdef KT2_PROF
@@ -1465,13 +1424,8 @@ __global__ void __launch_bounds__(T2, KT2_MINB) k_tile2(TileArgs A) {
               ahi = f2(kA ? R.o[1] : 0.f, kB ? R.o[1] : 0.f);
             } else {
               float2 l, h;
-              if (KT2_QC == 3) {  // offsets from the record's form centre (exact)
-                const float rdu0 = (float)lx + 0.5f - R.ctr[0];
-                const float2 RDU1 = f2((float)ly + 0.5f - R.ctr[1], (float)ly + 4.5f - R.ctr[1]);
-                opacity2<NV>(R, 0, rdu0, RDU1, rdu0, RDU1, l, h);
-              } else {
-                opacity2<NV>(R, qcw, du0, DU1, du0b, DU1b, l, h);
-              }
+              // offsets from the record's form centre (exact)
+              opacity2<NV>(R, lxh - R.ctr[0], f2(LYH.x - R.ctr[1], LYH.y - R.ctr[1]), l, h);
               const bool st = flags & F_STRADDLE;
               alo = f2(kA && !st ? l.x : 0.f, kB && !st ? l.y : 0.f);
               ahi = f2(kA ? h.x : 0.f, kB ? h.y : 0.f);

@@ -74,7 +74,7 @@ def test_block_edge_precision_case(ctx, oracle):
     """The one case of a 2000-case sweep above 1e-4 with block-centred fp32 forms
     (profiles/r02_parity_sweep.md): cancellation in x = x_b + du D2 and m = p_m + du q_m for a
     small Gaussian near a block edge (1.8e-4 at TS 16 / 32).  With the forms centred on each
-    record's own centre (the pixel corner nearest its mean, k_tile.cu stage_forms / KT2_QC 3)
+    record's own centre (the pixel corner nearest its mean, k_tile.cu stage_forms / stage_forms2)
     it is within 1e-4 at every tile size."""
     w, tile, batch = _case(5906)
     ctx.load_workload(w)
