@@ -950,7 +950,7 @@ __device__ __forceinline__ void stage_forms2(SRec2<NV>& S, const HotRec<NV>* H, 
     S.d2[k] = (float)d2l;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double w0l = wl[c], w0h = wh[c], w1l = wl[3 + c], w1h = wh[3 + c];
+      const double w1l = wl[3 + c], w1h = wh[3 + c];
       const double a0 = wa[c], b0 = wb[c], a1 = wa[3 + c], b1 = wb[3 + c];
       const double q1lo = w1l * (w1l >= 0 ? d2l : d2h), q1hi = w1h * (w1h >= 0 ? d2h : d2l);
       S.B[c][k] = make_float4((float)(0.5 * (a0 + b0)), (float)(0.5 * (b0 - a0)),
